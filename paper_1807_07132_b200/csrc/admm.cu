@@ -1,0 +1,511 @@
+// Consensus ADMM over device-resident shards (run_admm, inc/admm.hpp:17-140).
+//
+// One rank per GPU. Each rank owns `n_local` ADMM workers (shards). Per outer iteration:
+//   1. every local worker runs the run_worker ADMM branch (src/worker.cpp:168-196) on device;
+//   2. the consensus sum S = sum_i (rho_i x_i - y_i) | sum_i rho_i is formed per rank in ascending
+//      worker order and combined with ONE ncclAllReduce (the reference's gather + z_update);
+//   3. every rank forms the identical z = S / (lambda + sum rho), updates its own y_i and y_hat_i,
+//      and computes residual / tolerance partials; per-rank scalars travel in one small
+//      ncclAllGather and are combined on every host in rank order;
+//   4. spectral penalty selection runs per worker on local data only.
+// The reference's scatter/gather frames (inc/comm.hpp) disappear: z is formed redundantly on every
+// GPU, y_i and rho_i never leave their GPU.
+#include <nccl.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "solver.h"
+#include "solver_kernels.h"
+
+using namespace nadmm;
+
+struct nadmm_comm_s {
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    Ctx* ctx = nullptr;
+};
+
+namespace nadmm {
+namespace {
+
+thread_local std::string* g_err_sink = nullptr;
+
+#define NADMM_NCCL(call)                                                                              \
+    do {                                                                                              \
+        ncclResult_t r__ = (call);                                                                    \
+        if (r__ != ncclSuccess) ::nadmm::raise(NADMM_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r__)); \
+    } while (0)
+
+constexpr int kMaxLocal = 16;
+
+struct LocalPtrs {
+    const double* x[kMaxLocal];
+    const double* y[kMaxLocal];
+    double rho[kMaxLocal];
+    int n;
+};
+
+#define GRID_STRIDE(j, d) \
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < (d); j += (int64_t)gridDim.x * blockDim.x)
+
+// S_local = sum_i (rho_i x_i - y_i), ascending local worker id.
+__global__ void k_local_sum(int64_t d, LocalPtrs lp, double rho_sum, double* __restrict__ buf) {
+    GRID_STRIDE(j, d) {
+        double s = lp.rho[0] * lp.x[0][j] - lp.y[0][j];
+        for (int i = 1; i < lp.n; ++i) s += lp.rho[i] * lp.x[i][j] - lp.y[i][j];
+        buf[j] = s;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) buf[d] = rho_sum;
+}
+
+// z_update: z = S / (lambda + sum rho); prev_z kept; partials |z|^2.
+__global__ void k_z_update(int64_t d, const double* __restrict__ buf, double lambda, double* __restrict__ z,
+                           double* __restrict__ pz, double* part) {
+    __shared__ double red[32];
+    const double denom = lambda + buf[d];
+    double zz = 0.0;
+    GRID_STRIDE(j, d) {
+        pz[j] = z[j];
+        const double v = buf[j] / denom;
+        z[j] = v;
+        zz += v * v;
+    }
+    const double t = block_sum(zz, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+// Per worker: y_hat = y + rho (z_prev - x); y += rho (z - x); partials
+// of |z - x|^2 (primal), |rho (z - z_prev)|^2 (dual), |x|^2 and |y_new|^2 (tolerances).
+__global__ void k_worker_update(int64_t d, double rho, const double* __restrict__ x, double* __restrict__ y,
+                                double* __restrict__ yh, const double* __restrict__ z, const double* __restrict__ pz,
+                                double* part /* 4 x kBlockPartials */) {
+    __shared__ double red[32];
+    double pr = 0.0, du = 0.0, xx = 0.0, yy = 0.0;
+    GRID_STRIDE(j, d) {
+        const double xj = x[j], yj = y[j];
+        if (yh) yh[j] = yj + rho * (pz[j] - xj);
+        const double yn = yj + rho * (z[j] - xj);
+        y[j] = yn;
+        const double r = z[j] - xj;
+        const double q = rho * (z[j] - pz[j]);
+        pr += r * r;
+        du += q * q;
+        xx += xj * xj;
+        yy += yn * yn;
+    }
+    double t = block_sum(pr, red);
+    if (threadIdx.x == 0) part[0 * kBlockPartials + blockIdx.x] = t;
+    t = block_sum(du, red);
+    if (threadIdx.x == 0) part[1 * kBlockPartials + blockIdx.x] = t;
+    t = block_sum(xx, red);
+    if (threadIdx.x == 0) part[2 * kBlockPartials + blockIdx.x] = t;
+    t = block_sum(yy, red);
+    if (threadIdx.x == 0) part[3 * kBlockPartials + blockIdx.x] = t;
+}
+
+// Secant dots for the spectral update: <dx,dyh>, |dx|^2, |dyh|^2, <dz,-dy>, |dz|^2, |dy|^2.
+__global__ void k_sps_dots(int64_t d, const double* __restrict__ x, const double* __restrict__ xs,
+                           const double* __restrict__ yh, const double* __restrict__ yhs, const double* __restrict__ z,
+                           const double* __restrict__ zs, const double* __restrict__ y, const double* __restrict__ ys,
+                           double* part /* 6 x kBlockPartials */) {
+    __shared__ double red[32];
+    double a[6] = {0, 0, 0, 0, 0, 0};
+    GRID_STRIDE(j, d) {
+        const double dx = x[j] - xs[j], dyh = yh[j] - yhs[j], dz = z[j] - zs[j], dy = -(y[j] - ys[j]);
+        a[0] += dx * dyh;
+        a[1] += dx * dx;
+        a[2] += dyh * dyh;
+        a[3] += dz * dy;
+        a[4] += dz * dz;
+        a[5] += dy * dy;
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        const double t = block_sum(a[q], red);
+        if (threadIdx.x == 0) part[q * kBlockPartials + blockIdx.x] = t;
+    }
+}
+
+// Reduce `count` groups of `n` partials (group stride kBlockPartials) into out[count].
+__global__ void k_reduce_groups(const double* part, int n, int count, double* out) {
+    const int g = blockIdx.x;
+    if (g >= count || threadIdx.x >= 32) return;
+    const double v = reduce_partials(part + (int64_t)g * kBlockPartials, n);
+    if (threadIdx.x == 0) out[g] = v;
+}
+
+// Hybrid spectral step of one side (same arithmetic as the oracle's spectral_side).
+bool spectral_side(double ab, double aa, double bb, double eps_cor, double* est) {
+    if (!(aa > 0.0) || !(bb > 0.0) || !(ab > 0.0)) return false;
+    const double cor = ab / (std::sqrt(aa) * std::sqrt(bb));
+    if (!(cor > eps_cor)) return false;
+    const double sd = bb / ab, mg = ab / aa;
+    *est = (2.0 * mg > sd) ? mg : sd - mg / 2.0;
+    return true;
+}
+
+template <typename T>
+T* dalloc(int64_t n) {
+    T* p = nullptr;
+    NADMM_CUDA(cudaMalloc(&p, sizeof(T) * (size_t)std::max<int64_t>(n, 1)));
+    NADMM_CUDA(cudaMemset(p, 0, sizeof(T) * (size_t)std::max<int64_t>(n, 1)));
+    return p;
+}
+
+struct RunBuffers {
+    std::vector<void*> owned;
+    template <typename T>
+    T* get(int64_t n) {
+        T* p = dalloc<T>(n);
+        owned.push_back(p);
+        return p;
+    }
+    ~RunBuffers() {
+        for (void* p : owned) cudaFree(p);
+    }
+};
+
+}  // namespace
+}  // namespace nadmm
+
+extern "C" {
+
+void nadmm_admm_cfg_default(nadmm_admm_cfg* c) {  // inc/admm.hpp:37-56, 107-117
+    std::memset(c, 0, sizeof *c);
+    c->lambda = 1e-5;
+    c->penalty_kind = 0;
+    c->rho0 = 1.0;
+    c->update_period = 2;
+    c->eps_cor = 0.2;
+    c->rho_min = 1e-6;
+    c->rho_max = 1e6;
+    c->eps_abs = 1e-3;
+    c->eps_rel = 1e-3;
+    c->max_outer_iters = 300;
+    c->standard_norms = 0;
+    c->inner_iters = 1;
+    nadmm_newton_cfg_default(&c->newton);
+    c->eval_objective = 0;
+    c->f_star = 0.0;
+    c->theta_stop = 0.0;
+}
+
+extern const char* nadmm_last_error(void);
+
+nadmm_status nadmm_comm_unique_id(uint8_t id_out[128]) {
+    try {
+        ncclUniqueId id;
+        NADMM_NCCL(ncclGetUniqueId(&id));
+        std::memcpy(id_out, id.internal, 128);
+        return NADMM_OK;
+    } catch (const Error& e) {
+        return e.code;
+    }
+}
+
+nadmm_status nadmm_comm_create(nadmm_ctx ctx, const uint8_t id[128], int32_t nranks, int32_t rank, nadmm_comm* out) {
+    try {
+        if (!ctx || !out) raise(NADMM_ECONFIG, "null argument");
+        if (nranks < 1 || rank < 0 || rank >= nranks) raise(NADMM_ECONFIG, "bad rank/nranks");
+        NADMM_CUDA(cudaSetDevice(ctx->device));
+        ncclUniqueId uid;
+        std::memcpy(uid.internal, id, 128);
+        auto* c = new nadmm_comm_s();
+        c->nranks = nranks;
+        c->rank = rank;
+        c->ctx = ctx;
+        ncclResult_t r = ncclCommInitRank(&c->comm, nranks, uid, rank);
+        if (r != ncclSuccess) {
+            delete c;
+            raise(NADMM_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        }
+        *out = c;
+        return NADMM_OK;
+    } catch (const Error& e) {
+        return e.code;
+    }
+}
+
+nadmm_status nadmm_comm_destroy(nadmm_comm c) {
+    if (!c) return NADMM_OK;
+    if (c->comm) ncclCommDestroy(c->comm);
+    delete c;
+    return NADMM_OK;
+}
+
+}  // extern "C"
+
+namespace nadmm {
+void set_last_error(const std::string& m);
+}
+
+extern "C" nadmm_status nadmm_admm_run(const nadmm_shard* shards, int32_t n_local, nadmm_comm comm,
+                                       const nadmm_admm_cfg* cfg_in, double* z_out, double* rho_out,
+                                       nadmm_metrics_row* rows, int32_t row_cap, int32_t* iterations,
+                                       int32_t* converged_out) {
+    try {
+        if (!shards || n_local < 1 || n_local > kMaxLocal) raise(NADMM_ECONFIG, "need 1..16 local shards");
+        nadmm_admm_cfg cfg;
+        if (cfg_in)
+            cfg = *cfg_in;
+        else
+            nadmm_admm_cfg_default(&cfg);
+        if (cfg.rho0 <= 0.0) raise(NADMM_ECONFIG, "rho0 must be > 0");
+        if (cfg.penalty_kind == 1 &&
+            (cfg.update_period < 1 || !(cfg.eps_cor > 0.0 && cfg.eps_cor < 1.0) || !(cfg.rho_min > 0.0) ||
+             cfg.rho_max < cfg.rho_min))
+            raise(NADMM_ECONFIG, "bad spectral penalty policy");  // PenaltyPolicy::validate (inc/admm.hpp:37-47)
+        if (cfg.inner_iters < 0) raise(NADMM_ECONFIG, "inner_iters must be >= 0");
+        nadmm_newton_cfg ncfg = cfg.newton;
+        ncfg.newton_max_iters = cfg.inner_iters;
+        validate_newton_cfg(ncfg);
+        Ctx* ctx = shards[0]->ctx;
+        const int64_t d = shards[0]->d;
+        for (int i = 0; i < n_local; ++i) {
+            if (!shards[i]) raise(NADMM_ECONFIG, "null shard");
+            if (shards[i]->ctx != ctx) raise(NADMM_ECONFIG, "all local shards must share one context");
+            if (shards[i]->d != d) raise(NADMM_ECONFIG, "shard weight dimensions differ");
+        }
+        if (comm && comm->ctx->device != ctx->device) raise(NADMM_ECONFIG, "communicator bound to another device");
+        NADMM_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t st = ctx->stream;
+        const int nranks = comm ? comm->nranks : 1, rank = comm ? comm->rank : 0;
+
+        // global worker count (workers are concatenated in rank order)
+        RunBuffers rb;
+        int n_total = n_local;
+        if (comm) {
+            int* cnt = rb.get<int>(nranks);
+            NADMM_CUDA(cudaMemcpyAsync(cnt + rank, &n_local, sizeof(int), cudaMemcpyHostToDevice, st));
+            NADMM_NCCL(ncclAllGather(cnt + rank, cnt, 1, ncclInt, comm->comm, st));
+            std::vector<int> h(nranks);
+            NADMM_CUDA(cudaMemcpyAsync(h.data(), cnt, sizeof(int) * nranks, cudaMemcpyDeviceToHost, st));
+            NADMM_CUDA(cudaStreamSynchronize(st));
+            n_total = 0;
+            for (int v : h) n_total += v;
+        }
+
+        const bool sps = cfg.penalty_kind == 1;
+        double* buf = rb.get<double>(d + 1);
+        double* z = rb.get<double>(d);
+        double* pz = rb.get<double>(d);
+        double* zs = sps ? rb.get<double>(d) : nullptr;
+        const int vg = vec_grid(*ctx, d);
+        double* zpart = rb.get<double>(kBlockPartials);
+        double* wpart = rb.get<double>((int64_t)n_local * 6 * kBlockPartials);
+        constexpr int kStats = 8;
+        double* wred = rb.get<double>((int64_t)n_local * 6 + 2);
+        double* fz = rb.get<double>(n_local);
+        double* rstat = rb.get<double>(kStats);
+        double* gstat = rb.get<double>((int64_t)kStats * nranks);
+        std::vector<double*> yh(n_local, nullptr), xs(n_local, nullptr), ys(n_local, nullptr), yhs(n_local, nullptr);
+        for (int i = 0; i < n_local; ++i) {
+            if (sps) {
+                yh[i] = rb.get<double>(d);
+                xs[i] = rb.get<double>(d);
+                ys[i] = rb.get<double>(d);
+                yhs[i] = rb.get<double>(d);
+            }
+            // AdmmState::initial: x_local = 0, y_i = 0 (src/worker.cpp:135)
+            Shard& s = *shards[i];
+            NADMM_CUDA(cudaMemsetAsync(s.x, 0, sizeof(double) * d, st));
+            NADMM_CUDA(cudaMemsetAsync(s.y, 0, sizeof(double) * d, st));
+            if (s.cache_at == Shard::kAtX) s.cache_at = Shard::kNone;
+        }
+        std::vector<double> rho(n_local, cfg.rho0);
+        std::vector<double> hstat((size_t)kStats * nranks);
+        std::vector<double> hred((size_t)n_local * 6 + 2);
+
+        cudaEvent_t ev_start, ev_now;
+        NADMM_CUDA(cudaEventCreate(&ev_start));
+        NADMM_CUDA(cudaEventCreate(&ev_now));
+        NADMM_CUDA(cudaEventRecord(ev_start, st));
+        int k = 0, snap_it = 0;
+        bool conv = false;
+        for (int it = 0; it < cfg.max_outer_iters; ++it) {
+            // (1) scatter z / solve / gather, one worker at a time on this GPU
+            int inner = 0, cg_sum = 0, fe_sum = 0, flags = 0;
+            for (int i = 0; i < n_local; ++i) {
+                Shard& s = *shards[i];
+                NADMM_CUDA(cudaMemcpyAsync(s.z, z, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+                SolveResult r = device_newton_solve(s, ncfg, 0.0, true, rho[i], cfg.inner_iters);
+                if (r.error) raise((nadmm_status)r.error, "worker inner solve failed");
+                inner += r.iterations;
+                cg_sum += r.cg_sum;
+                fe_sum += r.fe_sum;
+                flags |= r.flags;
+            }
+            // (2) consensus sum + one allreduce
+            LocalPtrs lp{};
+            lp.n = n_local;
+            double rho_sum = 0.0;
+            for (int i = 0; i < n_local; ++i) {
+                lp.x[i] = shards[i]->x;
+                lp.y[i] = shards[i]->y;
+                lp.rho[i] = rho[i];
+                rho_sum += rho[i];
+            }
+            k_local_sum<<<vg, 256, 0, st>>>(d, lp, rho_sum, buf);
+            NADMM_LAUNCH_CHECK();
+            ctx->stats.kernel_launches++;
+            if (comm) NADMM_NCCL(ncclAllReduce(buf, buf, d + 1, ncclDouble, ncclSum, comm->comm, st));
+            // (3) z, y, y_hat, residual partials
+            k_z_update<<<vg, 256, 0, st>>>(d, buf, cfg.lambda, z, pz, zpart);
+            NADMM_LAUNCH_CHECK();
+            ctx->stats.kernel_launches++;
+            for (int i = 0; i < n_local; ++i) {
+                Shard& s = *shards[i];
+                k_worker_update<<<vg, 256, 0, st>>>(d, rho[i], s.x, s.y, sps ? yh[i] : nullptr, z, pz,
+                                                    wpart + (int64_t)i * 6 * kBlockPartials);
+                NADMM_LAUNCH_CHECK();
+                ctx->stats.kernel_launches++;
+            }
+            ++k;
+            // local F_i(z) (global objective of Eq. (5)) for the metrics stream
+            if (cfg.eval_objective) {
+                for (int i = 0; i < n_local; ++i) {
+                    Shard& s = *shards[i];
+                    op_value(s, z, fz + i, 0, nullptr);
+                }
+            }
+            // per-worker partial groups -> scalars
+            for (int i = 0; i < n_local; ++i) {
+                k_reduce_groups<<<4, 32, 0, st>>>(wpart + (int64_t)i * 6 * kBlockPartials, vg, 4, wred + (int64_t)i * 6);
+                ctx->stats.kernel_launches++;
+            }
+            k_reduce_groups<<<1, 32, 0, st>>>(zpart, vg, 1, wred + (int64_t)n_local * 6);
+            ctx->stats.kernel_launches++;
+            NADMM_LAUNCH_CHECK();
+            std::vector<double> hfz(n_local, 0.0);
+            NADMM_CUDA(cudaMemcpyAsync(hred.data(), wred, sizeof(double) * hred.size(), cudaMemcpyDeviceToHost, st));
+            if (cfg.eval_objective)
+                NADMM_CUDA(cudaMemcpyAsync(hfz.data(), fz, sizeof(double) * n_local, cudaMemcpyDeviceToHost, st));
+            NADMM_CUDA(cudaStreamSynchronize(st));
+            // rank scalars: sum|x_i|^2, max|y_i|^2, max primal_i, max dual_i, sum primal^2, sum dual^2, sum F_i
+            double rs[kStats] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int i = 0; i < n_local; ++i) {
+                const double* w = hred.data() + (int64_t)i * 6;
+                const double prim = std::sqrt(w[0]), dual = std::sqrt(w[1]);
+                rs[0] += w[2];
+                rs[1] = std::max(rs[1], w[3]);
+                rs[2] = std::max(rs[2], prim);
+                rs[3] = std::max(rs[3], dual);
+                rs[4] += w[0];
+                rs[5] += w[1];
+                rs[6] += hfz[i];
+                if (std::isnan(prim) || std::isnan(dual)) rs[2] = NAN;
+            }
+            rs[7] = hred[(size_t)n_local * 6];  // |z|^2
+            if (comm) {
+                NADMM_CUDA(cudaMemcpyAsync(rstat, rs, sizeof rs, cudaMemcpyHostToDevice, st));
+                NADMM_NCCL(ncclAllGather(rstat, gstat, kStats, ncclDouble, comm->comm, st));
+                NADMM_CUDA(cudaMemcpyAsync(hstat.data(), gstat, sizeof(double) * hstat.size(), cudaMemcpyDeviceToHost, st));
+                NADMM_CUDA(cudaStreamSynchronize(st));
+            } else {
+                std::memcpy(hstat.data(), rs, sizeof rs);
+            }
+            double sx = 0.0, ymax = 0.0, pmax = 0.0, dmax = 0.0, psq = 0.0, dsq = 0.0, F = 0.0;
+            for (int r = 0; r < nranks; ++r) {  // rank order: deterministic combination
+                const double* h = hstat.data() + (size_t)r * kStats;
+                sx += h[0];
+                ymax = std::max(ymax, h[1]);
+                pmax = std::max(pmax, h[2]);
+                dmax = std::max(dmax, h[3]);
+                psq += h[4];
+                dsq += h[5];
+                F += h[6];
+                if (std::isnan(h[2])) pmax = NAN;
+            }
+            const double zz = hstat[7];
+            // tolerances, squared norms unless standard_norms
+            double a = sx, b = n_total * zz, c = ymax;
+            if (cfg.standard_norms) {
+                a = std::sqrt(sx);
+                b = std::sqrt((double)n_total) * std::sqrt(zz);
+                c = std::sqrt(ymax);
+            }
+            const double eps_pri = std::sqrt((double)n_total) * cfg.eps_abs + cfg.eps_rel * std::max(a, b);
+            const double eps_dual = std::sqrt((double)d) * cfg.eps_abs + cfg.eps_rel * c;
+            conv = k >= 1 && pmax <= eps_pri && dmax <= eps_dual;  // has_converged
+            // (4) spectral penalty selection every T_f iterations against the last snapshot
+            if (sps && k - snap_it >= cfg.update_period) {
+                for (int i = 0; i < n_local; ++i) {
+                    Shard& s = *shards[i];
+                    double* part = wpart + (int64_t)i * 6 * kBlockPartials;
+                    k_sps_dots<<<vg, 256, 0, st>>>(d, s.x, xs[i], yh[i], yhs[i], z, zs, s.y, ys[i], part);
+                    k_reduce_groups<<<6, 32, 0, st>>>(part, vg, 6, wred + (int64_t)i * 6);
+                    ctx->stats.kernel_launches += 2;
+                }
+                NADMM_LAUNCH_CHECK();
+                NADMM_CUDA(cudaMemcpyAsync(hred.data(), wred, sizeof(double) * n_local * 6, cudaMemcpyDeviceToHost, st));
+                NADMM_CUDA(cudaStreamSynchronize(st));
+                for (int i = 0; i < n_local; ++i) {
+                    const double* w = hred.data() + (int64_t)i * 6;
+                    double ah = 0.0, bh = 0.0;
+                    const bool xo = spectral_side(w[0], w[1], w[2], cfg.eps_cor, &ah);
+                    const bool zo = spectral_side(w[3], w[4], w[5], cfg.eps_cor, &bh);
+                    double r = rho[i];
+                    if (xo && zo)
+                        r = std::sqrt(ah * bh);
+                    else if (xo)
+                        r = std::sqrt(ah);
+                    else if (zo)
+                        r = std::sqrt(bh);
+                    rho[i] = std::min(std::max(r, cfg.rho_min), cfg.rho_max);
+                    Shard& s = *shards[i];
+                    NADMM_CUDA(cudaMemcpyAsync(xs[i], s.x, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+                    NADMM_CUDA(cudaMemcpyAsync(ys[i], s.y, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+                    NADMM_CUDA(cudaMemcpyAsync(yhs[i], yh[i], sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+                }
+                NADMM_CUDA(cudaMemcpyAsync(zs, z, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+                snap_it = k;
+            }
+            NADMM_CUDA(cudaEventRecord(ev_now, st));
+            NADMM_CUDA(cudaEventSynchronize(ev_now));
+            float ms = 0.f;
+            NADMM_CUDA(cudaEventElapsedTime(&ms, ev_start, ev_now));
+            double theta = NAN;
+            const double Fz = cfg.eval_objective ? F + 0.5 * cfg.lambda * zz : NAN;
+            if (cfg.eval_objective && cfg.f_star > 0.0) theta = (Fz - cfg.f_star) / cfg.f_star;
+            if (rows && it < row_cap) {
+                nadmm_metrics_row& m = rows[it];
+                m.iteration = k;
+                m.wall_seconds = ms * 1e-3;
+                m.train_objective = Fz;
+                m.theta = theta;
+                m.primal_norm = std::sqrt(psq);
+                m.dual_norm = std::sqrt(dsq);
+                m.eps_pri = eps_pri;
+                m.eps_dual = eps_dual;
+                m.inner_iterations = inner;
+                m.cg_iters = cg_sum;
+                m.fn_evals = fe_sum;
+                m.flags = flags;
+                double rsum = 0.0;
+                for (double v : rho) rsum += v;
+                m.rho_mean = rsum / n_local;
+                m.messages = 2LL * n_total * k;
+            }
+            if (conv) break;
+            if (cfg.theta_stop > 0.0 && !std::isnan(theta) && theta <= cfg.theta_stop) break;
+        }
+        cudaEventDestroy(ev_start);
+        cudaEventDestroy(ev_now);
+        if (z_out) {
+            NADMM_CUDA(cudaMemcpyAsync(z_out, z, sizeof(double) * d, cudaMemcpyDeviceToHost, st));
+        }
+        NADMM_CUDA(cudaStreamSynchronize(st));
+        if (rho_out)
+            for (int i = 0; i < n_local; ++i) rho_out[i] = rho[i];
+        if (iterations) *iterations = k;
+        if (converged_out) *converged_out = conv ? 1 : 0;
+        return NADMM_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    }
+}

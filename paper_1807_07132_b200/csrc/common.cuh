@@ -1,0 +1,78 @@
+// Shared device/host helpers for the Newton-ADMM sm_100a library.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/nadmm_cuda.h"
+
+namespace nadmm {
+
+// Internal error carrying an nadmm_status; converted to a return code at the C ABI.
+struct Error : std::runtime_error {
+    nadmm_status code;
+    Error(nadmm_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void raise(nadmm_status c, const std::string& m) { throw Error(c, m); }
+
+#define NADMM_CUDA(call)                                                                               \
+    do {                                                                                               \
+        cudaError_t e__ = (call);                                                                      \
+        if (e__ != cudaSuccess)                                                                        \
+            ::nadmm::raise(NADMM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__) + " @" + \
+                                            __FILE__ + ":" + std::to_string(__LINE__));                \
+    } while (0)
+
+#define NADMM_LAUNCH_CHECK() NADMM_CUDA(cudaGetLastError())
+
+constexpr int kMaxClasses = 128;   // C - 1 <= kMaxClasses on the SIMT paths
+constexpr int kBlockPartials = 1024;  // max blocks writing partials in one reduction slot
+
+// ---------------------------------------------------------------------------------------------
+// Deterministic reductions. Every block writes one partial per slot; consumers reduce the partials
+// with reduce_partials() executed by one full warp: lane l sums parts[l], parts[l+32], ... in
+// ascending order, then a fixed xor-butterfly combines the lanes. Results are bit-identical across
+// runs and across the blocks that redundantly evaluate them.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide sum in fixed order; result valid in thread 0. `scratch` holds >= 32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (warp == 0) {
+        r = lane < nw ? scratch[lane] : 0.0;
+        r = warp_sum(r);
+    }
+    return r;
+}
+
+// Must be called by all 32 lanes of a warp.
+__device__ __forceinline__ double reduce_partials(const double* parts, int n) {
+    const int lane = threadIdx.x & 31;
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) s += parts[i];
+    return warp_sum(s);
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace nadmm

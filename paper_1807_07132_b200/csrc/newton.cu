@@ -1,0 +1,204 @@
+// Composite data-pass ops and the device-resident inexact Newton-CG driver.
+//
+// newton_solve (src/newton.cpp:73-132) runs entirely on the device: one CUDA graph per Newton
+// iteration (CG with device-side stop flags, certificate Hv, fallbacks, batched Armijo search,
+// step, fused cache+gradient pass at the new point), replayed per iteration. The host synchronises
+// once per Newton iteration (once per outer ADMM iteration with inner_iters = 1).
+#include <cstring>
+
+#include "solver.h"
+#include "solver_kernels.h"
+
+namespace nadmm {
+
+// ---------------------------------------------------------------------------------------------
+// Composite ops (one or two data passes each)
+// ---------------------------------------------------------------------------------------------
+void op_cache_grad(Shard& s, const double* w, const int32_t* guard) {
+    if (dmma_supported(s)) {
+        dmma_pass(s, kModeCache, w, guard);
+        finalize_partials(s, s.part_chunks, kXtuGrad, w, s.gbase, nullptr, 0, guard, nullptr);
+    } else {
+        rows_pass(s, kModeCache, w, guard);
+        xtu_pass(s, kXtuGrad, w, s.gbase, nullptr, 0, guard);
+    }
+    loss_finalize(s, w, 1, s.scal + 0, guard);
+}
+
+int op_hv(Shard& s, const double* v, double* out, const double* dotvec, int dot_slot, const int32_t* guard) {
+    HvTimer* tm = (s.capture_timing && s.hv_timer_site >= 0 && s.hv_timer_site < (int)s.hv_timers.size())
+                      ? &s.hv_timers[s.hv_timer_site]
+                      : nullptr;
+    if (tm) NADMM_CUDA(cudaEventRecord(tm->start, s.ctx->stream));
+    int g = 0;
+    if (dmma_supported(s)) {
+        dmma_pass(s, kModeHv, v, guard);
+        if (tm) NADMM_CUDA(cudaEventRecord(tm->stop, s.ctx->stream));
+        finalize_partials(s, s.part_chunks, kXtuHv, v, out, dotvec, dot_slot, guard, &g);
+    } else {
+        rows_pass(s, kModeHv, v, guard);
+        g = xtu_pass(s, kXtuHv, v, out, dotvec, dot_slot, guard);
+        if (tm) NADMM_CUDA(cudaEventRecord(tm->stop, s.ctx->stream));
+    }
+    return g;
+}
+
+void op_lp(Shard& s, const double* p, const int32_t* guard) {
+    if (dmma_supported(s))
+        dmma_pass(s, kModeLp, p, guard);
+    else
+        rows_pass(s, kModeLp, p, guard);
+}
+
+void op_value(Shard& s, const double* w, double* dst, int add_ridge, const int32_t* guard) {
+    if (dmma_supported(s))
+        dmma_pass(s, kModeValue, w, guard);
+    else
+        rows_pass(s, kModeValue, w, guard);
+    loss_finalize(s, w, add_ridge, dst, guard);
+}
+
+void op_predict(Shard& s, const double* w) { rows_pass(s, kModePredict, w, nullptr); }
+
+// ---------------------------------------------------------------------------------------------
+// Solver driver
+// ---------------------------------------------------------------------------------------------
+void validate_newton_cfg(const nadmm_newton_cfg& c) {  // NewtonConfig::validate (src/newton.cpp:8-17)
+    if (c.cg_tol <= 0.0 || c.cg_tol >= 1.0) raise(NADMM_ECONFIG, "cg_tol must lie in (0,1)");
+    if (c.armijo_beta <= 0.0 || c.armijo_beta >= 1.0) raise(NADMM_ECONFIG, "armijo_beta must lie in (0,1)");
+    if (c.backtrack_gamma <= 0.0 || c.backtrack_gamma >= 1.0) raise(NADMM_ECONFIG, "backtrack_gamma must lie in (0,1)");
+    if (c.cg_max_iters < 1) raise(NADMM_ECONFIG, "cg_max_iters must be >= 1");
+    if (c.ls_max_iters < 0) raise(NADMM_ECONFIG, "ls_max_iters must be >= 0");
+    if (c.newton_max_iters < 0) raise(NADMM_ECONFIG, "newton_max_iters must be >= 0");
+    if (c.grad_tol < 0.0) raise(NADMM_ECONFIG, "grad_tol must be >= 0");
+    if (c.cg_max_iters > kMaxCg) raise(NADMM_ECONFIG, "cg_max_iters exceeds the device solver limit (256)");
+    if (c.ls_max_iters > kMaxLs) raise(NADMM_ECONFIG, "ls_max_iters exceeds the device solver limit (62)");
+}
+
+void set_params(Shard& s, const nadmm_newton_cfg& c, double lambda, bool aug, double rho) {
+    DevParams h{};
+    h.lambda = lambda;
+    h.rho = aug ? rho : 0.0;
+    h.augmented = aug ? 1 : 0;
+    h.cg_max_iters = c.cg_max_iters;
+    h.cg_tol = c.cg_tol;
+    h.armijo_beta = c.armijo_beta;
+    h.backtrack_gamma = c.backtrack_gamma;
+    h.ls_max_iters = c.ls_max_iters;
+    h.grad_tol = c.grad_tol;
+    *s.prm_host = h;
+    NADMM_CUDA(cudaMemcpyAsync(s.prm, s.prm_host, sizeof(DevParams), cudaMemcpyHostToDevice, s.ctx->stream));
+}
+
+void set_lambda_only(Shard& s, double lambda) {
+    DevParams h = *s.prm_host;
+    h.lambda = lambda;
+    h.augmented = 0;
+    h.rho = 0.0;
+    *s.prm_host = h;
+    NADMM_CUDA(cudaMemcpyAsync(s.prm, s.prm_host, sizeof(DevParams), cudaMemcpyHostToDevice, s.ctx->stream));
+}
+
+void ensure_cache_at_x(Shard& s, double lambda) {
+    if (s.cache_at == Shard::kAtX && s.cache_lambda == lambda) return;
+    op_cache_grad(s, s.x, nullptr);
+    s.cache_at = Shard::kAtX;
+    s.cache_lambda = lambda;
+}
+
+static void destroy_graphs(Shard& s) {
+    if (s.g_iter) cudaGraphExecDestroy(s.g_iter);
+    s.g_iter = nullptr;
+    s.g_cg_max = s.g_ls_max = -1;
+}
+
+static void capture_iteration_graph(Shard& s, int cg_max, int ls_max) {
+    if (s.g_iter && s.g_cg_max == cg_max && s.g_ls_max == ls_max && s.g_timing == s.ctx->timing) return;
+    destroy_graphs(s);
+    cudaStream_t st = s.ctx->stream;
+    const nadmm_stats saved = s.ctx->stats;
+    s.ensure_timers(s.ctx->timing ? cg_max + 1 : 0);
+    cudaGraph_t graph = nullptr;
+    NADMM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+        s.capture_timing = s.ctx->timing;
+        launch_newton_iteration(s, cg_max, ls_max);
+        s.capture_timing = false;
+    } catch (...) {
+        s.capture_timing = false;
+        cudaStreamEndCapture(st, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    NADMM_CUDA(cudaStreamEndCapture(st, &graph));
+    s.g_nodes = s.ctx->stats.kernel_launches - saved.kernel_launches;
+    s.ctx->stats = saved;
+    NADMM_CUDA(cudaGraphInstantiate(&s.g_iter, graph, 0));
+    cudaGraphDestroy(graph);
+    s.g_cg_max = cg_max;
+    s.g_ls_max = ls_max;
+    s.g_timing = s.ctx->timing;
+}
+
+// Reads back the solver state; accumulates the Hv timers of the Hv passes that actually ran.
+static void readback(Shard& s, int cg_max) {
+    NADMM_CUDA(cudaMemcpyAsync(s.st_host, s.st, sizeof(DevState), cudaMemcpyDeviceToHost, s.ctx->stream));
+    NADMM_CUDA(cudaStreamSynchronize(s.ctx->stream));
+    if (s.g_timing && !s.hv_timers.empty()) {
+        const DevState& h = *s.st_host;
+        for (int it = 0; it <= cg_max && it < (int)s.hv_timers.size(); ++it) {
+            const bool ran = it < cg_max ? h.cg_act[it] != 0 : h.cert_act != 0;
+            if (!ran) continue;
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, s.hv_timers[it].start, s.hv_timers[it].stop) == cudaSuccess) {
+                s.ctx->stats.hv_kernel_ms += ms;
+                s.ctx->stats.hv_kernel_samples++;
+            }
+        }
+    }
+}
+
+SolveResult device_newton_solve(Shard& s, const nadmm_newton_cfg& cfg, double lambda, bool aug, double rho,
+                                int newton_max) {
+    validate_newton_cfg(cfg);
+    if (aug && rho <= 0.0) raise(NADMM_ECONFIG, "augmented objective requires rho > 0");
+    set_params(s, cfg, lambda, aug, rho);
+    capture_iteration_graph(s, cfg.cg_max_iters, cfg.ls_max_iters);
+    ensure_cache_at_x(s, lambda);
+    int nvec = 0;
+    launch_grad_aug(s, nullptr, &nvec);
+    launch_value_finish(s, nvec, 1, nullptr);
+    SolveResult res;
+    for (int k = 0; k < newton_max; ++k) {
+        NADMM_CUDA(cudaGraphLaunch(s.g_iter, s.ctx->stream));
+        s.ctx->stats.kernel_launches += s.g_nodes;
+        readback(s, cfg.cg_max_iters);
+        if (!s.st_host->active) break;
+    }
+    if (newton_max == 0) readback(s, cfg.cg_max_iters);
+    const DevState& h = *s.st_host;
+    s.cache_at = Shard::kAtX;
+    s.cache_lambda = lambda;
+    if (h.error) {
+        res.error = h.error;
+        return res;
+    }
+    res.iterations = h.iter;
+    res.final_grad_norm = h.g_norm;
+    res.converged = h.g_norm < cfg.grad_tol;  // src/newton.cpp:128-130 (or the early return at 83-86)
+    res.trace.resize(std::min(h.iter, kTraceCap));
+    if (!res.trace.empty())
+        NADMM_CUDA(cudaMemcpy(res.trace.data(), s.trace, sizeof(DevTrace) * res.trace.size(), cudaMemcpyDeviceToHost));
+    res.cg_sum = 0;
+    res.fe_sum = 0;
+    res.flags = 0;
+    for (const auto& t : res.trace) {
+        res.cg_sum += t.cg_iters;
+        res.fe_sum += t.fn_evals;
+        if (t.ls_capped) res.flags |= 1;
+        if (t.cg_fallback) res.flags |= 2;
+    }
+    return res;
+}
+
+}  // namespace nadmm

@@ -1,0 +1,27 @@
+// Host-side solver entry points shared by the C ABI, the worker and the ADMM driver.
+#pragma once
+
+#include <vector>
+
+#include "state.h"
+
+namespace nadmm {
+
+struct SolveResult {
+    int error = 0;
+    int iterations = 0;
+    bool converged = false;
+    double final_grad_norm = 0.0;
+    std::vector<DevTrace> trace;
+    int cg_sum = 0, fe_sum = 0, flags = 0;
+};
+
+void validate_newton_cfg(const nadmm_newton_cfg& c);
+void set_params(Shard& s, const nadmm_newton_cfg& c, double lambda, bool aug, double rho);
+void set_lambda_only(Shard& s, double lambda);
+void ensure_cache_at_x(Shard& s, double lambda);
+// newton_solve (src/newton.cpp:73-132) from s.x with z/y in s.z/s.y; result x left in s.x.
+SolveResult device_newton_solve(Shard& s, const nadmm_newton_cfg& cfg, double lambda, bool aug, double rho,
+                                int newton_max);
+
+}  // namespace nadmm

@@ -1,0 +1,190 @@
+"""GPU parity: the CUDA product (through the C ABI) against the CPU oracle on the same inputs.
+
+Tiers: (i) kernel outputs at identical inputs <= 1e-12 relative; (ii) one Newton
+solve: identical cg_iters / step / flags per iteration, x and objective <= 1e-10; (iii) full ADMM
+run: identical iteration count and predictions, F(z) and z <= 1e-9 relative.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from util import random_csr, random_dense, rel
+
+pytestmark = pytest.mark.gpu
+
+TOL_KERNEL = 1e-12
+TOL_NEWTON = 1e-10
+TOL_ADMM = 1e-9
+
+DENSE_SHAPES = [(50, 7, 4), (200, 33, 10), (129, 5, 2), (300, 28, 2), (1000, 784, 10), (96, 3072, 10), (77, 65, 21)]
+
+
+def shards(nadmm, X, y, C):
+    return nadmm.Dataset.dense(X, y, C), oracle.Shard(X, y, C)
+
+
+@pytest.mark.parametrize("n,p,C", DENSE_SHAPES)
+@pytest.mark.parametrize("lam", [0.0, 1e-3])
+def test_dense_model_ops(nadmm, port, n, p, C, lam):
+    rng = np.random.default_rng(n * 1000 + p + C)
+    X, y = random_dense(rng, n, p, C, scale=1.0 / np.sqrt(p))
+    ds, sh = shards(nadmm, X, y, C)
+    d = sh.d
+    w = rng.normal(size=d)
+    v = rng.normal(size=d)
+    lg, rm, al, pr = port.cache(sh, w)
+    c = nadmm.stable_exp_cache(ds, w)
+    assert rel(c.logits, lg) <= TOL_KERNEL
+    assert rel(c.row_max, rm) <= TOL_KERNEL
+    assert rel(c.alpha, al) <= TOL_KERNEL
+    assert rel(c.probs, pr) <= TOL_KERNEL
+    assert abs(nadmm.loss(ds, w, lam) - port.loss(sh, w, lam)) <= TOL_KERNEL * abs(port.loss(sh, w, lam))
+    assert rel(nadmm.gradient(ds, w, lam), port.gradient(sh, w, lam)) <= TOL_KERNEL
+    assert rel(nadmm.hessian_vec(ds, w, v, lam), port.hessian_vec(sh, w, v, lam)) <= TOL_KERNEL
+    np.testing.assert_array_equal(nadmm.predict(ds, w), port.predict(sh, w))
+
+
+@pytest.mark.parametrize("n,p,C,dens", [(100, 50, 5, 0.2), (300, 2000, 20, 0.01), (64, 9, 2, 0.5)])
+def test_sparse_model_ops(nadmm, port, n, p, C, dens):
+    rng = np.random.default_rng(7 + n)
+    ip, ix, vv, y = random_csr(rng, n, p, C, dens)
+    ds = nadmm.Dataset.sparse(ip, ix, vv, y, C, p)
+    sh = oracle.Shard(labels=y, C_=C, csr=(ip, ix, vv), p=p)
+    w = rng.normal(size=sh.d) * 0.5
+    v = rng.normal(size=sh.d)
+    assert abs(nadmm.loss(ds, w, 1e-3) - port.loss(sh, w, 1e-3)) <= TOL_KERNEL * abs(port.loss(sh, w, 1e-3))
+    assert rel(nadmm.gradient(ds, w, 0.0), port.gradient(sh, w, 0.0)) <= TOL_KERNEL
+    assert rel(nadmm.hessian_vec(ds, w, v, 1e-3), port.hessian_vec(sh, w, v, 1e-3)) <= TOL_KERNEL
+    np.testing.assert_array_equal(nadmm.predict(ds, w), port.predict(sh, w))
+    # sparse / dense agreement (SPEC.md model-softmax invariants)
+    dd = nadmm.Dataset.dense(sh.dense(), y, C)
+    assert rel(nadmm.hessian_vec(dd, w, v, 0.0), nadmm.hessian_vec(ds, w, v, 0.0)) <= TOL_KERNEL
+
+
+def test_spec_known_answers(nadmm):
+    # loss, any data, w = 0, lambda = 0 -> n log C
+    X = np.arange(12.0).reshape(4, 3)
+    ds = nadmm.Dataset.dense(X, [1, 2, 3, 1], 3)
+    assert abs(nadmm.loss(ds, np.zeros(6)) - 4 * np.log(3)) < 1e-12
+    one = nadmm.Dataset.dense([[2.0]], [1], 2)
+    assert abs(nadmm.loss(one, [0.0]) - np.log(2)) < 1e-15
+    np.testing.assert_allclose(nadmm.gradient(one, [0.0]), [-1.0], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(nadmm.hessian_vec(one, [0.0], [3.0]), [3.0], rtol=0, atol=1e-15)
+    np.testing.assert_array_equal(nadmm.hessian_vec(ds, np.ones(6), np.zeros(6)), np.zeros(6))
+    big = nadmm.Dataset.dense([[1000.0]], [2], 2)
+    assert nadmm.loss(big, [1.0]) == 1000.0  # src/softmax.cpp:69-77 (SPEC.md:57 typo; b=2 -> 1000)
+    big1 = nadmm.Dataset.dense([[1000.0]], [1], 2)
+    assert nadmm.loss(big1, [1.0]) == 0.0
+    # predict: C=2, <a, x1> = 1 -> class 1; w = 0 -> class 1 (tie rule); C=3 logits (-5,-7) -> class 3
+    assert nadmm.predict(nadmm.Dataset.dense([[1.0]], [1], 2), [1.0])[0] == 1
+    assert nadmm.predict(ds, np.zeros(6)).tolist() == [1, 1, 1, 1]
+    p3 = nadmm.Dataset.dense([[1.0]], [1], 3)
+    assert nadmm.predict(p3, [-5.0, -7.0])[0] == 3
+
+
+def test_stability_large_features(nadmm, port):
+    rng = np.random.default_rng(3)
+    X, y = random_dense(rng, 40, 6, 4)
+    X *= 1e3
+    ds, sh = shards(nadmm, X, y, 4)
+    w = rng.normal(size=sh.d) * 1e2
+    v = rng.normal(size=sh.d)
+    assert np.isfinite(nadmm.loss(ds, w))
+    assert np.all(np.isfinite(nadmm.gradient(ds, w)))
+    assert np.all(np.isfinite(nadmm.hessian_vec(ds, w, v)))
+    assert rel(nadmm.hessian_vec(ds, w, v), port.hessian_vec(sh, w, v)) <= TOL_KERNEL
+
+
+def test_errors(nadmm):
+    with pytest.raises(nadmm.DataError):
+        nadmm.Dataset.dense([[1.0], [2.0]], [1, 3], 2)
+    with pytest.raises(nadmm.ConfigError):
+        nadmm.Dataset.dense([[1.0]], [1], 1)
+    with pytest.raises(nadmm.DataError):
+        nadmm.Dataset.dense([[np.nan]], [1], 2)
+    ds = nadmm.Dataset.dense([[1.0, 2.0]], [1], 2)
+    with pytest.raises(nadmm.ConfigError):
+        nadmm.loss(ds, [1.0])
+    with pytest.raises(nadmm.ConfigError):
+        nadmm.make_augmented_objective(nadmm.make_softmax_objective(ds, 0.0), 0.0, [0, 0], [0, 0])
+    with pytest.raises(nadmm.ConfigError):
+        nadmm.newton_solve(nadmm.make_softmax_objective(ds, 0.0), [0.0, 0.0], nadmm.NewtonConfig(cg_tol=2.0))
+
+
+def _cmp_trace(a, b):
+    assert len(a) == len(b)
+    for ra, rb in zip(a, b):
+        assert ra.cg_iters == rb["cg_iters"]
+        assert ra.fn_evals == rb["fn_evals"]
+        assert ra.step == rb["step"]
+        assert bool(ra.ls_capped) == bool(rb["ls_capped"])
+        assert bool(ra.cg_fallback) == bool(rb["cg_fallback"])
+        assert abs(ra.objective - rb["objective"]) <= TOL_NEWTON * abs(rb["objective"])
+        assert abs(ra.grad_norm - rb["grad_norm"]) <= 1e-8 * max(rb["grad_norm"], 1e-12)
+
+
+@pytest.mark.parametrize("n,p,C,lam", [(400, 20, 4, 1e-3), (2000, 784, 10, 1e-3), (300, 28, 2, 1e-3)])
+def test_newton_single_node(nadmm, port, n, p, C, lam):
+    Xtr, ytr, _, _ = port.generate_synthetic(n + n // 9 + 2, p, C, separation=3.0, noise=1.0, seed=1)
+    ds, sh = shards(nadmm, Xtr, ytr, C)
+    cfg = nadmm.NewtonConfig(newton_max_iters=4)
+    r = nadmm.newton_solve(nadmm.make_softmax_objective(ds, lam), np.zeros(sh.d), cfg)
+    o = port.newton_solve(sh, lam, np.zeros(sh.d), cfg=list(cfg.__dict__.values()))
+    _cmp_trace(r.trace, o["trace"])
+    assert rel(r.x, o["x"]) <= TOL_NEWTON
+    assert abs(r.final_grad_norm - o["final_grad_norm"]) <= 1e-7 * max(o["final_grad_norm"], 1e-12)
+
+
+def test_newton_augmented(nadmm, port):
+    rng = np.random.default_rng(11)
+    X, y = random_dense(rng, 500, 30, 5, scale=0.3)
+    ds, sh = shards(nadmm, X, y, 5)
+    z, yy, x0 = rng.normal(size=sh.d) * 0.1, rng.normal(size=sh.d) * 0.1, rng.normal(size=sh.d) * 0.05
+    cfg = nadmm.NewtonConfig(newton_max_iters=3)
+    base = nadmm.make_softmax_objective(ds, 0.0)
+    r = nadmm.newton_solve(nadmm.make_augmented_objective(base, 2.5, z, yy), x0, cfg)
+    o = port.newton_solve(sh, 0.0, x0, cfg=list(cfg.__dict__.values()), rho=2.5, z=z, y=yy)
+    _cmp_trace(r.trace, o["trace"])
+    assert rel(r.x, o["x"]) <= TOL_NEWTON
+
+
+def test_worker_sequence_matches_reference(nadmm, ref):
+    rng = np.random.default_rng(5)
+    X, y = random_dense(rng, 300, 12, 3, scale=0.5)
+    ds = nadmm.Dataset.dense(X, y, 3)
+    rw = ref.dataset(oracle.Shard(X, y, 3)).worker()
+    w = nadmm.Worker(ds)
+    d = ds.weight_dim()
+    for k in range(4):
+        z, yy = rng.normal(size=d) * 0.1, rng.normal(size=d) * 0.1
+        rho = [1.0, 1.0, 0.5, 3.0][k]
+        xg, sg = w.solve(rho, z, yy)
+        xr, sr = rw.solve(rho, z, yy)
+        assert rel(xg, xr) <= TOL_NEWTON
+        assert sg.cg_iters == sr["cg_iters"] and sg.fn_evals == sr["fn_evals"] and sg.flags == sr["flags"]
+        assert sg.inner_iters == sr["inner_iters"]
+
+
+@pytest.mark.parametrize("penalty", ["fixed", "spectral"])
+def test_admm_run_matches_oracle(nadmm, port, penalty):
+    N, C, p = 4, 4, 10
+    Xtr, ytr, _, _ = port.generate_synthetic(1200, p, C, separation=3.0, noise=1.0, seed=0)
+    owner = port.partition_owner(len(ytr), N)
+    parts_o = [oracle.Shard(Xtr[owner == i], ytr[owner == i], C) for i in range(N)]
+    parts_g = [nadmm.Dataset.dense(Xtr[owner == i], ytr[owner == i], C) for i in range(N)]
+    cfg_o = oracle.admm_cfg(n_workers=N, lam=1e-5, penalty=penalty, max_outer_iters=40)
+    ro = port.admm_run(parts_o, cfg_o)
+    cfg = nadmm.AdmmConfig(n_workers=N, lam=1e-5, penalty=nadmm.PenaltyPolicy(kind=penalty),
+                           stopping=nadmm.StoppingConfig(max_outer_iters=40))
+    rg = nadmm.run_admm(parts_g, cfg, nadmm.EvalContext(eval_objective=True))
+    assert rg.iterations == ro["iterations"]
+    assert rg.converged == ro["converged"]
+    assert rel(rg.z, ro["z"]) <= TOL_ADMM
+    for mg, mo in zip(rg.metrics, ro["metrics"]):
+        assert abs(mg["train_objective"] - mo["train_objective"]) <= TOL_ADMM * abs(mo["train_objective"])
+        assert mg["cg_iters"] == mo["cg_iters"] and mg["fn_evals"] == mo["fn_evals"]
+    np.testing.assert_allclose(rg.rho, ro["rho"], rtol=1e-9)
+    Xall = np.concatenate([s.X for s in parts_o])
+    yall = np.concatenate([s.labels for s in parts_o])
+    full_g = nadmm.Dataset.dense(Xall, yall, C)
+    np.testing.assert_array_equal(nadmm.predict(full_g, rg.z), port.predict(oracle.Shard(Xall, yall, C), ro["z"]))
