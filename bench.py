@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native Newton-ADMM hot path (contract: DESIGN.md "Measurement").
+
+Workload (BASELINE.json configs[1]): CIFAR-10-shaped synthetic dense data, 50,000 x 3,072, 10 classes,
+lambda = 1e-3, Newton-ADMM over 8 ADMM nodes (contiguous row shards of 6,250 rows), NewtonConfig
+defaults (10 CG iterations, tol 1e-4, 10 line-search trials), one inner Newton step per outer
+iteration, fixed rho = 1. With --gpus N each rank holds 8/N nodes (strong scaling; one NCCL
+allreduce per outer iteration). Data comes from the reference generator (src/data_io.cpp:330-370),
+separation 3, noise 1, seed 0.
+
+A step is one outer ADMM iteration. `value` = shard-level Hessian-vector products applied per
+second on device-resident data (whole job, max-over-ranks device time); `e2e` = the same metric
+through the reference-facing worker ABI (nadmm_worker_solve: z, y_i host->device, x_i device->host
+every step, reference-style host coordinator). `--impl reference` times the reference's own CPU
+worker solve (oracle/_ref: the reference sources built against the Eigen stand-in) on this host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_TOTAL, P, C, LAM = 55_556, 3072, 10, 1e-3  # floor(9n/10) = 50,000 train rows
+NODES = 8
+SEP, NOISE, SEED = 3.0, 1.0, 0
+THETA_TARGET = 0.05
+METRIC = "Hv products/s (Newton-ADMM shard Hessian-vector products; time-to-target alongside)"
+WORKLOAD = "cifar10-shaped dense 50000x3072 C=10 lambda=1e-3, Newton-ADMM over 8 row-shard nodes"
+
+
+def env_int(k, d):
+    return int(os.environ.get(k, d))
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device: int):
+        self.dev = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.samples = []
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            out = ""
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def summary(self) -> dict:
+        if not getattr(self, "samples", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = {0x1: "gpu_idle", 0x2: "applications_clocks", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+                 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake",
+                 0x100: "display_clocks"}
+        loaded = [s for s in self.samples if not (s[2] & 0x1)] or self.samples
+        mask = 0
+        for s in loaded:
+            mask |= s[2]
+        return {"sm_mhz": float(np.median([s[0] for s in loaded])), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": [v for k, v in names.items() if mask & k and k != 0x1], "samples": len(self.samples)}
+
+
+def make_data():
+    import paper_1807_07132_b200 as nadmm
+
+    Xtr, ytr, Xte, yte = nadmm.generate_synthetic(N_TOTAL, P, C, SEP, NOISE, SEED)
+    owner = nadmm.partition_owner(len(ytr), NODES)
+    return Xtr, ytr, Xte, yte, owner
+
+
+def hv_bytes(n_loc: int) -> int:
+    """Algorithmic bytes of one dense shard Hv: X once, P once, v in, Hv out."""
+    K = C - 1
+    return 8 * n_loc * P + 8 * n_loc * K + 16 * P * K
+
+
+def reference_worker_bench(Xs, ys, steps: int, warmup: int, threads: int):
+    """The reference's own worker solve (run_worker ADMM branch) on host cores, per shard."""
+    import oracle
+
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    r = oracle.ref()
+    kind = "reference"
+    if r is None:  # reference build unavailable -> C restatement
+        kind = "port"
+    sh = oracle.Shard(Xs, ys, C)
+    d = sh.d
+    rng = np.random.default_rng(0)
+    if kind == "reference":
+        w = r.dataset(sh).worker()
+        solve = lambda z, y: w.solve(1.0, z, y)
+    else:
+        P_ = oracle.Port()
+        state = {"x": np.zeros(d)}
+
+        def solve(z, y):
+            o = P_.newton_solve(sh, 0.0, state["x"], cfg=list(oracle.DEFAULT_NEWTON[:6]) + [1], rho=1.0, z=z, y=y)
+            state["x"] = o["x"]
+            tr = o["trace"]
+            return o["x"], {"cg_iters": sum(t["cg_iters"] for t in tr), "inner_iters": len(tr)}
+    z = np.zeros(d)
+    for _ in range(warmup):
+        solve(z, np.zeros(d))
+    hv, t0 = 0, time.perf_counter()
+    for k in range(steps):
+        z = rng.normal(size=d) * 1e-3
+        x, st = solve(z, np.zeros(d))
+        hv += int(st["cg_iters"]) + int(st["inner_iters"])  # CG Hv + certificate Hv per Newton step
+    dt = time.perf_counter() - t0
+    return kind, hv, dt
+
+
+def run_reference_arm(args):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return
+    import paper_1807_07132_b200 as nadmm
+
+    Xtr, ytr, _, _ = nadmm.generate_synthetic(N_TOTAL, P, C, SEP, NOISE, SEED)
+    owner = nadmm.partition_owner(len(ytr), NODES)
+    Xs, ys = Xtr[owner == 0], ytr[owner == 0]
+    threads = os.cpu_count() or 1
+    kind, hv, dt = reference_worker_bench(Xs, ys, args.steps, args.warmup, threads)
+    v = hv / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Hv/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "sample": "one ADMM node (6250x3072) worker solve per step"},
+            "cpu_baseline": {"value": v, "unit": "Hv/s", "cores": threads, "kind": kind,
+                             "sample": f"{args.steps} run_worker ADMM solves of node 0 (6250x3072, 10 CG + cert Hv each)"},
+            "e2e": {"value": v, "unit": "Hv/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-target run")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--cpu-steps", type=int, default=12)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # contract: W >= 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+    if NODES % world:
+        raise SystemExit(f"--gpus must divide {NODES}")
+    import paper_1807_07132_b200 as nadmm
+
+    torch.cuda.set_device(local)
+    ctx = nadmm.Context(local)
+    Xtr, ytr, Xte, yte, owner = make_data()
+    per = NODES // world
+    mine = list(range(rank * per, (rank + 1) * per))
+    shards = [nadmm.Dataset.dense(Xtr[owner == i], ytr[owner == i], C, ctx=ctx) for i in mine]
+    n_loc = int((owner == 0).sum())
+    comm = None
+    if world > 1:
+        uid = [nadmm.Communicator.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = nadmm.Communicator(ctx, uid[0], world, rank)
+
+    def barrier():
+        ctx.synchronize()
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t)
+        return float(t.item())
+
+    cfg = nadmm.AdmmConfig(n_workers=NODES, lam=LAM, stopping=nadmm.StoppingConfig(max_outer_iters=100000))
+    stream = torch.cuda.ExternalStream(ctx.stream)
+
+    # ---------------- value: device-resident consensus loop ----------------
+    sess = nadmm.AdmmSession(shards, cfg, nadmm.EvalContext(eval_objective=True, ignore_convergence=True), comm)
+    sess.step(args.warmup)
+    ctx.set_timing(True)
+    barrier()
+    ctx.reset_stats()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        done = sess.step(args.steps)
+        e1.record(stream)
+        e1.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    st = ctx.stats()
+    barrier()
+    ctx.set_timing(False)
+    assert done == args.steps, f"session stopped early ({done}/{args.steps})"
+    hv_total = sum_over_ranks(st["hv_products"])
+    value = hv_total / (ms * 1e-3)
+    hv_ms = st["hv_kernel_ms"] / max(1, st["hv_kernel_samples"])
+    achieved = hv_bytes(n_loc) / (hv_ms * 1e-3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "kernel": "dense Hv pass (shard 6250x3072)", "hv_pass_ms": hv_ms,
+                "bytes_per_hv": hv_bytes(n_loc), "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"}
+    sess_res = sess.result()
+    sess.close()
+
+    # ---------------- e2e: reference-facing worker ABI with host buffers ----------------
+    import torch as _t
+
+    d = (C - 1) * P
+    workers = [nadmm.Worker(s) for s in shards]
+    zbuf = _t.zeros(d, dtype=_t.float64).pin_memory().numpy()
+    ybufs = [_t.zeros(d, dtype=_t.float64).pin_memory().numpy() for _ in mine]
+    xbufs = [_t.zeros(d, dtype=_t.float64).pin_memory().numpy() for _ in mine]
+    rho = 1.0
+
+    def e2e_step():
+        hv = 0
+        for i, w in enumerate(workers):
+            x, s = w.solve(rho, zbuf, ybufs[i], cfg.newton, 1)
+            xbufs[i][:] = x
+            hv += s.cg_iters + s.inner_iters
+        S = np.zeros(d + 1)
+        for i in range(len(workers)):  # reference coordinator: z_update / y_update
+            S[:d] += rho * xbufs[i] - ybufs[i]
+        S[d] = rho * len(workers)
+        if dist:
+            tS = _t.from_numpy(S)
+            dist.all_reduce(tS)
+            S = tS.numpy()
+        zbuf[:] = S[:d] / (LAM + S[d])
+        for i in range(len(workers)):
+            ybufs[i][:] = ybufs[i] + rho * (zbuf - xbufs[i])
+        return hv
+
+    for _ in range(args.warmup):
+        e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    hv_e2e = sum(e2e_step() for _ in range(args.steps))
+    t_e2e = max_over_ranks(time.perf_counter() - t0)
+    hv_e2e = sum_over_ranks(hv_e2e)
+    e2e = {"value": hv_e2e / t_e2e, "unit": "Hv/s", "h2d_bytes_per_step": per * 2 * d * 8 * world,
+           "d2h_bytes_per_step": per * d * 8 * world,
+           "path": "nadmm_worker_solve per node (scatter z,y_i / gather x_i) + host coordinator"}
+
+    # ---------------- time to target: theta = (F - F*)/F* <= 0.05 ----------------
+    ttt = {}
+    if not args.no_ttt:
+        fstar = [None]
+        if rank == 0:
+            full = nadmm.Dataset.dense(Xtr, ytr, C, ctx=ctx)
+            ref = nadmm.newton_solve(nadmm.make_softmax_objective(full, LAM), np.zeros(d),
+                                     nadmm.NewtonConfig(cg_tol=1e-10, cg_max_iters=200, grad_tol=1e-10,
+                                                        newton_max_iters=60))  # compute_reference
+            fstar = [ref.trace[-1].objective if ref.trace else nadmm.loss(full, ref.x, LAM)]
+            full.close()
+        if dist:
+            dist.broadcast_object_list(fstar, src=0)
+        tcfg = nadmm.AdmmConfig(n_workers=NODES, lam=LAM, stopping=nadmm.StoppingConfig(max_outer_iters=300))
+        barrier()
+        s2 = nadmm.AdmmSession(shards, tcfg, nadmm.EvalContext(True, fstar[0], THETA_TARGET), comm)
+        s2.step(300)
+        res = s2.result()
+        rows = res.metrics
+        hit = [r for r in rows if r["theta"] == r["theta"] and r["theta"] <= THETA_TARGET]
+        t_hit = max_over_ranks(hit[0]["wall_seconds"] if hit else float("nan"))
+        ttt = {"time_to_target_s": t_hit if hit else None, "ttt_outer_iters": hit[0]["iteration"] if hit else None,
+               "theta_target": THETA_TARGET, "f_star": fstar[0], "final_theta": rows[-1]["theta"] if rows else None,
+               "ttt_converged_flag": res.converged}
+        Xte_ds = nadmm.Dataset.dense(Xte, yte, C, ctx=ctx)
+        ttt["test_accuracy"] = nadmm.accuracy(nadmm.predict(Xte_ds, res.z), yte)
+        s2.close()
+
+    # ---------------- CPU baseline (rank 0, N = 1 only) ----------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        kind, hv, dt = reference_worker_bench(Xtr[owner == 0], ytr[owner == 0], args.cpu_steps, 1, threads)
+        cpu = {"value": hv / dt, "unit": "Hv/s", "cores": threads, "kind": kind,
+               "sample": f"{args.cpu_steps} run_worker ADMM solves of node 0 (6250x3072) after 1 warm-up"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "Hv/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (reference generate_synthetic: separation 3, noise 1, seed 0)",
+                "config": {"workload": WORKLOAD, "n_train": int(len(ytr)), "p": P, "classes": C, "lambda": LAM,
+                           "admm_nodes": NODES, "nodes_per_gpu": per, "inner_iters": 1, "cg_max_iters": 10,
+                           "ls_max_iters": 10, "penalty": "fixed rho=1",
+                           "l2": "no flush: per-step inputs 1.23 GB/GPU at N=1 >> 126 MB L2"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(st["kernel_launches"]),
+                "clocks": clk.summary(), "outer_iters_per_s": args.steps / (ms * 1e-3),
+                "hv_per_step": hv_total / args.steps}
+        line.update(ttt)
+        print(json.dumps(line), flush=True)
+    if comm:
+        comm.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -196,6 +196,7 @@ typedef struct {                  /* AdmmConfig + PenaltyPolicy + StoppingConfig
     int32_t eval_objective;       /* evaluate F(z^k) = sum_i loss(D_i, z) + lambda/2 |z|^2 each iteration */
     double f_star;                /* > 0: theta = (F - F*)/F* recorded per row */
     double theta_stop;            /* > 0 (needs f_star): stop at the first k with theta <= theta_stop */
+    int32_t ignore_convergence;   /* throughput runs: report convergence in the rows but keep iterating */
 } nadmm_admm_cfg;
 
 void nadmm_admm_cfg_default(nadmm_admm_cfg* cfg);
@@ -224,6 +225,18 @@ typedef struct {                  /* MetricsRow subset (inc/metrics.hpp:15-27) *
 nadmm_status nadmm_admm_run(const nadmm_shard* shards, int32_t n_local, nadmm_comm comm, const nadmm_admm_cfg* cfg,
                             double* z_out, double* rho_out, nadmm_metrics_row* rows, int32_t row_cap,
                             int32_t* iterations, int32_t* converged);
+
+/* Stepping form of the same loop: create (AdmmState::initial), step up to n_iters outer iterations
+ * (stops early on convergence / theta_stop / max_outer_iters), read the result, free. rows gets
+ * one MetricsRow per iteration done in this call. */
+typedef struct nadmm_admm_s* nadmm_admm;
+nadmm_status nadmm_admm_create(const nadmm_shard* shards, int32_t n_local, nadmm_comm comm,
+                               const nadmm_admm_cfg* cfg, nadmm_admm* out);
+nadmm_status nadmm_admm_step(nadmm_admm run, int32_t n_iters, nadmm_metrics_row* rows, int32_t row_cap,
+                             int32_t* done, int32_t* finished);
+nadmm_status nadmm_admm_result(nadmm_admm run, double* z_out, double* rho_out, int32_t* iterations,
+                               int32_t* converged);
+nadmm_status nadmm_admm_free(nadmm_admm run);
 
 /* ------------------------------------------------------------------------------------------ */
 /* Host-only data fixtures (no GPU needed) -- src/data_io.cpp:16-43, 300-370                    */

@@ -468,6 +468,7 @@ class EvalContext:  # inc/admm.hpp:132-136
     eval_objective: bool = True
     f_star: Optional[float] = None
     theta_stop: float = 0.0
+    ignore_convergence: bool = False  # throughput runs: keep iterating past has_converged
 
 
 @dataclass
@@ -523,6 +524,54 @@ def run_admm(parts: Sequence[Dataset], cfg: AdmmConfig, eval: Optional[EvalConte
                                   cap, C.byref(it), C.byref(conv)))
     metrics = [{f: getattr(r, f) for f, _ in L.MetricsRow._fields_} for r in rows[: min(it.value, cap)]]
     return AdmmRunResult(z, metrics, bool(conv.value), it.value, rho)
+
+
+class AdmmSession:
+    """Stepping form of run_admm: AdmmState::initial, then `step(n)` outer iterations at a time."""
+
+    def __init__(self, parts: Sequence[Dataset], cfg: AdmmConfig, eval: Optional[EvalContext] = None,
+                 comm: Optional[Communicator] = None):
+        if not parts:
+            raise ConfigError("AdmmSession needs at least one shard")
+        ev = eval or EvalContext(eval_objective=False)
+        c = cfg.to_c()
+        c.eval_objective = int(ev.eval_objective)
+        c.f_star = float(ev.f_star or 0.0)
+        c.theta_stop = float(ev.theta_stop)
+        c.ignore_convergence = int(ev.ignore_convergence)
+        self._hs = (C.c_void_p * len(parts))(*[p.handle for p in parts])
+        self.parts, self.cfg = list(parts), cfg
+        h = C.c_void_p()
+        _check(L.lib().nadmm_admm_create(self._hs, len(parts), comm.handle if comm else None, C.byref(c), C.byref(h)))
+        self.handle = h
+        self.metrics: list = []
+        self.finished = False
+
+    def step(self, n: int) -> int:
+        rows = (L.MetricsRow * max(1, n))()
+        done, fin = C.c_int32(), C.c_int32()
+        _check(L.lib().nadmm_admm_step(self.handle, int(n), rows, max(1, n), C.byref(done), C.byref(fin)))
+        self.metrics += [{f: getattr(r, f) for f, _ in L.MetricsRow._fields_} for r in rows[: done.value]]
+        self.finished = bool(fin.value)
+        return done.value
+
+    def result(self) -> AdmmRunResult:
+        d = self.parts[0].weight_dim()
+        z, rho = np.zeros(d), np.zeros(len(self.parts))
+        it, conv = C.c_int32(), C.c_int32()
+        _check(L.lib().nadmm_admm_result(self.handle, _dp(z), _dp(rho), C.byref(it), C.byref(conv)))
+        return AdmmRunResult(z, self.metrics, bool(conv.value), it.value, rho)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            L.lib().nadmm_admm_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ---- data fixtures (src/data_io.cpp) --------------------------------------------------------------

@@ -49,7 +49,8 @@ class AdmmCfg(C.Structure):  # AdmmConfig + PenaltyPolicy + StoppingConfig (inc/
                 ("eps_cor", C.c_double), ("rho_min", C.c_double), ("rho_max", C.c_double),
                 ("eps_abs", C.c_double), ("eps_rel", C.c_double), ("max_outer_iters", C.c_int32),
                 ("standard_norms", C.c_int32), ("inner_iters", C.c_int32), ("newton", NewtonCfg),
-                ("eval_objective", C.c_int32), ("f_star", C.c_double), ("theta_stop", C.c_double)]
+                ("eval_objective", C.c_int32), ("f_star", C.c_double), ("theta_stop", C.c_double),
+                ("ignore_convergence", C.c_int32)]
 
 
 class MetricsRow(C.Structure):  # MetricsRow (inc/metrics.hpp:15-27)
@@ -97,6 +98,11 @@ SIGNATURES = {
     "nadmm_admm_cfg_default": (None, [C.POINTER(AdmmCfg)]),
     "nadmm_admm_run": (S, [C.POINTER(VP), C.c_int32, VP, C.POINTER(AdmmCfg), D, D, C.POINTER(MetricsRow),
                            C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "nadmm_admm_create": (S, [C.POINTER(VP), C.c_int32, VP, C.POINTER(AdmmCfg), C.POINTER(VP)]),
+    "nadmm_admm_step": (S, [VP, C.c_int32, C.POINTER(MetricsRow), C.c_int32, C.POINTER(C.c_int32),
+                            C.POINTER(C.c_int32)]),
+    "nadmm_admm_result": (S, [VP, D, D, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "nadmm_admm_free": (S, [VP]),
     "nadmm_data_last_error": (C.c_char_p, []),
     "nadmm_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "nadmm_generate_synthetic": (S, [C.c_int64, C.c_int64, C.c_int32, C.c_double, C.c_double, C.c_uint64, D, I32,

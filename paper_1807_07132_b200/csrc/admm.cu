@@ -241,15 +241,32 @@ nadmm_status nadmm_comm_destroy(nadmm_comm c) {
 
 namespace nadmm {
 void set_last_error(const std::string& m);
-}
 
-extern "C" nadmm_status nadmm_admm_run(const nadmm_shard* shards, int32_t n_local, nadmm_comm comm,
-                                       const nadmm_admm_cfg* cfg_in, double* z_out, double* rho_out,
-                                       nadmm_metrics_row* rows, int32_t row_cap, int32_t* iterations,
-                                       int32_t* converged_out) {
-    try {
-        if (!shards || n_local < 1 || n_local > kMaxLocal) raise(NADMM_ECONFIG, "need 1..16 local shards");
-        nadmm_admm_cfg cfg;
+// One consensus run (AdmmState + the run_admm loop); stepping lets callers time exact iteration
+// windows (bench.py) while nadmm_admm_run drives it to completion.
+struct AdmmRun {
+    std::vector<Shard*> shards;
+    nadmm_comm comm = nullptr;
+    nadmm_admm_cfg cfg{};
+    nadmm_newton_cfg ncfg{};
+    Ctx* ctx = nullptr;
+    cudaStream_t st = nullptr;
+    int64_t d = 0;
+    int n_local = 0, n_total = 0, nranks = 1, rank = 0;
+    bool sps = false;
+    RunBuffers rb;
+    double *buf = nullptr, *z = nullptr, *pz = nullptr, *zs = nullptr, *zpart = nullptr, *wpart = nullptr;
+    double *wred = nullptr, *fz = nullptr, *rstat = nullptr, *gstat = nullptr;
+    std::vector<double*> yh, xs, ys, yhs;
+    std::vector<double> rho, hstat, hred;
+    int vg = 1;
+    int k = 0, snap_it = 0;
+    bool conv = false, stop = false;
+    cudaEvent_t ev_start = nullptr, ev_now = nullptr;
+    static constexpr int kStats = 8;
+
+    AdmmRun(const nadmm_shard* sh, int32_t nl, nadmm_comm c, const nadmm_admm_cfg* cfg_in) : comm(c), n_local(nl) {
+        if (!sh || nl < 1 || nl > kMaxLocal) raise(NADMM_ECONFIG, "need 1..16 local shards");
         if (cfg_in)
             cfg = *cfg_in;
         else
@@ -260,25 +277,26 @@ extern "C" nadmm_status nadmm_admm_run(const nadmm_shard* shards, int32_t n_loca
              cfg.rho_max < cfg.rho_min))
             raise(NADMM_ECONFIG, "bad spectral penalty policy");  // PenaltyPolicy::validate (inc/admm.hpp:37-47)
         if (cfg.inner_iters < 0) raise(NADMM_ECONFIG, "inner_iters must be >= 0");
-        nadmm_newton_cfg ncfg = cfg.newton;
+        ncfg = cfg.newton;
         ncfg.newton_max_iters = cfg.inner_iters;
         validate_newton_cfg(ncfg);
-        Ctx* ctx = shards[0]->ctx;
-        const int64_t d = shards[0]->d;
-        for (int i = 0; i < n_local; ++i) {
-            if (!shards[i]) raise(NADMM_ECONFIG, "null shard");
-            if (shards[i]->ctx != ctx) raise(NADMM_ECONFIG, "all local shards must share one context");
-            if (shards[i]->d != d) raise(NADMM_ECONFIG, "shard weight dimensions differ");
+        for (int i = 0; i < nl; ++i) {
+            if (!sh[i]) raise(NADMM_ECONFIG, "null shard");
+            shards.push_back(sh[i]);
+        }
+        ctx = shards[0]->ctx;
+        d = shards[0]->d;
+        for (Shard* s : shards) {
+            if (s->ctx != ctx) raise(NADMM_ECONFIG, "all local shards must share one context");
+            if (s->d != d) raise(NADMM_ECONFIG, "shard weight dimensions differ");
         }
         if (comm && comm->ctx->device != ctx->device) raise(NADMM_ECONFIG, "communicator bound to another device");
         NADMM_CUDA(cudaSetDevice(ctx->device));
-        cudaStream_t st = ctx->stream;
-        const int nranks = comm ? comm->nranks : 1, rank = comm ? comm->rank : 0;
-
-        // global worker count (workers are concatenated in rank order)
-        RunBuffers rb;
-        int n_total = n_local;
-        if (comm) {
+        st = ctx->stream;
+        nranks = comm ? comm->nranks : 1;
+        rank = comm ? comm->rank : 0;
+        n_total = n_local;
+        if (comm) {  // global worker count; workers are concatenated in rank order
             int* cnt = rb.get<int>(nranks);
             NADMM_CUDA(cudaMemcpyAsync(cnt + rank, &n_local, sizeof(int), cudaMemcpyHostToDevice, st));
             NADMM_NCCL(ncclAllGather(cnt + rank, cnt, 1, ncclInt, comm->comm, st));
@@ -288,21 +306,22 @@ extern "C" nadmm_status nadmm_admm_run(const nadmm_shard* shards, int32_t n_loca
             n_total = 0;
             for (int v : h) n_total += v;
         }
-
-        const bool sps = cfg.penalty_kind == 1;
-        double* buf = rb.get<double>(d + 1);
-        double* z = rb.get<double>(d);
-        double* pz = rb.get<double>(d);
-        double* zs = sps ? rb.get<double>(d) : nullptr;
-        const int vg = vec_grid(*ctx, d);
-        double* zpart = rb.get<double>(kBlockPartials);
-        double* wpart = rb.get<double>((int64_t)n_local * 6 * kBlockPartials);
-        constexpr int kStats = 8;
-        double* wred = rb.get<double>((int64_t)n_local * 6 + 2);
-        double* fz = rb.get<double>(n_local);
-        double* rstat = rb.get<double>(kStats);
-        double* gstat = rb.get<double>((int64_t)kStats * nranks);
-        std::vector<double*> yh(n_local, nullptr), xs(n_local, nullptr), ys(n_local, nullptr), yhs(n_local, nullptr);
+        sps = cfg.penalty_kind == 1;
+        buf = rb.get<double>(d + 1);
+        z = rb.get<double>(d);
+        pz = rb.get<double>(d);
+        zs = sps ? rb.get<double>(d) : nullptr;
+        vg = vec_grid(*ctx, d);
+        zpart = rb.get<double>(kBlockPartials);
+        wpart = rb.get<double>((int64_t)n_local * 6 * kBlockPartials);
+        wred = rb.get<double>((int64_t)n_local * 6 + 2);
+        fz = rb.get<double>(n_local);
+        rstat = rb.get<double>(kStats);
+        gstat = rb.get<double>((int64_t)kStats * nranks);
+        yh.assign(n_local, nullptr);
+        xs.assign(n_local, nullptr);
+        ys.assign(n_local, nullptr);
+        yhs.assign(n_local, nullptr);
         for (int i = 0; i < n_local; ++i) {
             if (sps) {
                 yh[i] = rb.get<double>(d);
@@ -316,196 +335,266 @@ extern "C" nadmm_status nadmm_admm_run(const nadmm_shard* shards, int32_t n_loca
             NADMM_CUDA(cudaMemsetAsync(s.y, 0, sizeof(double) * d, st));
             if (s.cache_at == Shard::kAtX) s.cache_at = Shard::kNone;
         }
-        std::vector<double> rho(n_local, cfg.rho0);
-        std::vector<double> hstat((size_t)kStats * nranks);
-        std::vector<double> hred((size_t)n_local * 6 + 2);
-
-        cudaEvent_t ev_start, ev_now;
+        rho.assign(n_local, cfg.rho0);
+        hstat.assign((size_t)kStats * nranks, 0.0);
+        hred.assign((size_t)n_local * 6 + 2, 0.0);
         NADMM_CUDA(cudaEventCreate(&ev_start));
         NADMM_CUDA(cudaEventCreate(&ev_now));
         NADMM_CUDA(cudaEventRecord(ev_start, st));
-        int k = 0, snap_it = 0;
-        bool conv = false;
-        for (int it = 0; it < cfg.max_outer_iters; ++it) {
-            // (1) scatter z / solve / gather, one worker at a time on this GPU
-            int inner = 0, cg_sum = 0, fe_sum = 0, flags = 0;
-            for (int i = 0; i < n_local; ++i) {
-                Shard& s = *shards[i];
-                NADMM_CUDA(cudaMemcpyAsync(s.z, z, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
-                SolveResult r = device_newton_solve(s, ncfg, 0.0, true, rho[i], cfg.inner_iters);
-                if (r.error) raise((nadmm_status)r.error, "worker inner solve failed");
-                inner += r.iterations;
-                cg_sum += r.cg_sum;
-                fe_sum += r.fe_sum;
-                flags |= r.flags;
-            }
-            // (2) consensus sum + one allreduce
-            LocalPtrs lp{};
-            lp.n = n_local;
-            double rho_sum = 0.0;
-            for (int i = 0; i < n_local; ++i) {
-                lp.x[i] = shards[i]->x;
-                lp.y[i] = shards[i]->y;
-                lp.rho[i] = rho[i];
-                rho_sum += rho[i];
-            }
-            k_local_sum<<<vg, 256, 0, st>>>(d, lp, rho_sum, buf);
+    }
+
+    ~AdmmRun() {
+        if (ev_start) cudaEventDestroy(ev_start);
+        if (ev_now) cudaEventDestroy(ev_now);
+    }
+
+    // One outer iteration (solve, gather, z, y, penalty, metrics).
+    void iterate(nadmm_metrics_row* row) {
+        int inner = 0, cg_sum = 0, fe_sum = 0, flags = 0;
+        for (int i = 0; i < n_local; ++i) {  // (1) scatter z / solve / gather
+            Shard& s = *shards[i];
+            NADMM_CUDA(cudaMemcpyAsync(s.z, z, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+            SolveResult r = device_newton_solve(s, ncfg, 0.0, true, rho[i], cfg.inner_iters);
+            if (r.error) raise((nadmm_status)r.error, "worker inner solve failed");
+            inner += r.iterations;
+            cg_sum += r.cg_sum;
+            fe_sum += r.fe_sum;
+            flags |= r.flags;
+        }
+        LocalPtrs lp{};  // (2) consensus sum + one allreduce
+        lp.n = n_local;
+        double rho_sum = 0.0;
+        for (int i = 0; i < n_local; ++i) {
+            lp.x[i] = shards[i]->x;
+            lp.y[i] = shards[i]->y;
+            lp.rho[i] = rho[i];
+            rho_sum += rho[i];
+        }
+        k_local_sum<<<vg, 256, 0, st>>>(d, lp, rho_sum, buf);
+        NADMM_LAUNCH_CHECK();
+        ctx->stats.kernel_launches++;
+        if (comm) NADMM_NCCL(ncclAllReduce(buf, buf, d + 1, ncclDouble, ncclSum, comm->comm, st));
+        k_z_update<<<vg, 256, 0, st>>>(d, buf, cfg.lambda, z, pz, zpart);  // (3) z, y, residual partials
+        NADMM_LAUNCH_CHECK();
+        ctx->stats.kernel_launches++;
+        for (int i = 0; i < n_local; ++i) {
+            Shard& s = *shards[i];
+            k_worker_update<<<vg, 256, 0, st>>>(d, rho[i], s.x, s.y, sps ? yh[i] : nullptr, z, pz,
+                                                wpart + (int64_t)i * 6 * kBlockPartials);
             NADMM_LAUNCH_CHECK();
             ctx->stats.kernel_launches++;
-            if (comm) NADMM_NCCL(ncclAllReduce(buf, buf, d + 1, ncclDouble, ncclSum, comm->comm, st));
-            // (3) z, y, y_hat, residual partials
-            k_z_update<<<vg, 256, 0, st>>>(d, buf, cfg.lambda, z, pz, zpart);
-            NADMM_LAUNCH_CHECK();
+        }
+        ++k;
+        if (cfg.eval_objective)  // F_i(z) of the global objective (Eq. (5)) for the metrics stream
+            for (int i = 0; i < n_local; ++i) op_value(*shards[i], z, fz + i, 0, nullptr);
+        for (int i = 0; i < n_local; ++i) {
+            k_reduce_groups<<<4, 32, 0, st>>>(wpart + (int64_t)i * 6 * kBlockPartials, vg, 4, wred + (int64_t)i * 6);
             ctx->stats.kernel_launches++;
-            for (int i = 0; i < n_local; ++i) {
-                Shard& s = *shards[i];
-                k_worker_update<<<vg, 256, 0, st>>>(d, rho[i], s.x, s.y, sps ? yh[i] : nullptr, z, pz,
-                                                    wpart + (int64_t)i * 6 * kBlockPartials);
-                NADMM_LAUNCH_CHECK();
-                ctx->stats.kernel_launches++;
-            }
-            ++k;
-            // local F_i(z) (global objective of Eq. (5)) for the metrics stream
-            if (cfg.eval_objective) {
-                for (int i = 0; i < n_local; ++i) {
-                    Shard& s = *shards[i];
-                    op_value(s, z, fz + i, 0, nullptr);
-                }
-            }
-            // per-worker partial groups -> scalars
-            for (int i = 0; i < n_local; ++i) {
-                k_reduce_groups<<<4, 32, 0, st>>>(wpart + (int64_t)i * 6 * kBlockPartials, vg, 4, wred + (int64_t)i * 6);
-                ctx->stats.kernel_launches++;
-            }
-            k_reduce_groups<<<1, 32, 0, st>>>(zpart, vg, 1, wred + (int64_t)n_local * 6);
-            ctx->stats.kernel_launches++;
-            NADMM_LAUNCH_CHECK();
-            std::vector<double> hfz(n_local, 0.0);
-            NADMM_CUDA(cudaMemcpyAsync(hred.data(), wred, sizeof(double) * hred.size(), cudaMemcpyDeviceToHost, st));
-            if (cfg.eval_objective)
-                NADMM_CUDA(cudaMemcpyAsync(hfz.data(), fz, sizeof(double) * n_local, cudaMemcpyDeviceToHost, st));
+        }
+        k_reduce_groups<<<1, 32, 0, st>>>(zpart, vg, 1, wred + (int64_t)n_local * 6);
+        ctx->stats.kernel_launches++;
+        NADMM_LAUNCH_CHECK();
+        std::vector<double> hfz(n_local, 0.0);
+        NADMM_CUDA(cudaMemcpyAsync(hred.data(), wred, sizeof(double) * hred.size(), cudaMemcpyDeviceToHost, st));
+        if (cfg.eval_objective)
+            NADMM_CUDA(cudaMemcpyAsync(hfz.data(), fz, sizeof(double) * n_local, cudaMemcpyDeviceToHost, st));
+        NADMM_CUDA(cudaStreamSynchronize(st));
+        // rank scalars: sum|x_i|^2, max|y_i|^2, max primal_i, max dual_i, sum primal^2, sum dual^2, sum F_i, |z|^2
+        double rs[kStats] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i = 0; i < n_local; ++i) {
+            const double* w = hred.data() + (int64_t)i * 6;
+            const double prim = std::sqrt(w[0]), dual = std::sqrt(w[1]);
+            rs[0] += w[2];
+            rs[1] = std::max(rs[1], w[3]);
+            rs[2] = std::max(rs[2], prim);
+            rs[3] = std::max(rs[3], dual);
+            rs[4] += w[0];
+            rs[5] += w[1];
+            rs[6] += hfz[i];
+            if (std::isnan(prim) || std::isnan(dual)) rs[2] = NAN;
+        }
+        rs[7] = hred[(size_t)n_local * 6];
+        if (comm) {
+            NADMM_CUDA(cudaMemcpyAsync(rstat, rs, sizeof rs, cudaMemcpyHostToDevice, st));
+            NADMM_NCCL(ncclAllGather(rstat, gstat, kStats, ncclDouble, comm->comm, st));
+            NADMM_CUDA(cudaMemcpyAsync(hstat.data(), gstat, sizeof(double) * hstat.size(), cudaMemcpyDeviceToHost, st));
             NADMM_CUDA(cudaStreamSynchronize(st));
-            // rank scalars: sum|x_i|^2, max|y_i|^2, max primal_i, max dual_i, sum primal^2, sum dual^2, sum F_i
-            double rs[kStats] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int i = 0; i < n_local; ++i) {
-                const double* w = hred.data() + (int64_t)i * 6;
-                const double prim = std::sqrt(w[0]), dual = std::sqrt(w[1]);
-                rs[0] += w[2];
-                rs[1] = std::max(rs[1], w[3]);
-                rs[2] = std::max(rs[2], prim);
-                rs[3] = std::max(rs[3], dual);
-                rs[4] += w[0];
-                rs[5] += w[1];
-                rs[6] += hfz[i];
-                if (std::isnan(prim) || std::isnan(dual)) rs[2] = NAN;
-            }
-            rs[7] = hred[(size_t)n_local * 6];  // |z|^2
-            if (comm) {
-                NADMM_CUDA(cudaMemcpyAsync(rstat, rs, sizeof rs, cudaMemcpyHostToDevice, st));
-                NADMM_NCCL(ncclAllGather(rstat, gstat, kStats, ncclDouble, comm->comm, st));
-                NADMM_CUDA(cudaMemcpyAsync(hstat.data(), gstat, sizeof(double) * hstat.size(), cudaMemcpyDeviceToHost, st));
-                NADMM_CUDA(cudaStreamSynchronize(st));
-            } else {
-                std::memcpy(hstat.data(), rs, sizeof rs);
-            }
-            double sx = 0.0, ymax = 0.0, pmax = 0.0, dmax = 0.0, psq = 0.0, dsq = 0.0, F = 0.0;
-            for (int r = 0; r < nranks; ++r) {  // rank order: deterministic combination
-                const double* h = hstat.data() + (size_t)r * kStats;
-                sx += h[0];
-                ymax = std::max(ymax, h[1]);
-                pmax = std::max(pmax, h[2]);
-                dmax = std::max(dmax, h[3]);
-                psq += h[4];
-                dsq += h[5];
-                F += h[6];
-                if (std::isnan(h[2])) pmax = NAN;
-            }
-            const double zz = hstat[7];
-            // tolerances, squared norms unless standard_norms
-            double a = sx, b = n_total * zz, c = ymax;
-            if (cfg.standard_norms) {
-                a = std::sqrt(sx);
-                b = std::sqrt((double)n_total) * std::sqrt(zz);
-                c = std::sqrt(ymax);
-            }
-            const double eps_pri = std::sqrt((double)n_total) * cfg.eps_abs + cfg.eps_rel * std::max(a, b);
-            const double eps_dual = std::sqrt((double)d) * cfg.eps_abs + cfg.eps_rel * c;
-            conv = k >= 1 && pmax <= eps_pri && dmax <= eps_dual;  // has_converged
-            // (4) spectral penalty selection every T_f iterations against the last snapshot
-            if (sps && k - snap_it >= cfg.update_period) {
-                for (int i = 0; i < n_local; ++i) {
-                    Shard& s = *shards[i];
-                    double* part = wpart + (int64_t)i * 6 * kBlockPartials;
-                    k_sps_dots<<<vg, 256, 0, st>>>(d, s.x, xs[i], yh[i], yhs[i], z, zs, s.y, ys[i], part);
-                    k_reduce_groups<<<6, 32, 0, st>>>(part, vg, 6, wred + (int64_t)i * 6);
-                    ctx->stats.kernel_launches += 2;
-                }
-                NADMM_LAUNCH_CHECK();
-                NADMM_CUDA(cudaMemcpyAsync(hred.data(), wred, sizeof(double) * n_local * 6, cudaMemcpyDeviceToHost, st));
-                NADMM_CUDA(cudaStreamSynchronize(st));
-                for (int i = 0; i < n_local; ++i) {
-                    const double* w = hred.data() + (int64_t)i * 6;
-                    double ah = 0.0, bh = 0.0;
-                    const bool xo = spectral_side(w[0], w[1], w[2], cfg.eps_cor, &ah);
-                    const bool zo = spectral_side(w[3], w[4], w[5], cfg.eps_cor, &bh);
-                    double r = rho[i];
-                    if (xo && zo)
-                        r = std::sqrt(ah * bh);
-                    else if (xo)
-                        r = std::sqrt(ah);
-                    else if (zo)
-                        r = std::sqrt(bh);
-                    rho[i] = std::min(std::max(r, cfg.rho_min), cfg.rho_max);
-                    Shard& s = *shards[i];
-                    NADMM_CUDA(cudaMemcpyAsync(xs[i], s.x, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
-                    NADMM_CUDA(cudaMemcpyAsync(ys[i], s.y, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
-                    NADMM_CUDA(cudaMemcpyAsync(yhs[i], yh[i], sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
-                }
-                NADMM_CUDA(cudaMemcpyAsync(zs, z, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
-                snap_it = k;
-            }
-            NADMM_CUDA(cudaEventRecord(ev_now, st));
-            NADMM_CUDA(cudaEventSynchronize(ev_now));
-            float ms = 0.f;
-            NADMM_CUDA(cudaEventElapsedTime(&ms, ev_start, ev_now));
-            double theta = NAN;
-            const double Fz = cfg.eval_objective ? F + 0.5 * cfg.lambda * zz : NAN;
-            if (cfg.eval_objective && cfg.f_star > 0.0) theta = (Fz - cfg.f_star) / cfg.f_star;
-            if (rows && it < row_cap) {
-                nadmm_metrics_row& m = rows[it];
-                m.iteration = k;
-                m.wall_seconds = ms * 1e-3;
-                m.train_objective = Fz;
-                m.theta = theta;
-                m.primal_norm = std::sqrt(psq);
-                m.dual_norm = std::sqrt(dsq);
-                m.eps_pri = eps_pri;
-                m.eps_dual = eps_dual;
-                m.inner_iterations = inner;
-                m.cg_iters = cg_sum;
-                m.fn_evals = fe_sum;
-                m.flags = flags;
-                double rsum = 0.0;
-                for (double v : rho) rsum += v;
-                m.rho_mean = rsum / n_local;
-                m.messages = 2LL * n_total * k;
-            }
-            if (conv) break;
-            if (cfg.theta_stop > 0.0 && !std::isnan(theta) && theta <= cfg.theta_stop) break;
+        } else {
+            std::memcpy(hstat.data(), rs, sizeof rs);
         }
-        cudaEventDestroy(ev_start);
-        cudaEventDestroy(ev_now);
-        if (z_out) {
-            NADMM_CUDA(cudaMemcpyAsync(z_out, z, sizeof(double) * d, cudaMemcpyDeviceToHost, st));
+        double sx = 0.0, ymax = 0.0, pmax = 0.0, dmax = 0.0, psq = 0.0, dsq = 0.0, F = 0.0;
+        for (int r = 0; r < nranks; ++r) {  // rank order: deterministic combination
+            const double* h = hstat.data() + (size_t)r * kStats;
+            sx += h[0];
+            ymax = std::max(ymax, h[1]);
+            pmax = std::max(pmax, h[2]);
+            dmax = std::max(dmax, h[3]);
+            psq += h[4];
+            dsq += h[5];
+            F += h[6];
+            if (std::isnan(h[2])) pmax = NAN;
         }
+        const double zz = hstat[7];
+        // tolerances, squared norms unless standard_norms
+        double a = sx, b = n_total * zz, c = ymax;
+        if (cfg.standard_norms) {
+            a = std::sqrt(sx);
+            b = std::sqrt((double)n_total) * std::sqrt(zz);
+            c = std::sqrt(ymax);
+        }
+        const double eps_pri = std::sqrt((double)n_total) * cfg.eps_abs + cfg.eps_rel * std::max(a, b);
+        const double eps_dual = std::sqrt((double)d) * cfg.eps_abs + cfg.eps_rel * c;
+        conv = k >= 1 && pmax <= eps_pri && dmax <= eps_dual;  // has_converged
+        if (sps && k - snap_it >= cfg.update_period) spectral();  // (4) SPS against the last snapshot
+        NADMM_CUDA(cudaEventRecord(ev_now, st));
+        NADMM_CUDA(cudaEventSynchronize(ev_now));
+        float ms = 0.f;
+        NADMM_CUDA(cudaEventElapsedTime(&ms, ev_start, ev_now));
+        double theta = NAN;
+        const double Fz = cfg.eval_objective ? F + 0.5 * cfg.lambda * zz : NAN;
+        if (cfg.eval_objective && cfg.f_star > 0.0) theta = (Fz - cfg.f_star) / cfg.f_star;
+        if (row) {
+            nadmm_metrics_row& m = *row;
+            m.iteration = k;
+            m.wall_seconds = ms * 1e-3;
+            m.train_objective = Fz;
+            m.theta = theta;
+            m.primal_norm = std::sqrt(psq);
+            m.dual_norm = std::sqrt(dsq);
+            m.eps_pri = eps_pri;
+            m.eps_dual = eps_dual;
+            m.inner_iterations = inner;
+            m.cg_iters = cg_sum;
+            m.fn_evals = fe_sum;
+            m.flags = flags;
+            double rsum = 0.0;
+            for (double v : rho) rsum += v;
+            m.rho_mean = rsum / n_local;
+            m.messages = 2LL * n_total * k;
+        }
+        if (conv && !cfg.ignore_convergence) stop = true;
+        if (cfg.theta_stop > 0.0 && !std::isnan(theta) && theta <= cfg.theta_stop) stop = true;
+        if (k >= cfg.max_outer_iters) stop = true;
+    }
+
+    void spectral() {
+        for (int i = 0; i < n_local; ++i) {
+            Shard& s = *shards[i];
+            double* part = wpart + (int64_t)i * 6 * kBlockPartials;
+            k_sps_dots<<<vg, 256, 0, st>>>(d, s.x, xs[i], yh[i], yhs[i], z, zs, s.y, ys[i], part);
+            k_reduce_groups<<<6, 32, 0, st>>>(part, vg, 6, wred + (int64_t)i * 6);
+            ctx->stats.kernel_launches += 2;
+        }
+        NADMM_LAUNCH_CHECK();
+        NADMM_CUDA(cudaMemcpyAsync(hred.data(), wred, sizeof(double) * n_local * 6, cudaMemcpyDeviceToHost, st));
+        NADMM_CUDA(cudaStreamSynchronize(st));
+        for (int i = 0; i < n_local; ++i) {
+            const double* w = hred.data() + (int64_t)i * 6;
+            double ah = 0.0, bh = 0.0;
+            const bool xo = spectral_side(w[0], w[1], w[2], cfg.eps_cor, &ah);
+            const bool zo = spectral_side(w[3], w[4], w[5], cfg.eps_cor, &bh);
+            double r = rho[i];
+            if (xo && zo)
+                r = std::sqrt(ah * bh);
+            else if (xo)
+                r = std::sqrt(ah);
+            else if (zo)
+                r = std::sqrt(bh);
+            rho[i] = std::min(std::max(r, cfg.rho_min), cfg.rho_max);
+            Shard& s = *shards[i];
+            NADMM_CUDA(cudaMemcpyAsync(xs[i], s.x, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+            NADMM_CUDA(cudaMemcpyAsync(ys[i], s.y, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+            NADMM_CUDA(cudaMemcpyAsync(yhs[i], yh[i], sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+        }
+        NADMM_CUDA(cudaMemcpyAsync(zs, z, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+        snap_it = k;
+    }
+
+    int step(int n, nadmm_metrics_row* rows, int row_cap) {
+        int done = 0;
+        while (done < n && !stop) {
+            iterate(rows && done < row_cap ? rows + done : nullptr);
+            ++done;
+        }
+        return done;
+    }
+
+    void result(double* z_out, double* rho_out) {
+        if (z_out) NADMM_CUDA(cudaMemcpyAsync(z_out, z, sizeof(double) * d, cudaMemcpyDeviceToHost, st));
         NADMM_CUDA(cudaStreamSynchronize(st));
         if (rho_out)
             for (int i = 0; i < n_local; ++i) rho_out[i] = rho[i];
-        if (iterations) *iterations = k;
-        if (converged_out) *converged_out = conv ? 1 : 0;
+    }
+};
+
+}  // namespace nadmm
+
+struct nadmm_admm_s : nadmm::AdmmRun {
+    using AdmmRun::AdmmRun;
+};
+
+extern "C" {
+
+nadmm_status nadmm_admm_create(const nadmm_shard* shards, int32_t n_local, nadmm_comm comm, const nadmm_admm_cfg* cfg,
+                               nadmm_admm* out) {
+    try {
+        if (!out) raise(NADMM_ECONFIG, "null output");
+        (void)cudaGetLastError();
+        *out = new nadmm_admm_s(shards, n_local, comm, cfg);
         return NADMM_OK;
     } catch (const Error& e) {
         set_last_error(e.what());
         return e.code;
     }
 }
+
+nadmm_status nadmm_admm_step(nadmm_admm run, int32_t n_iters, nadmm_metrics_row* rows, int32_t row_cap,
+                             int32_t* done, int32_t* finished) {
+    try {
+        if (!run) raise(NADMM_ECONFIG, "null run");
+        (void)cudaGetLastError();  // clear stale errors left by other libraries in this thread
+        NADMM_CUDA(cudaSetDevice(run->ctx->device));
+        const int n = run->step(n_iters, rows, row_cap);
+        if (done) *done = n;
+        if (finished) *finished = run->stop ? 1 : 0;
+        return NADMM_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    }
+}
+
+nadmm_status nadmm_admm_result(nadmm_admm run, double* z_out, double* rho_out, int32_t* iterations,
+                               int32_t* converged) {
+    try {
+        if (!run) raise(NADMM_ECONFIG, "null run");
+        (void)cudaGetLastError();  // clear stale errors left by other libraries in this thread
+        NADMM_CUDA(cudaSetDevice(run->ctx->device));
+        run->result(z_out, rho_out);
+        if (iterations) *iterations = run->k;
+        if (converged) *converged = run->conv ? 1 : 0;
+        return NADMM_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    }
+}
+
+nadmm_status nadmm_admm_free(nadmm_admm run) {
+    delete run;
+    return NADMM_OK;
+}
+
+nadmm_status nadmm_admm_run(const nadmm_shard* shards, int32_t n_local, nadmm_comm comm, const nadmm_admm_cfg* cfg,
+                            double* z_out, double* rho_out, nadmm_metrics_row* rows, int32_t row_cap,
+                            int32_t* iterations, int32_t* converged) {
+    nadmm_admm run = nullptr;
+    nadmm_status rc = nadmm_admm_create(shards, n_local, comm, cfg, &run);
+    if (rc) return rc;
+    rc = nadmm_admm_step(run, run->cfg.max_outer_iters, rows, row_cap, nullptr, nullptr);
+    if (!rc) rc = nadmm_admm_result(run, z_out, rho_out, iterations, converged);
+    nadmm_admm_free(run);
+    return rc;
+}
+
+}  // extern "C"

@@ -20,6 +20,9 @@ thread_local std::string g_last_error;
 template <typename F>
 nadmm_status guard(F&& f) {
     try {
+        // Launch checks read cudaGetLastError(); clear stale errors other libraries left in this
+        // thread (e.g. a framework probing an external stream) so they are not attributed to us.
+        (void)cudaGetLastError();
         f();
         return NADMM_OK;
     } catch (const Error& e) {
@@ -85,6 +88,7 @@ void alloc_work(Shard& s) {
         s.part_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(2LL * s.ctx->num_sms, cap));
         s.part = dev_alloc<double>(s, s.part_chunks * s.d);
     }
+    dmma_setup(s);
     s.blk = dev_alloc<double>(s, (int64_t)kSlotCount * kBlockPartials);
     NADMM_CUDA(cudaMemsetAsync(s.blk, 0, sizeof(double) * kSlotCount * kBlockPartials, s.ctx->stream));
     for (double** v : {&s.x, &s.g, &s.pd, &s.r, &s.dv, &s.hd, &s.z, &s.y, &s.t, &s.tmp, &s.gbase, &s.cache_x}) {

@@ -17,7 +17,7 @@ namespace nadmm {
 void op_cache_grad(Shard& s, const double* w, const int32_t* guard) {
     if (dmma_supported(s)) {
         dmma_pass(s, kModeCache, w, guard);
-        finalize_partials(s, s.part_chunks, kXtuGrad, w, s.gbase, nullptr, 0, guard, nullptr);
+        finalize_partials(s, s.last_chunks,kXtuGrad, w, s.gbase, nullptr, 0, guard, nullptr);
     } else {
         rows_pass(s, kModeCache, w, guard);
         xtu_pass(s, kXtuGrad, w, s.gbase, nullptr, 0, guard);
@@ -29,16 +29,16 @@ int op_hv(Shard& s, const double* v, double* out, const double* dotvec, int dot_
     HvTimer* tm = (s.capture_timing && s.hv_timer_site >= 0 && s.hv_timer_site < (int)s.hv_timers.size())
                       ? &s.hv_timers[s.hv_timer_site]
                       : nullptr;
-    if (tm) NADMM_CUDA(cudaEventRecord(tm->start, s.ctx->stream));
+    if (tm) NADMM_CUDA(cudaEventRecordWithFlags(tm->start, s.ctx->stream, cudaEventRecordExternal));
     int g = 0;
     if (dmma_supported(s)) {
         dmma_pass(s, kModeHv, v, guard);
-        if (tm) NADMM_CUDA(cudaEventRecord(tm->stop, s.ctx->stream));
-        finalize_partials(s, s.part_chunks, kXtuHv, v, out, dotvec, dot_slot, guard, &g);
+        if (tm) NADMM_CUDA(cudaEventRecordWithFlags(tm->stop, s.ctx->stream, cudaEventRecordExternal));
+        finalize_partials(s, s.last_chunks,kXtuHv, v, out, dotvec, dot_slot, guard, &g);
     } else {
         rows_pass(s, kModeHv, v, guard);
         g = xtu_pass(s, kXtuHv, v, out, dotvec, dot_slot, guard);
-        if (tm) NADMM_CUDA(cudaEventRecord(tm->stop, s.ctx->stream));
+        if (tm) NADMM_CUDA(cudaEventRecordWithFlags(tm->stop, s.ctx->stream, cudaEventRecordExternal));
     }
     return g;
 }

@@ -129,6 +129,8 @@ struct Shard {
     int part_chunks = 0;
     double* blk = nullptr;
     int rows_grid = 0;  // blocks of the last rows pass (partials count)
+    int last_chunks = 0;    // split-K partial chunks written by the last fused DMMA pass
+    int dmma_clusters = 0;  // co-resident clusters of the fused DMMA pass (0: path unavailable)
     // memo: the point the device cache (L0, P, rowM, rowA, gbase, loss) was built at: the solver
     // iterate s.x, or s.cache_x holding the host vector of the last model-level call
     enum CachePoint { kNone = 0, kAtX = 1, kAtHost = 2 } cache_at = kNone;
@@ -185,6 +187,8 @@ void op_predict(Shard& s, const double* w);
 
 // ---- dense fast path (kernels_dmma.cu) ----
 bool dmma_supported(const Shard& s);
+// Once per shard, outside stream capture: kernel attributes + co-resident cluster count.
+void dmma_setup(Shard& s);
 void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
 
 }  // namespace nadmm
