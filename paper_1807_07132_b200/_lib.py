@@ -114,10 +114,35 @@ SIGNATURES = {
 _lib = None
 
 
+def _preload_nccl() -> None:
+    """Bind libnccl.so.2 to the newest NCCL in the environment before our library resolves it.
+
+    The library links against the libnccl.so.2 soname. When PyTorch is in the process it needs its
+    own (newer) NCCL; loading the system copy first would break a later `import torch`. Preloading the
+    wheel's NCCL (RTLD_GLOBAL) makes both resolve to one, ABI-compatible, copy."""
+    import importlib.util
+
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    if not spec or not spec.submodule_search_locations:
+        return
+    for loc in spec.submodule_search_locations:
+        cand = Path(loc) / "lib" / "libnccl.so.2"
+        if cand.exists():
+            try:
+                C.CDLL(str(cand), mode=C.RTLD_GLOBAL)
+            except OSError:
+                pass
+            return
+
+
 def lib() -> C.CDLL:
     """Load the CUDA library (fails loudly when it was not built)."""
     global _lib
     if _lib is None:
+        _preload_nccl()
         if not LIB_PATH.exists():
             raise ImportError(f"{LIB_PATH} missing: build it with paper_1807_07132_b200/build.sh "
                               "(or __graft_entry__.build()); there is no CPU fallback")

@@ -75,7 +75,8 @@ void validate_common(int64_t n, int64_t p, const int32_t* labels, int32_t C) {
 }
 
 void alloc_work(Shard& s) {
-    const int64_t nk = s.n * s.K;
+    // row padding: the fused pass TMA-loads whole 16-row tiles of P and labels
+    const int64_t nk = (s.n + kRowPad) * s.K;
     s.L0 = dev_alloc<double>(s, nk);
     s.P = dev_alloc<double>(s, nk);
     s.U = dev_alloc<double>(s, nk);
@@ -284,7 +285,8 @@ nadmm_status nadmm_shard_dense(nadmm_ctx ctx, const double* X, int64_t n, int64_
         s->ldx = p;
         s->X = dev_alloc<double>(*s, n * p);
         upload(s->X, X, sizeof(double) * n * p, ctx->stream);
-        s->labels = dev_alloc<int32_t>(*s, n);
+        s->labels = dev_alloc<int32_t>(*s, n + kRowPad);
+        NADMM_CUDA(cudaMemsetAsync(s->labels, 0, sizeof(int32_t) * (n + kRowPad), ctx->stream));
         upload(s->labels, labels, sizeof(int32_t) * n, ctx->stream);
         alloc_work(*s);
         NADMM_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -380,7 +382,8 @@ nadmm_status nadmm_shard_csr(nadmm_ctx ctx, const int64_t* indptr, const int32_t
         upload(s->cptr, colptr.data(), sizeof(int64_t) * (p + 1), ctx->stream);
         upload(s->crow, crow.data(), sizeof(int32_t) * nnz, ctx->stream);
         upload(s->cval, cval.data(), sizeof(double) * nnz, ctx->stream);
-        s->labels = dev_alloc<int32_t>(*s, n);
+        s->labels = dev_alloc<int32_t>(*s, n + kRowPad);
+        NADMM_CUDA(cudaMemsetAsync(s->labels, 0, sizeof(int32_t) * (n + kRowPad), ctx->stream));
         upload(s->labels, labels, sizeof(int32_t) * n, ctx->stream);
         alloc_work(*s);
         NADMM_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -30,6 +30,7 @@ struct Error : std::runtime_error {
 #define NADMM_LAUNCH_CHECK() NADMM_CUDA(cudaGetLastError())
 
 constexpr int kMaxClasses = 128;   // C - 1 <= kMaxClasses on the SIMT paths
+constexpr int kRowPad = 32;        // extra rows allocated in row-indexed work buffers (tile over-read)
 constexpr int kBlockPartials = 1024;  // max blocks writing partials in one reduction slot
 
 // ---------------------------------------------------------------------------------------------
