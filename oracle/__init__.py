@@ -76,6 +76,15 @@ def _cfg(cfg) -> np.ndarray:
     return _f64(DEFAULT_NEWTON if cfg is None else cfg)
 
 
+def _put(ptr, n: int, values) -> None:
+    """Write a length-n vector into a ctypes double* (callback output)."""
+    np.ctypeslib.as_array(ptr, (n,))[:] = np.asarray(values, dtype=np.float64)
+
+
+def _get(ptr, n: int) -> np.ndarray:
+    return np.ctypeslib.as_array(ptr, (n,)).copy()
+
+
 def _trace_rows(buf: np.ndarray, n: int):
     return [dict(zip(TRACE_FIELDS, row.tolist())) for row in buf[: min(n, len(buf))]]
 
@@ -231,7 +240,7 @@ class Port:
     def cg_solve(self, apply, g, theta: float, max_iters: int):
         g = _f64(g)
         d = len(g)
-        cb = APPLY_FN(lambda i, o, n, u: o.__setitem__(slice(0, n), list(apply(np.ctypeslib.as_array(i, (n,)).copy()))))
+        cb = APPLY_FN(lambda i, o, n, u: _put(o, n, apply(_get(i, n))))
         p = np.zeros(d)
         it, ach, neg = C.c_int(), C.c_double(), C.c_int()
         self._chk(self.lib.nor_cg_solve(cb, None, _dp(g), C.c_int64(d), C.c_double(theta), C.c_int(max_iters),
@@ -243,8 +252,8 @@ class Port:
             _fields_ = [("value", VALUE_FN), ("grad", GRAD_FN), ("hvp", HVP_FN), ("user", VP), ("d", C.c_int64)]
 
         keep = [VALUE_FN(lambda x, n, u: float(value(np.ctypeslib.as_array(x, (n,)).copy())))]
-        keep.append(GRAD_FN(lambda x, g, n, u: g.__setitem__(slice(0, n), list(grad(np.ctypeslib.as_array(x, (n,)).copy())))) if grad else GRAD_FN())
-        keep.append(HVP_FN(lambda x, v, o, n, u: o.__setitem__(slice(0, n), list(hvp(np.ctypeslib.as_array(x, (n,)).copy(), np.ctypeslib.as_array(v, (n,)).copy())))) if hvp else HVP_FN())
+        keep.append(GRAD_FN(lambda x, g, n, u: _put(g, n, grad(_get(x, n)))) if grad else GRAD_FN())
+        keep.append(HVP_FN(lambda x, v, o, n, u: _put(o, n, hvp(_get(x, n), _get(v, n)))) if hvp else HVP_FN())
         o = Obj(keep[0], keep[1], keep[2], None, d)
         return o, keep
 
@@ -386,7 +395,7 @@ class Ref:
     def cg_solve(self, apply, g, theta, max_iters):
         g = _f64(g)
         d = len(g)
-        cb = APPLY_FN(lambda i, o, n, u: o.__setitem__(slice(0, n), list(apply(np.ctypeslib.as_array(i, (n,)).copy()))))
+        cb = APPLY_FN(lambda i, o, n, u: _put(o, n, apply(_get(i, n))))
         p = np.zeros(d)
         it, ach, neg = C.c_int(), C.c_double(), C.c_int()
         self._chk(self.lib.nadmm_ref_cg_solve(cb, None, _dp(g), C.c_int64(d), C.c_double(theta), C.c_int(max_iters),
@@ -406,8 +415,8 @@ class Ref:
         x0 = _f64(x0)
         d = len(x0)
         v = VALUE_FN(lambda x, n, u: float(value(np.ctypeslib.as_array(x, (n,)).copy())))
-        gr = GRAD_FN(lambda x, g, n, u: g.__setitem__(slice(0, n), list(grad(np.ctypeslib.as_array(x, (n,)).copy()))))
-        hv = HVP_FN(lambda x, vv, o, n, u: o.__setitem__(slice(0, n), list(hvp(np.ctypeslib.as_array(x, (n,)).copy(), np.ctypeslib.as_array(vv, (n,)).copy()))))
+        gr = GRAD_FN(lambda x, g, n, u: _put(g, n, grad(_get(x, n))))
+        hv = HVP_FN(lambda x, vv, o, n, u: _put(o, n, hvp(_get(x, n), _get(vv, n))))
         x = np.zeros(d)
         tr = np.zeros((trace_cap, 9))
         nt, conv, gn = C.c_int(), C.c_int(), C.c_double()
