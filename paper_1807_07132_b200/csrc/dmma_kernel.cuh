@@ -1,5 +1,18 @@
-// Fused single-pass FP64 DMMA kernel (device code). See kernels_dmma.cu for the design notes and
-// the host-side layout selection / launch.
+// Fused single-pass FP64 DMMA kernel (device code), warp-specialised. See kernels_dmma.cu for the
+// design notes and the host-side layout selection / launch.
+//
+// Warp roles in a CTA (blockDim = 32 * (NC + kDmmaAux)):
+//   * NC compute warps own W = 8*MT features each: phase A (partial logits, DMMA + DFMA) and phase B
+//     (X^T U accumulation, DMMA + DFMA), software-pipelined one tile apart (A(i+1) then B(i)), so the
+//     tensor pipe keeps issuing while tile i's logits travel through the cluster.
+//   * one pusher warp: sums the compute warps' partials (ascending warp order) and pushes the CTA
+//     partial to every CTA of the cluster (st.async + remote mbarrier complete_tx); it runs ahead of
+//     the epilogue by one tile.
+//   * kDmmaEpiWarps epilogue warps: sum the CS partials of a tile in rank order (every CTA derives
+//     bit-identical logits), then one thread per row runs the row epilogue (U, softmax cache, loss,
+//     argmax) in ascending class order, exactly like the SIMT path and the reference.
+//   * one producer warp: TMA (cp.async.bulk) of X row slices, P rows and labels into a STAGES ring.
+// All hand-offs are mbarriers; no block-wide barrier sits on the per-tile critical path.
 #pragma once
 
 #include <cuda.h>
@@ -9,9 +22,6 @@
 namespace nadmm {
 namespace dmma_detail {
 
-// ------------------------------------------------------------------------------------------------
-// PTX helpers
-// ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -29,6 +39,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // try_wait loop (default .acquire.cta semantics; the data it guards lives in shared memory).
@@ -97,16 +111,23 @@ __device__ __forceinline__ void st_async_v2(uint32_t remote_addr, double x, doub
                  : "memory");
 }
 
-__device__ __forceinline__ double hsum16(double v) {  // sum over a 16-lane half warp (fixed tree)
+// Fixed-topology pairwise sum of v[0..n) (n <= N): depth log2(N) instead of a serial chain. The
+// auxiliary warps share the FP64 pipe with the compute warps' DMMAs, so every dependent FP64 op on
+// their critical path costs a pipe turn; trees keep those paths short. Deterministic by construction.
+template <int N>
+__device__ __forceinline__ double tree_sum(double (&v)[N], int n) {
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
+    for (int i = 0; i < N; ++i)
+        if (i >= n) v[i] = 0.0;
+#pragma unroll
+    for (int w = 1; w < N; w *= 2)
+#pragma unroll
+        for (int i = 0; i + w < N; i += 2 * w) v[i] = v[i] + v[i + w];
+    return v[0];
 }
 
-__device__ __forceinline__ double hmax16(double v) {
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
+__device__ __forceinline__ void named_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(threads) : "memory");
 }
 
 }  // namespace dmma_detail
@@ -127,11 +148,33 @@ struct DmmaArgs {
     double* part;  // split-K partials, cluster-major: part[cluster * d + c*p + f]
     double* blk;   // block partial slots (loss / hits), one entry per cluster
     const int32_t* guard;
-    int fs;  // features per CTA (= NW * 8 * MT)
-    int S;   // padded shared row stride (doubles)
+    int fs;  // features per CTA (= NC * 8 * MT)
+    int S;   // padded shared row stride (doubles, even)
 };
 
-constexpr int kDmmaRecvBufs = 3;  // receive buffers: tile i's exchange overlaps tile i+1's phase A
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* local_bar, uint32_t rank) {
+    const uint32_t ra = dmma_detail::mapa(dmma_detail::smem_u32(local_bar), rank);
+    // Relaxed: a credit publishes no data. It only orders our completed reads of the peer-written
+    // buffer before the peer's next st.async into it (the loads' values were consumed already).
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(ra) : "memory");
+}
+
+#ifdef NADMM_DMMA_TRACE
+__device__ long long g_dmma_trace[64][16];  // per-tile clock64 stamps of CTA 0 (profiling builds only)
+#define DMMA_TRACE(i, k) \
+    do { \
+        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (i) < 64) g_dmma_trace[(i)][(k)] = clock64(); \
+    } while (0)
+#else
+#define DMMA_TRACE(i, k) \
+    do { \
+    } while (0)
+#endif
+
+constexpr int kDmmaRecvBufs = 4;  // receive buffers per CTA, flow-controlled by remote credits
+constexpr int kDmmaRedBufs = 2;   // compute-warp partial buffers (pusher frees them)
+constexpr int kDmmaEpiWarps = 2;  // epilogue warps
+constexpr int kDmmaAux = kDmmaEpiWarps + 2;  // + pusher + producer
 
 template <int K>
 struct DmmaSmem {
@@ -139,22 +182,26 @@ struct DmmaSmem {
     static constexpr int KP = (K + 1) & ~1;              // partial row stride (even: 16-byte pairs)
 };
 
-// Shared memory bytes of the kernel's carve-up (host and device agree on it).
-__host__ __device__ inline size_t dmma_smem_bytes(int stages, int bm, int nw, int S, int K, int cs) {
-    const int KS = ((K + 15) / 16) * 16 + 4, KP = (K + 1) & ~1;
-    const size_t dbl = (size_t)stages * bm * S + (size_t)stages * bm * K + 2 + (size_t)nw * bm * KP +
-                       (size_t)kDmmaRecvBufs * cs * bm * KP + (size_t)bm * KS + 64;
-    return sizeof(double) * dbl + 4 * ((size_t)stages * bm + 4) + 8 * (stages + kDmmaRecvBufs + 1);
+// Shared memory bytes of the kernel's carve-up (host and device agree on it). Every region holds an
+// even number of doubles, so all of them stay 16-byte aligned. U buffers: one per stage.
+__host__ __device__ inline size_t dmma_smem_bytes(int stages, int bm, int nc, int S, int K, int cs) {
+    const int KS = ((K + 15) / 16) * 16 + 4, KP = (K + 1) & ~1, KE = (K + 1) & ~1;
+    const size_t dbl = (size_t)stages * bm * S + (size_t)stages * bm * KE + (size_t)kDmmaRedBufs * nc * bm * KP +
+                       (size_t)kDmmaRecvBufs * cs * bm * KP + (size_t)stages * bm * KS + (size_t)kDmmaEpiWarps * bm * KP + 128;
+    const int nbars = 2 * stages + 2 * kDmmaRedBufs + 2 * kDmmaRecvBufs + stages;
+    return sizeof(double) * dbl + 4 * ((size_t)stages * bm + 4) + 8 * (nbars + 1);
 }
 
-template <int MT, int KT, int R, int BM, int STAGES, int MODE>
+// LAG: tiles of phase A in flight ahead of phase B; STAGES = LAG + 2 (A ring + one loading).
+template <int MT, int KT, int R, int BM, int LAG, int MODE>
 __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
     using namespace dmma_detail;
+    constexpr int STAGES = LAG + 2;
     constexpr int K = 8 * KT + R;
-    static_assert(K <= 16, "half-warp epilogue handles up to 16 classes");
-    static_assert(STAGES >= 3, "software pipeline keeps tiles i (phase B), i+1 (phase A), i+2 (loading)");
+    static_assert(BM % 8 == 0 && BM <= 32, "row tile");
     constexpr int KS = DmmaSmem<K>::KS;
     constexpr int KP = DmmaSmem<K>::KP;
+    constexpr int KE = (K + 1) & ~1;  // P rows are loaded K wide; region rounded to an even count
     constexpr int W = 8 * MT;
     constexpr int KSTEP_A = W / 4;
     constexpr bool PHASE_B = (MODE == kModeHv || MODE == kModeCache);
@@ -162,10 +209,11 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
     constexpr bool NEED_Y = (MODE == kModeCache || MODE == kModeValue || MODE == kModePredict);
     constexpr int G = BM / 8;      // row groups in phase A
     constexpr int PART = BM * KP;  // doubles per CTA partial
+    constexpr int EPI_THREADS = 32 * kDmmaEpiWarps;
     if (a.guard && !*a.guard) return;  // uniform across the grid: nothing is pending yet
 
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int nw = blockDim.x >> 5;
+    extern __shared__ __align__(128) double smem[];
+    const int nc = (int)(blockDim.x >> 5) - kDmmaAux;  // compute warps
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gq = lane >> 2, tq = lane & 3;  // fragment row / column-in-quad
     const uint32_t crank = cluster_ctarank(), csize = cluster_nctarank();
@@ -173,293 +221,408 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
     const int S = a.S, fs = a.fs;
     const int64_t p = a.p, n = a.n;
     const int f_cta = (int)crank * fs;  // first feature of this CTA
-    const int fw = warp * W;            // warp slice offset inside the CTA slice
 
     // shared memory carve-up (mirrors dmma_smem_bytes)
-    double* xs = reinterpret_cast<double*>(smem_raw);  // STAGES x BM x S
-    double* ps = xs + (size_t)STAGES * BM * S;         // STAGES x BM x K   (P rows)
-    double* red = ps + (size_t)STAGES * BM * K;        // nw x PART
-    red = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(red) + 15) & ~uintptr_t(15));
-    double* recv = red + (size_t)nw * PART;                   // kDmmaRecvBufs x CS x PART (peers write)
-    double* ut = recv + (size_t)kDmmaRecvBufs * csize * PART;  // BM x KS
-    double* misc = ut + BM * KS;                              // 64 doubles
-    int32_t* ys = reinterpret_cast<int32_t*>(misc + 64);      // STAGES x BM labels
+    double* xs = smem;                                               // STAGES x BM x S
+    double* ps = xs + (size_t)STAGES * BM * S;                       // STAGES x BM x KE (P rows)
+    double* red = ps + (size_t)STAGES * BM * KE;                     // kDmmaRedBufs x nc x PART
+    double* recv = red + (size_t)kDmmaRedBufs * nc * PART;           // kDmmaRecvBufs x CS x PART (peers)
+    double* ut = recv + (size_t)kDmmaRecvBufs * csize * PART;        // STAGES x BM x KS
+    double* lgb = ut + (size_t)STAGES * BM * KS;                     // kDmmaEpiWarps x BM x KP logits
+    double* misc = lgb + (size_t)kDmmaEpiWarps * BM * KP;           // 128 doubles
+    int32_t* ys = reinterpret_cast<int32_t*>(misc + 128);            // STAGES x BM labels
     uint64_t* bars = reinterpret_cast<uint64_t*>(ys + STAGES * BM + 4);
-    bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bars) + 7) & ~uintptr_t(7));
-    uint64_t* rbar = bars + STAGES;  // kDmmaRecvBufs
+    uint64_t* full = bars;                         // STAGES: TMA landed
+    uint64_t* empty = full + STAGES;               // STAGES: stage consumed (nc compute + epilogue warps)
+    uint64_t* red_full = empty + STAGES;           // kDmmaRedBufs: compute partials written (nc warps)
+    uint64_t* red_empty = red_full + kDmmaRedBufs;  // kDmmaRedBufs: pusher done reading (1)
+    uint64_t* rbar = red_empty + kDmmaRedBufs;     // kDmmaRecvBufs: cluster partials received (tx)
+    uint64_t* credit = rbar + kDmmaRecvBufs;       // kDmmaRecvBufs: every CTA consumed its copy (CS)
+    uint64_t* u_full = credit + kDmmaRecvBufs;     // STAGES: U tile ready (epilogue warps)
 
     const int64_t ntiles = (n + BM - 1) / BM;
-    const int my_tiles = cid < ntiles ? (int)((ntiles - 1 - cid) / ncl + 1) : 0;
+    const int T = cid < ntiles ? (int)((ntiles - 1 - cid) / ncl + 1) : 0;  // this cluster's tiles
     const int64_t rem_f = p - f_cta;
     const int valid_f = rem_f <= 0 ? 0 : (rem_f < fs ? (int)rem_f : fs);  // valid features in slice
     const uint32_t row_bytes = (uint32_t)valid_f * 8u;
 
-    // zero the X ring once: padding columns (beyond p) must read as 0, never as garbage
-    for (int i = threadIdx.x; i < STAGES * BM * S; i += blockDim.x) xs[i] = 0.0;
+    for (int i = threadIdx.x; i < STAGES * BM * S; i += blockDim.x) xs[i] = 0.0;  // padding reads 0
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
-        for (int b = 0; b < kDmmaRecvBufs; ++b) mbar_init(&rbar[b], 1);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], (uint32_t)(nc + 1));  // compute warps + the tile's epilogue warp
+            mbar_init(&u_full[s], 1);
+        }
+        for (int b = 0; b < kDmmaRedBufs; ++b) {
+            mbar_init(&red_full[b], (uint32_t)nc);
+            mbar_init(&red_empty[b], 1);
+        }
+        for (int b = 0; b < kDmmaRecvBufs; ++b) {
+            mbar_init(&rbar[b], 1);
+            mbar_init(&credit[b], csize);
+        }
         fence_mbar_init();
     }
     __syncthreads();
     fence_proxy_async();
-    if (csize > 1) cluster_sync_all();  // peers' receive barriers are initialised before any st.async
+    if (csize > 1) cluster_sync_all();  // peers' barriers are initialised before any remote traffic
 
     auto tile_of = [&](int i) -> int64_t { return (int64_t)cid + (int64_t)i * ncl; };
-    auto issue = [&](int i) {  // TMA for the cluster's i-th tile into stage i % STAGES
-        const int stage = i % STAGES;
-        const int64_t r0 = tile_of(i) * BM;
-        const int rows = (n - r0) < BM ? (int)(n - r0) : BM;
-        uint32_t bytes = row_bytes * (uint32_t)rows;
-        if (NEED_P) bytes += BM * K * 8;
-        if (NEED_Y) bytes += BM * 4;
-        mbar_expect_tx(&bars[stage], bytes);
-        if (row_bytes)
-            for (int r = 0; r < rows; ++r)
-                tma_bulk_g2s(xs + ((size_t)stage * BM + r) * S, a.X + (r0 + r) * a.ldx + f_cta, row_bytes, &bars[stage]);
-        if (NEED_P) tma_bulk_g2s(ps + (size_t)stage * BM * K, a.Pin + r0 * K, BM * K * 8, &bars[stage]);
-        if (NEED_Y) tma_bulk_g2s(ys + stage * BM, a.labels + r0, BM * 4, &bars[stage]);
-    };
+    const int role_pusher = nc, role_producer = nc + 1, role_epi0 = nc + 2;
 
-    if (threadIdx.x == 0)
-        for (int i = 0; i < STAGES && i < my_tiles; ++i) issue(i);
-
-    // V slice in registers: B fragments (k = tq, n = gq) and the remainder columns
-    double bv[KSTEP_A][KT > 0 ? KT : 1];
-    double vr[KSTEP_A][R > 0 ? R : 1];
-#pragma unroll
-    for (int s = 0; s < KSTEP_A; ++s) {
-        const int64_t f = (int64_t)f_cta + fw + 4 * s + tq;
-        const bool ok = f < p && fw + 4 * s + tq < fs;
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt) bv[s][kt] = ok ? a.V[(int64_t)(kt * 8 + gq) * p + f] : 0.0;
-#pragma unroll
-        for (int r = 0; r < R; ++r) vr[s][r] = ok ? a.V[(int64_t)(8 * KT + r) * p + f] : 0.0;
-    }
-
-    // phase-B accumulators, resident across all tiles
-    double accb[PHASE_B ? MT : 1][KT > 0 ? KT : 1][2];
-    double accbr[PHASE_B ? MT : 1][R > 0 ? R : 1];
-#pragma unroll
-    for (int m = 0; m < (PHASE_B ? MT : 1); ++m) {
-#pragma unroll
-        for (int kt = 0; kt < (KT > 0 ? KT : 1); ++kt) accb[m][kt][0] = accb[m][kt][1] = 0.0;
-#pragma unroll
-        for (int r = 0; r < (R > 0 ? R : 1); ++r) accbr[m][r] = 0.0;
-    }
-    double loss_acc = 0.0;  // rank-0 CTA: lane 0 of each half warp, rows in tile order
-
-    // ---- phase A of the cluster's i-th tile, then push the CTA partial to every CTA's receive slot ----
-    auto phase_a_and_push = [&](int i) {
-        const int stage = i % STAGES;
-        mbar_wait(&bars[stage], (uint32_t)((i / STAGES) & 1));
-        const double* xt = xs + (size_t)stage * BM * S;
-        double acca[2][G][KT > 0 ? KT : 1][2];  // even / odd k-steps: two independent DMMA chains
-        double accar[G][R > 0 ? R : 1];
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int g = 0; g < G; ++g)
-#pragma unroll
-                for (int kt = 0; kt < (KT > 0 ? KT : 1); ++kt) acca[h][g][kt][0] = acca[h][g][kt][1] = 0.0;
-#pragma unroll
-        for (int g = 0; g < G; ++g)
-#pragma unroll
-            for (int r = 0; r < (R > 0 ? R : 1); ++r) accar[g][r] = 0.0;
-#pragma unroll
-        for (int s = 0; s < KSTEP_A; ++s) {
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const double x = xt[(g * 8 + gq) * S + fw + 4 * s + tq];
-#pragma unroll
-                for (int kt = 0; kt < KT; ++kt) dmma(acca[s & 1][g][kt], x, bv[s][kt]);
-#pragma unroll
-                for (int r = 0; r < R; ++r) accar[g][r] = fma(x, vr[s][r], accar[g][r]);
+    if (warp == role_producer) {
+        // ============================== producer: TMA ==============================
+        if (lane == 0) {
+            for (int i = 0; i < T; ++i) {
+                const int stage = i % STAGES;
+                if (i >= STAGES) mbar_wait(&empty[stage], (uint32_t)(((i / STAGES) - 1) & 1));
+                const int64_t r0 = tile_of(i) * BM;
+                const int rows = (n - r0) < BM ? (int)(n - r0) : BM;
+                uint32_t bytes = row_bytes * (uint32_t)rows;
+                if (NEED_P) bytes += BM * K * 8;
+                if (NEED_Y) bytes += BM * 4;
+                fence_proxy_async();
+                mbar_expect_tx(&full[stage], bytes);
+                if (row_bytes)
+                    for (int r = 0; r < rows; ++r)
+                        tma_bulk_g2s(xs + ((size_t)stage * BM + r) * S, a.X + (r0 + r) * a.ldx + f_cta, row_bytes,
+                                     &full[stage]);
+                if (NEED_P) tma_bulk_g2s(ps + (size_t)stage * BM * KE, a.Pin + r0 * K, BM * K * 8, &full[stage]);
+                if (NEED_Y) tma_bulk_g2s(ys + stage * BM, a.labels + r0, BM * 4, &full[stage]);
             }
         }
+    } else if (warp == role_pusher) {
+        // ============================== pusher: CTA partial -> cluster ==============================
+        for (int i = 0; i < T; ++i) {
+            const int b = i % kDmmaRedBufs, br = i % kDmmaRecvBufs;
+            mbar_wait(&red_full[b], (uint32_t)((i / kDmmaRedBufs) & 1));
+            DMMA_TRACE(i, 2);
+            // every CTA of the cluster released receive buffer br (its previous tile's epilogue is done)
+            if (i >= kDmmaRecvBufs) mbar_wait(&credit[br], (uint32_t)(((i / kDmmaRecvBufs) - 1) & 1));
+            const double* rd = red + (size_t)b * nc * PART;
+            const uint32_t dst_local = smem_u32(recv + ((size_t)br * csize + crank) * PART);
+            const uint32_t bar_local = smem_u32(&rbar[br]);
+            for (int i2 = lane; i2 < PART / 2; i2 += 32) {
+                double v0[8], v1[8];
 #pragma unroll
-        for (int g = 0; g < G; ++g)
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                double v = accar[g][r];
-                v += __shfl_xor_sync(0xffffffffu, v, 1);
-                v += __shfl_xor_sync(0xffffffffu, v, 2);
-                accar[g][r] = v;
+                for (int w = 0; w < 8; ++w) {
+                    double2 v = make_double2(0.0, 0.0);
+                    if (w < nc) v = *reinterpret_cast<const double2*>(rd + (size_t)w * PART + 2 * i2);
+                    v0[w] = v.x;
+                    v1[w] = v.y;
+                }
+                const double s0 = tree_sum(v0, nc), s1 = tree_sum(v1, nc);
+                for (uint32_t q = 0; q < csize; ++q)
+                    st_async_v2(mapa(dst_local + 16u * i2, q), s0, s1, mapa(bar_local, q));
             }
-        double* rw = red + (size_t)warp * PART;
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-#pragma unroll
-            for (int kt = 0; kt < KT; ++kt) {
-                const int o = (g * 8 + gq) * KP + kt * 8 + 2 * tq;
-                rw[o] = acca[0][g][kt][0] + acca[1][g][kt][0];
-                rw[o + 1] = acca[0][g][kt][1] + acca[1][g][kt][1];
-            }
-            if (tq == 0)
-#pragma unroll
-                for (int r = 0; r < R; ++r) rw[(g * 8 + gq) * KP + 8 * KT + r] = accar[g][r];
+            __syncwarp();
+            DMMA_TRACE(i, 3);
+            if (lane == 0) mbar_arrive(&red_empty[b]);
         }
-        __syncthreads();
-        // CTA partial (ascending warp order) -> slot [buf][crank] of every CTA in the cluster
-        const int buf = i % kDmmaRecvBufs;
-        const uint32_t dst_local = smem_u32(recv + ((size_t)buf * csize + crank) * PART);
-        const uint32_t bar_local = smem_u32(&rbar[buf]);
-        for (int i2 = threadIdx.x; i2 < PART / 2; i2 += blockDim.x) {
-            double s0 = 0.0, s1 = 0.0;
-            for (int w = 0; w < nw; ++w) {
-                const double2 v = *reinterpret_cast<const double2*>(red + (size_t)w * PART + 2 * i2);
-                s0 += v.x;
-                s1 += v.y;
+    } else if (warp >= role_epi0) {
+        // ============================== epilogue warps ==============================
+        // Warp e owns tiles i == e (mod kDmmaEpiWarps): each tile's epilogue is a short dependent chain
+        // of FP64 ops that queue behind the compute warps' DMMAs, so tiles are processed in parallel
+        // by independent warps rather than cooperatively.
+        const int ew = warp - role_epi0;
+        double* lgw = lgb + (size_t)ew * BM * KP;  // this warp's full-logit tile
+        double loss_acc = 0.0;                     // row lanes of the rank-0 CTA
+        constexpr int NE = (BM * K + 31) / 32;     // elements per lane in pass 1
+        for (int i = ew; i < T; i += kDmmaEpiWarps) {
+            const int stage = i % STAGES, br = i % kDmmaRecvBufs;
+            const int64_t r0 = tile_of(i) * BM;
+            if (lane == 0) mbar_expect_tx(&rbar[br], (uint32_t)csize * PART * 8u);
+            mbar_wait(&rbar[br], (uint32_t)((i / kDmmaRecvBufs) & 1));
+            if (ew == 0) DMMA_TRACE(i, 4);
+            if (NEED_P || NEED_Y) mbar_wait(&full[stage], (uint32_t)((i / STAGES) & 1));
+            if (ew == 0) DMMA_TRACE(i, 8);
+            // (1) full logits: sum of the CS partials in a fixed rank-order tree, all lanes' elements
+            //     loaded first so the trees of one lane are independent
+            const double* rv = recv + (size_t)br * csize * PART;
+            {
+                double v[NE][8];
+#pragma unroll
+                for (int j = 0; j < NE; ++j) {
+                    const int e = lane + 32 * j;
+                    const int row = e / K, c = e - row * K;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        v[j][q] = (e < BM * K && q < (int)csize) ? rv[(size_t)q * PART + row * KP + c] : 0.0;
+                }
+#pragma unroll
+                for (int j = 0; j < NE; ++j) {
+                    const int e = lane + 32 * j;
+                    const double s = tree_sum(v[j], (int)csize);
+                    if (e < BM * K) lgw[(e / K) * KP + (e % K)] = s;
+                }
             }
-            for (uint32_t q = 0; q < csize; ++q) st_async_v2(mapa(dst_local + 16u * i2, q), s0, s1, mapa(bar_local, q));
-        }
-        __syncthreads();  // red is free for the next phase A
-    };
-
-    const int hrow = lane >> 4, hc = lane & 15;  // epilogue: half warp per row, lane = class
-    if (my_tiles > 0) phase_a_and_push(0);
-    for (int i = 0; i < my_tiles; ++i) {
-        const int stage = i % STAGES;
-        const int buf = i % kDmmaRecvBufs;
-        const int64_t r0 = tile_of(i) * BM;
-        // overlap: tile i+1's phase A runs while tile i's partials travel through the cluster
-        if (i + 1 < my_tiles) phase_a_and_push(i + 1);
-        if (threadIdx.x == 0) mbar_expect_tx(&rbar[buf], (uint32_t)csize * PART * 8u);
-        mbar_wait(&rbar[buf], (uint32_t)((i / kDmmaRecvBufs) & 1));
-
-        // ---------------- epilogue: full logits (ascending cluster rank) -> U / cache ----------------
-        const double* rv = recv + (size_t)buf * csize * PART;
-        for (int row = warp * 2 + hrow; row < BM; row += 2 * nw) {
-            const int64_t gi = r0 + row;
-            const bool valid = gi < n;  // uniform over the half warp
-            const bool cl = hc < K;
-            double lg = 0.0;
-            if (cl)
-                for (uint32_t q = 0; q < csize; ++q) lg += rv[(size_t)q * PART + row * KP + hc];
-            double* urow = ut + row * KS;
-            if (MODE == kModeHv) {
-                const double pr = (cl && valid) ? ps[(size_t)stage * BM * K + row * K + hc] : 0.0;
-                const double vw = lg * pr;
-                const double rs = hsum16(vw);
-                if (cl) urow[hc] = valid ? vw - pr * rs : 0.0;
-            } else if (MODE == kModeLp) {
-                if (valid && cl && crank == 0) a.Lp[gi * K + hc] = lg;
-            } else {
-                const double m = fmax(hmax16(cl ? lg : -INFINITY), 0.0);
-                const double e = cl ? exp(lg - m) : 0.0;
-                const double alpha = exp(-m) + hsum16(e);
-                const int b = valid ? ys[stage * BM + row] : 0;
-                const double lb = hsum16((cl && hc == b - 1) ? lg : 0.0);
-                const double pc = e / alpha;
-                if (MODE == kModeCache || MODE == kModeValue) {
-                    if (valid && crank == 0 && hc == 0) loss_acc += (m + log(alpha)) - (b <= K ? lb : 0.0);
-                    if (MODE == kModeCache) {
-                        if (cl) urow[hc] = valid ? ((hc == b - 1) ? pc - 1.0 : pc) : 0.0;
-                        if (valid && cl && crank == 0) {
-                            a.L0[gi * K + hc] = lg;
-                            a.P[gi * K + hc] = pc;
-                            if (hc == 0) {
+            __syncwarp();
+            if (ew == 0) DMMA_TRACE(i, 9);
+            // receive buffer br consumed: return one credit to every CTA of the cluster
+            if (lane == 0)
+                for (uint32_t q = 0; q < csize; ++q) mbar_arrive_remote(&credit[br], q);
+            if (ew == 0) DMMA_TRACE(i, 11);
+            // (2) row epilogue, one lane per row
+            if (lane < BM) {
+                const int row = lane;
+                const int64_t gi = r0 + row;
+                const bool valid = gi < n;
+                const double* lg = lgw + row * KP;
+                double* urow = ut + (size_t)stage * BM * KS + row * KS;
+                if (MODE == kModeHv) {
+                    const double* pr = ps + (size_t)stage * BM * KE + row * K;
+                    if (valid) {
+                        constexpr int KT2 = K <= 2 ? 2 : K <= 4 ? 4 : K <= 8 ? 8 : K <= 16 ? 16 : 32;
+                        double vw[KT2], pv[K], vt[KT2];
+#pragma unroll
+                        for (int c = 0; c < KT2; ++c) {
+                            vw[c] = 0.0;
+                            if (c < K) {
+                                pv[c] = pr[c];
+                                vw[c] = lg[c] * pv[c];
+                            }
+                            vt[c] = vw[c];
+                        }
+                        const double rs = tree_sum(vt, K);  // row_sum(V o P)
+#pragma unroll
+                        for (int c = 0; c < K; ++c) urow[c] = vw[c] - pv[c] * rs;
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < K; ++c) urow[c] = 0.0;
+                    }
+                } else if (MODE == kModeLp) {
+                    if (valid && crank == 0)
+#pragma unroll
+                        for (int c = 0; c < K; ++c) a.Lp[gi * K + c] = lg[c];
+                } else if (valid) {
+                    double m = lg[0];
+#pragma unroll
+                    for (int c = 1; c < K; ++c) m = lg[c] > m ? lg[c] : m;
+                    m = m > 0.0 ? m : 0.0;
+                    constexpr int KT2 = K <= 2 ? 2 : K <= 4 ? 4 : K <= 8 ? 8 : K <= 16 ? 16 : 32;
+                    double e[KT2], et2[KT2];
+#pragma unroll
+                    for (int c = 0; c < KT2; ++c) {
+                        e[c] = c < K ? exp(lg[c] - m) : 0.0;
+                        et2[c] = e[c];
+                    }
+                    const double alpha = exp(-m) + tree_sum(et2, K);
+                    const int yb = ys[stage * BM + row];
+                    double lb = 0.0;
+#pragma unroll
+                    for (int c = 0; c < K; ++c)
+                        if (c == yb - 1) lb = lg[c];
+                    if (MODE == kModeCache || MODE == kModeValue) {
+                        if (crank == 0) loss_acc += (m + log(alpha)) - (yb <= K ? lb : 0.0);
+                        if (MODE == kModeCache) {
+#pragma unroll
+                            for (int c = 0; c < K; ++c) {
+                                const double pc = e[c] / alpha;
+                                urow[c] = (c == yb - 1) ? pc - 1.0 : pc;
+                                if (crank == 0) {
+                                    a.L0[gi * K + c] = lg[c];
+                                    a.P[gi * K + c] = pc;
+                                }
+                            }
+                            if (crank == 0) {
                                 a.rowM[gi] = m;
                                 a.rowA[gi] = alpha;
                             }
                         }
-                    }
-                } else if (MODE == kModePredict) {
-                    const double best = hmax16(cl ? pc : -INFINITY);
-                    const unsigned eq = __ballot_sync(0xffffffffu, cl && pc == best);
-                    const unsigned half = (eq >> (hrow * 16)) & 0xffffu;
-                    int arg = __ffs(half);  // smallest class index attaining the max (tie rule)
-                    const double residual = exp(-m) / alpha;
-                    if (residual > best) arg = K + 1;
-                    if (valid && crank == 0 && hc == 0) {
+                    } else if (MODE == kModePredict && crank == 0) {
+                        const double residual = exp(-m) / alpha;
+                        double best = e[0] / alpha;
+#pragma unroll
+                        for (int c = 1; c < K; ++c) best = (e[c] / alpha > best) ? e[c] / alpha : best;
+                        int arg = 0;
+                        for (int c = 0; c < K; ++c)
+                            if (e[c] / alpha == best) {
+                                arg = c + 1;
+                                break;
+                            }
+                        if (residual > best) arg = K + 1;
                         a.pred[gi] = arg;
-                        loss_acc += (arg == b) ? 1.0 : 0.0;
+                        loss_acc += (arg == yb) ? 1.0 : 0.0;
                     }
+                } else if (MODE == kModeCache) {
+#pragma unroll
+                    for (int c = 0; c < K; ++c) urow[c] = 0.0;
                 }
             }
+            __syncwarp();  // U rows complete, lgw reusable
+            if (ew == 0) DMMA_TRACE(i, 12);
+            if (lane == 0) {
+                if (ew == 0) DMMA_TRACE(i, 5);
+                if (PHASE_B) mbar_arrive(&u_full[stage]);
+                mbar_arrive(&empty[stage]);
+            }
         }
-        __syncthreads();
+        // cluster's loss / hit partial (rank-0 CTA): rows of warp 0's tiles, then warp 1's, ...
+        if (MODE == kModeCache || MODE == kModeValue || MODE == kModePredict) {
+            if (lane < BM) misc[ew * BM + lane] = loss_acc;
+            named_sync(1, 32 * kDmmaEpiWarps);
+            if (ew == 0 && lane == 0 && crank == 0) {
+                double s = 0.0;
+                for (int q = 0; q < BM * kDmmaEpiWarps; ++q) s += misc[q];
+                const int slotid = MODE == kModePredict ? kSlotHits : kSlotLoss;
+                a.blk[(int64_t)slotid * kBlockPartials + cid] = s;
+            }
+        }
+    } else {
+        // ============================== compute warps ==============================
+        const int fw = warp * W;  // warp slice offset inside the CTA slice
+        // V slice in registers: B fragments (k = tq, n = gq) and the remainder columns
+        double bv[KSTEP_A][KT > 0 ? KT : 1];
+        double vr[KSTEP_A][R > 0 ? R : 1];
+#pragma unroll
+        for (int s = 0; s < KSTEP_A; ++s) {
+            const int64_t f = (int64_t)f_cta + fw + 4 * s + tq;
+            const bool ok = f < p && fw + 4 * s + tq < fs;
+#pragma unroll
+            for (int kt = 0; kt < KT; ++kt) bv[s][kt] = ok ? a.V[(int64_t)(kt * 8 + gq) * p + f] : 0.0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) vr[s][r] = ok ? a.V[(int64_t)(8 * KT + r) * p + f] : 0.0;
+        }
+        double accb[PHASE_B ? MT : 1][KT > 0 ? KT : 1][2];
+        double accbr[PHASE_B ? MT : 1][R > 0 ? R : 1];
+#pragma unroll
+        for (int m = 0; m < (PHASE_B ? MT : 1); ++m) {
+#pragma unroll
+            for (int kt = 0; kt < (KT > 0 ? KT : 1); ++kt) accb[m][kt][0] = accb[m][kt][1] = 0.0;
+#pragma unroll
+            for (int r = 0; r < (R > 0 ? R : 1); ++r) accbr[m][r] = 0.0;
+        }
 
-        // ---------------- phase B: X_slice^T U into the resident accumulators ----------------
-        if (PHASE_B) {
+        auto phase_a = [&](int i) {
+            const int stage = i % STAGES, b = i % kDmmaRedBufs;
+            mbar_wait(&full[stage], (uint32_t)((i / STAGES) & 1));
+            if (warp == 0) DMMA_TRACE(i, 0);
             const double* xt = xs + (size_t)stage * BM * S;
+            double acca[2][G][KT > 0 ? KT : 1][2];  // even / odd k-steps: two independent DMMA chains
+            double accar[G][R > 0 ? R : 1];
 #pragma unroll
-            for (int s = 0; s < BM / 4; ++s) {
-                const int row = 4 * s + tq;
-                double ub[KT > 0 ? KT : 1], ur[R > 0 ? R : 1];
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int kt = 0; kt < KT; ++kt) ub[kt] = ut[row * KS + kt * 8 + gq];
+                for (int g = 0; g < G; ++g)
 #pragma unroll
-                for (int r = 0; r < R; ++r) ur[r] = ut[row * KS + 8 * KT + r];
-                const double* xr = xt + (size_t)row * S + fw;
+                    for (int kt = 0; kt < (KT > 0 ? KT : 1); ++kt) acca[h][g][kt][0] = acca[h][g][kt][1] = 0.0;
 #pragma unroll
-                for (int mp = 0; mp < MT / 2; ++mp) {
-                    const double2 x2 = *reinterpret_cast<const double2*>(xr + mp * 16 + 2 * gq);
+            for (int g = 0; g < G; ++g)
 #pragma unroll
-                    for (int kt = 0; kt < KT; ++kt) {
-                        dmma(accb[2 * mp][kt], x2.x, ub[kt]);
-                        dmma(accb[2 * mp + 1][kt], x2.y, ub[kt]);
-                    }
+                for (int r = 0; r < (R > 0 ? R : 1); ++r) accar[g][r] = 0.0;
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        accbr[2 * mp][r] = fma(x2.x, ur[r], accbr[2 * mp][r]);
-                        accbr[2 * mp + 1][r] = fma(x2.y, ur[r], accbr[2 * mp + 1][r]);
-                    }
-                }
-                if (MT & 1) {
-                    const double x = xr[(MT - 1) * 8 + gq];
+            for (int s = 0; s < KSTEP_A; ++s) {
 #pragma unroll
-                    for (int kt = 0; kt < KT; ++kt) dmma(accb[MT - 1][kt], x, ub[kt]);
+                for (int g = 0; g < G; ++g) {
+                    const double x = xt[(g * 8 + gq) * S + fw + 4 * s + tq];
 #pragma unroll
-                    for (int r = 0; r < R; ++r) accbr[MT - 1][r] = fma(x, ur[r], accbr[MT - 1][r]);
+                    for (int kt = 0; kt < KT; ++kt) dmma(acca[s & 1][g][kt], x, bv[s][kt]);
+#pragma unroll
+                    for (int r = 0; r < R; ++r) accar[g][r] = fma(x, vr[s][r], accar[g][r]);
                 }
             }
-        }
-        __syncthreads();  // stage i and ut free (all warps past phase B)
-        if (threadIdx.x == 0 && i + STAGES < my_tiles) {
-            fence_proxy_async();
-            issue(i + STAGES);
-        }
-    }
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    double v = accar[g][r];
+                    v += __shfl_xor_sync(0xffffffffu, v, 1);
+                    v += __shfl_xor_sync(0xffffffffu, v, 2);
+                    accar[g][r] = v;
+                }
+            if (i >= kDmmaRedBufs) mbar_wait(&red_empty[b], (uint32_t)(((i / kDmmaRedBufs) - 1) & 1));
+            double* rw = red + ((size_t)b * nc + warp) * PART;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+#pragma unroll
+                for (int kt = 0; kt < KT; ++kt) {
+                    const int o = (g * 8 + gq) * KP + kt * 8 + 2 * tq;
+                    *reinterpret_cast<double2*>(rw + o) =
+                        make_double2(acca[0][g][kt][0] + acca[1][g][kt][0], acca[0][g][kt][1] + acca[1][g][kt][1]);
+                }
+                if (tq == 0)
+#pragma unroll
+                    for (int r = 0; r < R; ++r) rw[(g * 8 + gq) * KP + 8 * KT + r] = accar[g][r];
+            }
+            __syncwarp();
+            if (warp == 0) DMMA_TRACE(i, 1);
+            if (lane == 0) mbar_arrive(&red_full[b]);
+        };
 
-    // ---------------- write this cluster's split-K partial of X^T U ----------------
-    if (PHASE_B) {
-        const int64_t d = (int64_t)K * p;
-        double* out = a.part + (int64_t)cid * d;
+        for (int i = 0; i < LAG && i < T; ++i) phase_a(i);
+        for (int i = 0; i < T; ++i) {
+            const int stage = i % STAGES;
+            if (i + LAG < T) phase_a(i + LAG);
+            if (PHASE_B) {
+                mbar_wait(&u_full[stage], (uint32_t)((i / STAGES) & 1));
+                if (warp == 0) DMMA_TRACE(i, 6);
+                const double* xt = xs + (size_t)stage * BM * S;
+                const double* utb = ut + (size_t)stage * BM * KS;
 #pragma unroll
-        for (int m = 0; m < MT; ++m) {
-            // feature of fragment row gq in m-tile m (pairs interleave; an odd tail is contiguous)
-            const int loc = (MT % 2 == 1 && m == MT - 1) ? (m * 8 + gq) : ((m / 2) * 16 + 2 * gq + (m & 1));
-            const int64_t f = (int64_t)f_cta + fw + loc;
-            const bool ok = f < p && fw + loc < fs;
+                for (int s = 0; s < BM / 4; ++s) {
+                    const int row = 4 * s + tq;
+                    double ub[KT > 0 ? KT : 1], ur[R > 0 ? R : 1];
 #pragma unroll
-            for (int kt = 0; kt < KT; ++kt) {
-                if (ok) {
-                    out[(int64_t)(kt * 8 + 2 * tq) * p + f] = accb[m][kt][0];
-                    out[(int64_t)(kt * 8 + 2 * tq + 1) * p + f] = accb[m][kt][1];
+                    for (int kt = 0; kt < KT; ++kt) ub[kt] = utb[row * KS + kt * 8 + gq];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) ur[r] = utb[row * KS + 8 * KT + r];
+                    const double* xr = xt + (size_t)row * S + fw;
+#pragma unroll
+                    for (int mp = 0; mp < MT / 2; ++mp) {
+                        const double2 x2 = *reinterpret_cast<const double2*>(xr + mp * 16 + 2 * gq);
+#pragma unroll
+                        for (int kt = 0; kt < KT; ++kt) {
+                            dmma(accb[2 * mp][kt], x2.x, ub[kt]);
+                            dmma(accb[2 * mp + 1][kt], x2.y, ub[kt]);
+                        }
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            accbr[2 * mp][r] = fma(x2.x, ur[r], accbr[2 * mp][r]);
+                            accbr[2 * mp + 1][r] = fma(x2.y, ur[r], accbr[2 * mp + 1][r]);
+                        }
+                    }
+                    if (MT & 1) {
+                        const double x = xr[(MT - 1) * 8 + gq];
+#pragma unroll
+                        for (int kt = 0; kt < KT; ++kt) dmma(accb[MT - 1][kt], x, ub[kt]);
+#pragma unroll
+                        for (int r = 0; r < R; ++r) accbr[MT - 1][r] = fma(x, ur[r], accbr[MT - 1][r]);
+                    }
                 }
             }
+            __syncwarp();
+            if (warp == 0) DMMA_TRACE(i, 7);
+            if (lane == 0) mbar_arrive(&empty[stage]);
+        }
+
+        // ---------------- this cluster's split-K partial of X^T U ----------------
+        if (PHASE_B) {
+            const int64_t d = (int64_t)K * p;
+            double* out = a.part + (int64_t)cid * d;
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                double v = accbr[m][r];
-                v += __shfl_xor_sync(0xffffffffu, v, 1);
-                v += __shfl_xor_sync(0xffffffffu, v, 2);
-                if (ok && tq == 0) out[(int64_t)(8 * KT + r) * p + f] = v;
+            for (int m = 0; m < MT; ++m) {
+                // feature of fragment row gq in m-tile m (pairs interleave; an odd tail is contiguous)
+                const int loc = (MT % 2 == 1 && m == MT - 1) ? (m * 8 + gq) : ((m / 2) * 16 + 2 * gq + (m & 1));
+                const int64_t f = (int64_t)f_cta + fw + loc;
+                const bool ok = f < p && fw + loc < fs;
+#pragma unroll
+                for (int kt = 0; kt < KT; ++kt) {
+                    if (ok) {
+                        out[(int64_t)(kt * 8 + 2 * tq) * p + f] = accb[m][kt][0];
+                        out[(int64_t)(kt * 8 + 2 * tq + 1) * p + f] = accb[m][kt][1];
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    double v = accbr[m][r];
+                    v += __shfl_xor_sync(0xffffffffu, v, 1);
+                    v += __shfl_xor_sync(0xffffffffu, v, 2);
+                    if (ok && tq == 0) out[(int64_t)(8 * KT + r) * p + f] = v;
+                }
             }
         }
     }
-    if (MODE == kModeCache || MODE == kModeValue || MODE == kModePredict) {
-        // cluster's loss / hit partial (rank-0 CTA; fixed order over the per-half-warp accumulators)
-        __syncthreads();
-        if ((lane & 15) == 0) misc[warp * 2 + hrow] = loss_acc;
-        __syncthreads();
-        if (threadIdx.x == 0 && crank == 0) {
-            double s = 0.0;
-            for (int i = 0; i < 2 * nw; ++i) s += misc[i];
-            const int slotid = MODE == kModePredict ? kSlotHits : kSlotLoss;
-            a.blk[(int64_t)slotid * kBlockPartials + cid] = s;
-        }
-    }
+    __syncthreads();
     if (csize > 1) cluster_sync_all();  // no CTA leaves while peers may still target its shared memory
 }
 

@@ -40,8 +40,9 @@ namespace nadmm {
 // ------------------------------------------------------------------------------------------------
 namespace {
 
-constexpr int kBM = 16;
-constexpr int kStages = 3;
+constexpr int kBM = 8;
+constexpr int kLag = 4;
+constexpr int kStages = kLag + 2;
 
 struct Layout {
     bool ok = false;
@@ -59,7 +60,7 @@ Layout choose_layout(int64_t p, int K) {
         for (int cs : {1, 2, 4, 8}) {
             const int W = 8 * mt;
             const int nw = (int)((p + (int64_t)cs * W - 1) / ((int64_t)cs * W));
-            if (nw < 2 || nw > 12) continue;
+            if (nw < 2 || nw > 8) continue;  // compute warps; + kDmmaAux exchange/producer warps
             const int fs = nw * W;
             const double waste = (double)cs * fs / (double)p - 1.0;
             if (waste > 0.15) continue;
@@ -80,7 +81,7 @@ Layout choose_layout(int64_t p, int K) {
 cudaLaunchConfig_t make_cfg(Shard& s, const Layout& L, int clusters, cudaLaunchAttribute* attr) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(clusters * L.cs, 1, 1);
-    cfg.blockDim = dim3(32 * L.nw, 1, 1);
+    cfg.blockDim = dim3(32 * (L.nw + kDmmaAux), 1, 1);
     cfg.dynamicSmemBytes = L.smem;
     cfg.stream = s.ctx->stream;
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -96,7 +97,7 @@ cudaLaunchConfig_t make_cfg(Shard& s, const Layout& L, int clusters, cudaLaunchA
 // co-resident cluster count is queried there too.
 template <int MT, int MODE>
 int setup_mt(Shard& s, const Layout& L) {
-    auto kern = dmma_pass_kernel<MT, 1, 1, kBM, kStages, MODE>;
+    auto kern = dmma_pass_kernel<MT, 1, 1, kBM, kLag, MODE>;
     NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchAttribute attr[1];
@@ -118,7 +119,7 @@ int setup_modes(Shard& s, const Layout& L) {
 
 template <int MT, int MODE>
 void launch_mt(Shard& s, const Layout& L, const DmmaArgs& a, int clusters) {
-    auto kern = dmma_pass_kernel<MT, 1, 1, kBM, kStages, MODE>;
+    auto kern = dmma_pass_kernel<MT, 1, 1, kBM, kLag, MODE>;
     cudaLaunchAttribute attr[1];
     cudaLaunchConfig_t cfg = make_cfg(s, L, clusters, attr);
     NADMM_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
@@ -198,3 +199,9 @@ void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
 }
 
 }  // namespace nadmm
+
+#ifdef NADMM_DMMA_TRACE
+extern "C" __attribute__((visibility("default"))) int nadmm_debug_dmma_trace(long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, nadmm::g_dmma_trace, sizeof(nadmm::g_dmma_trace));
+}
+#endif
