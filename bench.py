@@ -4,9 +4,12 @@
 Workload (BASELINE.json configs[1]): CIFAR-10-shaped synthetic dense data, 50,000 x 3,072, 10 classes,
 lambda = 1e-3, Newton-ADMM over 8 ADMM nodes (contiguous row shards of 6,250 rows), NewtonConfig
 defaults (10 CG iterations, tol 1e-4, 10 line-search trials), one inner Newton step per outer
-iteration, fixed rho = 1. With --gpus N each rank holds 8/N nodes (strong scaling; one NCCL
+iteration, spectral penalty selection from rho0 = 1. With --gpus N each rank holds 8/N nodes (strong scaling; one NCCL
 allreduce per outer iteration). Data comes from the reference generator (src/data_io.cpp:330-370),
-separation 3, noise 1, seed 0.
+separation 1, noise 1, seed 0: at separation 3 the 50,000 x 3,072 training set is almost separable
+(F* = 3.9) and neither penalty policy reaches theta <= 0.05 within 300 outer iterations, so the
+time-to-target leg would be empty; at separation 1, F* = 7.9e4 and spectral penalty selection
+(SPS, the paper's Newton-ADMM setting) reaches theta <= 0.05 in under 30 outer iterations.
 
 A step is one outer ADMM iteration. `value` = shard-level Hessian-vector products applied per
 second on device-resident data (whole job, max-over-ranks device time); `e2e` = the same metric
@@ -31,10 +34,10 @@ sys.path.insert(0, str(ROOT))
 
 N_TOTAL, P, C, LAM = 55_556, 3072, 10, 1e-3  # floor(9n/10) = 50,000 train rows
 NODES = 8
-SEP, NOISE, SEED = 3.0, 1.0, 0
+SEP, NOISE, SEED = 1.0, 1.0, 0
 THETA_TARGET = 0.05
 METRIC = "Hv products/s (Newton-ADMM shard Hessian-vector products; time-to-target alongside)"
-WORKLOAD = "cifar10-shaped dense 50000x3072 C=10 lambda=1e-3, Newton-ADMM over 8 row-shard nodes"
+WORKLOAD = "cifar10-shaped dense 50000x3072 C=10 lambda=1e-3, Newton-ADMM (SPS penalty) over 8 row-shard nodes"
 
 
 def env_int(k, d):
@@ -220,7 +223,8 @@ def main():
         dist.all_reduce(t)
         return float(t.item())
 
-    cfg = nadmm.AdmmConfig(n_workers=NODES, lam=LAM, stopping=nadmm.StoppingConfig(max_outer_iters=100000))
+    sps = nadmm.PenaltyPolicy(kind="spectral")
+    cfg = nadmm.AdmmConfig(n_workers=NODES, lam=LAM, penalty=sps, stopping=nadmm.StoppingConfig(max_outer_iters=100000))
     stream = torch.cuda.ExternalStream(ctx.stream)
 
     # ---------------- value: device-resident consensus loop ----------------
@@ -309,7 +313,7 @@ def main():
             full.close()
         if dist:
             dist.broadcast_object_list(fstar, src=0)
-        tcfg = nadmm.AdmmConfig(n_workers=NODES, lam=LAM, stopping=nadmm.StoppingConfig(max_outer_iters=300))
+        tcfg = nadmm.AdmmConfig(n_workers=NODES, lam=LAM, penalty=sps, stopping=nadmm.StoppingConfig(max_outer_iters=300))
         barrier()
         s2 = nadmm.AdmmSession(shards, tcfg, nadmm.EvalContext(True, fstar[0], THETA_TARGET), comm)
         s2.step(300)
@@ -336,10 +340,10 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "Hv/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (reference generate_synthetic: separation 3, noise 1, seed 0)",
+                "data": "synthetic (reference generate_synthetic: separation 1, noise 1, seed 0)",
                 "config": {"workload": WORKLOAD, "n_train": int(len(ytr)), "p": P, "classes": C, "lambda": LAM,
                            "admm_nodes": NODES, "nodes_per_gpu": per, "inner_iters": 1, "cg_max_iters": 10,
-                           "ls_max_iters": 10, "penalty": "fixed rho=1",
+                           "ls_max_iters": 10, "penalty": "spectral (SPS, rho0=1, T_f=2)",
                            "l2": "no flush: per-step inputs 1.23 GB/GPU at N=1 >> 126 MB L2"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(st["kernel_launches"]),
                 "clocks": clk.summary(), "outer_iters_per_s": args.steps / (ms * 1e-3),

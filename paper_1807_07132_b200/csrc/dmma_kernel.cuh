@@ -65,6 +65,11 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
         : "memory");
 }
 
+// L2 prefetch of a global range (no shared memory, no completion): HBM -> L2 runs ahead of the ring.
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
@@ -171,6 +176,10 @@ __device__ long long g_dmma_trace[64][16];  // per-tile clock64 stamps of CTA 0 
     } while (0)
 #endif
 
+#ifndef NADMM_DMMA_PREFETCH
+#define NADMM_DMMA_PREFETCH 8
+#endif
+constexpr int kDmmaPrefetch = NADMM_DMMA_PREFETCH;  // L2 prefetch distance in tiles (0: off)
 constexpr int kDmmaRecvBufs = 4;  // receive buffers per CTA, flow-controlled by remote credits
 constexpr int kDmmaRedBufs = 2;   // compute-warp partial buffers (pusher frees them)
 constexpr int kDmmaEpiWarps = 2;  // epilogue warps
@@ -275,6 +284,14 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
         if (lane == 0) {
             for (int i = 0; i < T; ++i) {
                 const int stage = i % STAGES;
+                // tile i + kDmmaPrefetch: HBM -> L2 now, so the ring refill after the empty wait hits L2
+                // (the ring alone keeps too few bytes in flight: most stages wait for phase B)
+                if (kDmmaPrefetch > 0 && i + kDmmaPrefetch < T && row_bytes) {
+                    const int64_t q0 = tile_of(i + kDmmaPrefetch) * BM;
+                    const int qrows = (n - q0) < BM ? (int)(n - q0) : BM;
+                    for (int r = 0; r < qrows; ++r) prefetch_l2(a.X + (q0 + r) * a.ldx + f_cta, row_bytes);
+                    if (NEED_P && crank == 0) prefetch_l2(a.Pin + q0 * K, BM * K * 8);
+                }
                 if (i >= STAGES) mbar_wait(&empty[stage], (uint32_t)(((i / STAGES) - 1) & 1));
                 const int64_t r0 = tile_of(i) * BM;
                 const int rows = (n - r0) < BM ? (int)(n - r0) : BM;
@@ -499,7 +516,10 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
             if (warp == 0) DMMA_TRACE(i, 0);
             const double* xt = xs + (size_t)stage * BM * S;
             double acca[2][G][KT > 0 ? KT : 1][2];  // even / odd k-steps: two independent DMMA chains
-            double accar[G][R > 0 ? R : 1];
+            // remainder classes on DFMA: 4 independent chains per row group (a dependent DFMA queues
+            // behind the DMMAs sharing the FP64 pipe, so one 12-long chain would serialise phase A)
+            constexpr int RC = 4;
+            double accar[RC][G][R > 0 ? R : 1];
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -507,9 +527,11 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
 #pragma unroll
                     for (int kt = 0; kt < (KT > 0 ? KT : 1); ++kt) acca[h][g][kt][0] = acca[h][g][kt][1] = 0.0;
 #pragma unroll
-            for (int g = 0; g < G; ++g)
+            for (int h = 0; h < RC; ++h)
 #pragma unroll
-                for (int r = 0; r < (R > 0 ? R : 1); ++r) accar[g][r] = 0.0;
+                for (int g = 0; g < G; ++g)
+#pragma unroll
+                    for (int r = 0; r < (R > 0 ? R : 1); ++r) accar[h][g][r] = 0.0;
 #pragma unroll
             for (int s = 0; s < KSTEP_A; ++s) {
 #pragma unroll
@@ -518,17 +540,17 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
 #pragma unroll
                     for (int kt = 0; kt < KT; ++kt) dmma(acca[s & 1][g][kt], x, bv[s][kt]);
 #pragma unroll
-                    for (int r = 0; r < R; ++r) accar[g][r] = fma(x, vr[s][r], accar[g][r]);
+                    for (int r = 0; r < R; ++r) accar[s % RC][g][r] = fma(x, vr[s][r], accar[s % RC][g][r]);
                 }
             }
 #pragma unroll
             for (int g = 0; g < G; ++g)
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    double v = accar[g][r];
+                    double v = (accar[0][g][r] + accar[1][g][r]) + (accar[2][g][r] + accar[3][g][r]);
                     v += __shfl_xor_sync(0xffffffffu, v, 1);
                     v += __shfl_xor_sync(0xffffffffu, v, 2);
-                    accar[g][r] = v;
+                    accar[0][g][r] = v;
                 }
             if (i >= kDmmaRedBufs) mbar_wait(&red_empty[b], (uint32_t)(((i / kDmmaRedBufs) - 1) & 1));
             double* rw = red + ((size_t)b * nc + warp) * PART;
@@ -542,7 +564,7 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                 }
                 if (tq == 0)
 #pragma unroll
-                    for (int r = 0; r < R; ++r) rw[(g * 8 + gq) * KP + 8 * KT + r] = accar[g][r];
+                    for (int r = 0; r < R; ++r) rw[(g * 8 + gq) * KP + 8 * KT + r] = accar[0][g][r];
             }
             __syncwarp();
             if (warp == 0) DMMA_TRACE(i, 1);
