@@ -351,10 +351,14 @@ struct AdmmRun {
     // One outer iteration (solve, gather, z, y, penalty, metrics).
     void iterate(nadmm_metrics_row* row) {
         int inner = 0, cg_sum = 0, fe_sum = 0, flags = 0;
-        for (int i = 0; i < n_local; ++i) {  // (1) scatter z / solve / gather
+        std::vector<char> pending(n_local, 0);
+        for (int i = 0; i < n_local; ++i) {  // (1) scatter z / solve (all workers enqueued back to back)
             Shard& s = *shards[i];
             NADMM_CUDA(cudaMemcpyAsync(s.z, z, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
-            SolveResult r = device_newton_solve(s, ncfg, 0.0, true, rho[i], cfg.inner_iters);
+            pending[i] = !solve_launch(s, ncfg, 0.0, true, rho[i], cfg.inner_iters);
+        }
+        for (int i = 0; i < n_local; ++i) {  // gather the workers' inner stats
+            SolveResult r = solve_collect(*shards[i], ncfg, pending[i]);
             if (r.error) raise((nadmm_status)r.error, "worker inner solve failed");
             inner += r.iterations;
             cg_sum += r.cg_sum;

@@ -97,12 +97,15 @@ void alloc_work(Shard& s) {
         NADMM_CUDA(cudaMemsetAsync(*v, 0, sizeof(double) * s.d, s.ctx->stream));
     }
     s.scal = dev_alloc<double>(s, 8);
+    s.gbar = dev_alloc<unsigned long long>(s, 8);
+    NADMM_CUDA(cudaMemsetAsync(s.gbar, 0, 8 * sizeof(unsigned long long), s.ctx->stream));
     s.prm = dev_alloc<DevParams>(s, 1);
     s.st = dev_alloc<DevState>(s, 1);
     s.trace = dev_alloc<DevTrace>(s, kTraceCap);
     NADMM_CUDA(cudaMemsetAsync(s.st, 0, sizeof(DevState), s.ctx->stream));
     NADMM_CUDA(cudaMallocHost(&s.prm_host, sizeof(DevParams)));
     NADMM_CUDA(cudaMallocHost(&s.st_host, sizeof(DevState)));
+    NADMM_CUDA(cudaMallocHost(&s.trace_host, sizeof(DevTrace) * kTraceCap));
     std::memset(s.prm_host, 0, sizeof(DevParams));
     NADMM_CUDA(cudaMemcpyAsync(s.prm, s.prm_host, sizeof(DevParams), cudaMemcpyHostToDevice, s.ctx->stream));
 }
@@ -151,6 +154,7 @@ Shard::~Shard() {
         if (t.start) cudaEventDestroy(t.start);
         if (t.stop) cudaEventDestroy(t.stop);
     }
+    for (cudaEvent_t e : tl_events) cudaEventDestroy(e);
     for (double** v : {&X, &vals, &cval, &L0, &P, &U, &Lp, &rowM, &rowA, &part, &blk, &cache_x, &gbase, &scal, &x, &g,
                        &pd, &r, &dv, &hd, &z, &y, &t, &tmp})
         dev_free(*v);
@@ -160,11 +164,13 @@ Shard::~Shard() {
     dev_free(crow);
     dev_free(labels);
     dev_free(pred);
+    dev_free(gbar);
     dev_free(prm);
     dev_free(st);
     dev_free(trace);
     if (prm_host) cudaFreeHost(prm_host);
     if (st_host) cudaFreeHost(st_host);
+    if (trace_host) cudaFreeHost(trace_host);
 }
 
 void Shard::ensure_timers(int n) {
@@ -587,3 +593,21 @@ nadmm_status nadmm_worker_solve(nadmm_worker w, double rho, const double* z, con
 namespace nadmm {
 void set_last_error(const std::string& m) { g_last_error = m; }
 }  // namespace nadmm
+
+// Profiling hook (not part of the ABI header): per-node durations of the last replay of the shard's
+// captured Newton-iteration graph, when it was captured with NADMM_GRAPH_TIMELINE=1. Returns the
+// number of intervals written (interval i ends at the mark names[i]).
+extern "C" __attribute__((visibility("default"))) int nadmm_debug_graph_timeline(nadmm_shard sh, float* ms,
+                                                                               const char** names, int cap) {
+    if (!sh) return -1;
+    nadmm::Shard& s = *sh;
+    if (cudaStreamSynchronize(s.ctx->stream) != cudaSuccess) return -1;
+    int n = 0;
+    for (size_t i = 1; i < s.tl_names.size() && n < cap; ++i, ++n) {
+        float t = -1.f;
+        if (cudaEventElapsedTime(&t, s.tl_events[i - 1], s.tl_events[i]) != cudaSuccess) t = -1.f;
+        ms[n] = t;
+        names[n] = s.tl_names[i];
+    }
+    return n;
+}

@@ -70,8 +70,35 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
 __device__ __forceinline__ double reduce_partials(const double* parts, int n) {
     const int lane = threadIdx.x & 31;
     double s = 0.0;
-    for (int i = lane; i < n; i += 32) s += parts[i];
+    int i = lane;
+    for (; i + 96 < n; i += 128) {  // four loads in flight, additions in the same ascending order
+        const double v0 = parts[i], v1 = parts[i + 32], v2 = parts[i + 64], v3 = parts[i + 96];
+        s += v0;
+        s += v1;
+        s += v2;
+        s += v3;
+    }
+    for (; i < n; i += 32) s += parts[i];
     return warp_sum(s);
+}
+
+// Software grid barrier for kernels whose whole grid is co-resident (small persistent grids on the
+// context's stream). `ctr` is a monotonically increasing per-kernel counter that only launches of
+// the same grid size touch, so it is a multiple of gridDim.x whenever such a launch starts; every
+// block must reach every barrier (callers branch only on grid-uniform values).
+__device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long nb = gridDim.x;
+        __threadfence();
+        const unsigned long long old = atomicAdd(ctr, 1ULL);
+        const unsigned long long target = (old / nb + 1) * nb;
+        unsigned long long cur;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(cur) : "l"(ctr) : "memory");
+        } while (cur < target);
+    }
+    __syncthreads();
 }
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }

@@ -180,6 +180,11 @@ __device__ long long g_dmma_trace[64][16];  // per-tile clock64 stamps of CTA 0 
 #define NADMM_DMMA_PREFETCH 8
 #endif
 constexpr int kDmmaPrefetch = NADMM_DMMA_PREFETCH;  // L2 prefetch distance in tiles (0: off)
+#ifndef NADMM_DMMA_CHAINS
+#define NADMM_DMMA_CHAINS 4
+#endif
+constexpr int kDmmaChains = NADMM_DMMA_CHAINS;  // phase-A accumulator chains per warp
+
 constexpr int kDmmaRecvBufs = 4;  // receive buffers per CTA, flow-controlled by remote credits
 constexpr int kDmmaRedBufs = 2;   // compute-warp partial buffers (pusher frees them)
 constexpr int kDmmaEpiWarps = 2;  // epilogue warps
@@ -515,13 +520,16 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
             mbar_wait(&full[stage], (uint32_t)((i / STAGES) & 1));
             if (warp == 0) DMMA_TRACE(i, 0);
             const double* xt = xs + (size_t)stage * BM * S;
-            double acca[2][G][KT > 0 ? KT : 1][2];  // even / odd k-steps: two independent DMMA chains
+            // NCH independent DMMA accumulator chains over the k-steps: a dependent DMMA waits behind the
+            // other warps' DMMAs in the shared FP64 pipe, so short chains keep phase A throughput-bound
+            constexpr int NCH = (KSTEP_A % kDmmaChains == 0) ? kDmmaChains : ((KSTEP_A % 2 == 0) ? 2 : 1);
+            double acca[NCH][G][KT > 0 ? KT : 1][2];
             // remainder classes on DFMA: 4 independent chains per row group (a dependent DFMA queues
             // behind the DMMAs sharing the FP64 pipe, so one 12-long chain would serialise phase A)
             constexpr int RC = 4;
             double accar[RC][G][R > 0 ? R : 1];
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < NCH; ++h)
 #pragma unroll
                 for (int g = 0; g < G; ++g)
 #pragma unroll
@@ -538,7 +546,7 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                 for (int g = 0; g < G; ++g) {
                     const double x = xt[(g * 8 + gq) * S + fw + 4 * s + tq];
 #pragma unroll
-                    for (int kt = 0; kt < KT; ++kt) dmma(acca[s & 1][g][kt], x, bv[s][kt]);
+                    for (int kt = 0; kt < KT; ++kt) dmma(acca[s % NCH][g][kt], x, bv[s][kt]);
 #pragma unroll
                     for (int r = 0; r < R; ++r) accar[s % RC][g][r] = fma(x, vr[s][r], accar[s % RC][g][r]);
                 }
@@ -552,6 +560,17 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                     v += __shfl_xor_sync(0xffffffffu, v, 2);
                     accar[0][g][r] = v;
                 }
+#pragma unroll
+            for (int w = 1; w < NCH; w *= 2)  // fixed pairwise fold of the chains into chain 0
+#pragma unroll
+                for (int h = 0; h + w < NCH; h += 2 * w)
+#pragma unroll
+                    for (int g = 0; g < G; ++g)
+#pragma unroll
+                        for (int kt = 0; kt < KT; ++kt) {
+                            acca[h][g][kt][0] = acca[h][g][kt][0] + acca[h + w][g][kt][0];
+                            acca[h][g][kt][1] = acca[h][g][kt][1] + acca[h + w][g][kt][1];
+                        }
             if (i >= kDmmaRedBufs) mbar_wait(&red_empty[b], (uint32_t)(((i / kDmmaRedBufs) - 1) & 1));
             double* rw = red + ((size_t)b * nc + warp) * PART;
 #pragma unroll
@@ -560,7 +579,7 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                 for (int kt = 0; kt < KT; ++kt) {
                     const int o = (g * 8 + gq) * KP + kt * 8 + 2 * tq;
                     *reinterpret_cast<double2*>(rw + o) =
-                        make_double2(acca[0][g][kt][0] + acca[1][g][kt][0], acca[0][g][kt][1] + acca[1][g][kt][1]);
+                        make_double2(acca[0][g][kt][0], acca[0][g][kt][1]);
                 }
                 if (tq == 0)
 #pragma unroll

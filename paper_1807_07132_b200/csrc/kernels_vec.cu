@@ -102,40 +102,40 @@ __global__ void k_value_finish(DevState* st, const DevParams* prm, const double*
     }
 }
 
-// Loop head of newton_solve (src/newton.cpp:80-87) and cg_solve's entry (19-30).
-__global__ void k_newton_begin(DevState* st, const DevParams* prm) {
-    if (threadIdx.x != 0) return;
-    int run = st->active;
-    if (run) {
-        st->rec_gnorm = st->g_norm;
-        if (st->g_norm < prm->grad_tol) {
-            st->converged = 1;
-            st->active = 0;
-            run = 0;
-        } else if (!(st->g_norm > 0.0)) {  // cg_solve requires ||g|| > 0 (ConfigError)
-            st->error = NADMM_ECONFIG;
-            st->active = 0;
-            run = 0;
+// Loop head of newton_solve (src/newton.cpp:80-87) and cg_solve's entry (19-30): p = 0, r = -g,
+// d = r. Every block derives `run` from the state written by the previous launch; block 0 alone
+// updates the state (it only ever clears `active` when `run` is false for every block as well).
+__global__ void __launch_bounds__(256) k_begin_init(int64_t d, DevState* st, const DevParams* prm,
+                                                    const double* __restrict__ g, double* __restrict__ p,
+                                                    double* __restrict__ r, double* __restrict__ dv) {
+    const double gn = st->g_norm;
+    const bool run = st->active && !(gn < prm->grad_tol) && gn > 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (st->active) {
+            st->rec_gnorm = gn;
+            if (gn < prm->grad_tol) {
+                st->converged = 1;
+                st->active = 0;
+            } else if (!(gn > 0.0)) {  // cg_solve requires ||g|| > 0 (ConfigError)
+                st->error = NADMM_ECONFIG;
+                st->active = 0;
+            }
         }
+        st->it_act = run;
+        st->cg_act[0] = run;
+        st->cg_iters = 0;
+        st->cg_neg = 0;
+        st->cg_failed = 0;
+        st->fallback = 0;
+        st->cg_residual = 0.0;
+        st->cg_stop = prm->cg_tol * gn;
+        st->r_sq[0] = st->g_sq;  // r = -g: |r|^2 == |g|^2 bit-for-bit under the same reduction order
+        st->ls_alpha = 0.0;
+        st->ls_evals = 0;
+        st->ls_capped = 0;
+        st->cert_act = run;
     }
-    st->it_act = run;
-    st->cg_act[0] = run;
-    st->cg_iters = 0;
-    st->cg_neg = 0;
-    st->cg_failed = 0;
-    st->fallback = 0;
-    st->cg_residual = 0.0;
-    st->cg_stop = prm->cg_tol * st->g_norm;
-    st->r_sq[0] = st->g_sq;  // r = -g: |r|^2 == |g|^2 bit-for-bit under the same reduction order
-    st->ls_alpha = 0.0;
-    st->ls_evals = 0;
-    st->ls_capped = 0;
-}
-
-// p = 0, r = -g, d = r.
-__global__ void k_cg_init(int64_t d, const double* __restrict__ g, double* __restrict__ p, double* __restrict__ r,
-                          double* __restrict__ dv, const int32_t* guard) {
-    if (guard && !*guard) return;
+    if (!run) return;
     GRID_STRIDE(j, d) {
         p[j] = 0.0;
         r[j] = -g[j];
@@ -143,33 +143,91 @@ __global__ void k_cg_init(int64_t d, const double* __restrict__ g, double* __res
     }
 }
 
-// One CG step after Hd = H d (src/newton.cpp:31-45): curvature test, p += a d, r -= a Hd, <r,r>.
-__global__ void k_cg_step(int it, int64_t d, DevState* st, const double* __restrict__ g, double* __restrict__ p,
-                          double* __restrict__ r, const double* __restrict__ dv, const double* __restrict__ hd,
-                          double* blk, int ncurv) {
+// Sum of the fused dense pass's split-K partials at element j, in cluster order (loads batched so
+// they are in flight together; the additions keep the sequential order).
+__device__ __forceinline__ double sum_chunks(const double* __restrict__ part, int chunks, int64_t d, int64_t j) {
+    double s = 0.0;
+    int ch = 0;
+    for (; ch + 8 <= chunks; ch += 8) {
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = part[(int64_t)(ch + q) * d + j];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s += v[q];
+    }
+    for (; ch < chunks; ++ch) s += part[(int64_t)ch * d + j];
+    return s;
+}
+
+// One fused CG tail per iteration (persistent grid, two software grid barriers), replacing the
+// finalize / step / direction launches:
+//   (0) chunks > 0: Hd = sum of the fused pass's split-K partials + lambda d (+ rho d when
+//       augmented) (src/softmax.cpp:108-110, src/objective.cpp:52-54), <d, Hd> partials
+//   (1) step:       curvature test, p += a d, r -= a Hd, <r, r> partials   (src/newton.cpp:31-45)
+//   (2) direction:  stop test, d = r + b d                                  (src/newton.cpp:46-50)
+// Every block reduces the same partials in the same order, so all blocks take the same branches.
+// Block 0 also refreshes cert_act (= the Newton iteration runs and CG did not fail) on every exit:
+// the last tail's value guards the certificate Hv.
+__global__ void __launch_bounds__(256, 4) k_cg_tail(int it, int64_t d, DevState* st, const DevParams* prm,
+                                                    const double* __restrict__ part, int chunks,
+                                                    const double* __restrict__ g, double* __restrict__ p,
+                                                    double* __restrict__ r, double* __restrict__ dv,
+                                                    double* __restrict__ hd, double* blk, int ncurv,
+                                                    unsigned long long* hv_ctr, unsigned long long* bar) {
     __shared__ double red[32];
-    __shared__ double curv_s;
-    if (!st->cg_act[it]) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) st->cg_mid[it] = 0;
+    __shared__ double sc;
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    auto done = [&](int act_next) {
+        if (lead) {
+            st->cg_act[it + 1] = act_next;
+            st->cert_act = st->it_act && !st->cg_failed;
+        }
+    };
+    if (!st->cg_act[it]) {  // grid-uniform: written by an earlier launch
+        if (lead) st->cg_mid[it] = 0;
+        done(0);
         return;
     }
-    const double curv = block_reduce_slot(blk, kSlotCurv, ncurv, &curv_s);
+    if (chunks > 0) {
+        if (hv_ctr && lead) atomicAdd(hv_ctr, 1ULL);
+        const double lam = prm->lambda;
+        const bool aug = prm->augmented;
+        const double rho = prm->rho;
+        double dacc = 0.0;
+        GRID_STRIDE(j, d) {
+            double s = sum_chunks(part, chunks, d, j);
+            const double vj = dv[j];
+            if (lam > 0.0) s = s + lam * vj;
+            if (aug) s = s + rho * vj;
+            hd[j] = s;
+            dacc += s * vj;
+        }
+        const double t = block_sum(dacc, red);
+        if (threadIdx.x == 0) slot_ptr(blk, kSlotCurv)[blockIdx.x] = t;
+        ncurv = gridDim.x;
+        grid_barrier(bar);
+    }
+    // ---- (1) step ----
+    const double curv = block_reduce_slot(blk, kSlotCurv, ncurv, &sc);
     if (!isfinite(curv)) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (lead) {
             st->cg_failed = 1;
             st->cg_mid[it] = 0;
         }
+        done(0);
         return;
     }
     if (curv <= 0.0) {
         if (it == 0) GRID_STRIDE(j, d) p[j] = -g[j];
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (lead) {
             st->cg_neg = 1;
             st->cg_mid[it] = 0;
         }
+        done(0);
         return;
     }
-    const double alpha = st->r_sq[it] / curv;
+    const double r_sq = st->r_sq[it];
+    const double alpha = r_sq / curv;
     double rr = 0.0;
     GRID_STRIDE(j, d) {
         p[j] += alpha * dv[j];
@@ -177,164 +235,153 @@ __global__ void k_cg_step(int it, int64_t d, DevState* st, const double* __restr
         r[j] = rj;
         rr += rj * rj;
     }
-    const double s = block_sum(rr, red);
-    if (threadIdx.x == 0) slot_ptr(blk, kSlotRr)[blockIdx.x] = s;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    {
+        const double t = block_sum(rr, red);
+        if (threadIdx.x == 0) slot_ptr(blk, kSlotRr)[blockIdx.x] = t;
+    }
+    if (lead) {
         st->cg_iters = it + 1;
         st->cg_mid[it] = 1;
     }
-}
-
-// Stop test and direction update (src/newton.cpp:46-50).
-__global__ void k_cg_dir(int it, int64_t d, DevState* st, const double* __restrict__ r, double* __restrict__ dv,
-                         double* blk, int nrr) {
-    __shared__ double rr_s;
-    if (!st->cg_mid[it]) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) st->cg_act[it + 1] = 0;
-        return;
-    }
-    const double r_sq_next = block_reduce_slot(blk, kSlotRr, nrr, &rr_s);
+    grid_barrier(bar);
+    // ---- (2) direction ----
+    __syncthreads();  // sc reused
+    const double r_sq_next = block_reduce_slot(blk, kSlotRr, gridDim.x, &sc);
     if (!isfinite(r_sq_next)) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            st->cg_failed = 1;
-            st->cg_act[it + 1] = 0;
-        }
+        if (lead) st->cg_failed = 1;
+        done(0);
         return;
     }
     if (sqrt(r_sq_next) <= st->cg_stop) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) st->cg_act[it + 1] = 0;
+        done(0);
         return;
     }
-    const double beta = r_sq_next / st->r_sq[it];
+    const double beta = r_sq_next / r_sq;
     GRID_STRIDE(j, d) dv[j] = r[j] + beta * dv[j];
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        st->r_sq[it + 1] = r_sq_next;
-        st->cg_act[it + 1] = 1;
-    }
+    if (lead) st->r_sq[it + 1] = r_sq_next;
+    done(1);
 }
 
-__global__ void k_after_cg(DevState* st) {
-    if (threadIdx.x == 0) st->cert_act = st->it_act && !st->cg_failed;
-}
-
-// Partials of |Hp + g|^2 for the CG certificate (src/newton.cpp:52).
-__global__ void k_cert(int64_t d, const double* __restrict__ hp, const double* __restrict__ g, double* blk,
-                       const int32_t* guard) {
-    if (guard && !*guard) return;
+// After the certificate Hv (src/newton.cpp:52) and cg_solve's return: |Hp + g| (report-only), the
+// CG-failure fallback p = -g (src/newton.cpp:100-104), the descent test p'g >= 0 -> p = -g
+// (105-109) and the line-search slope p'g. One grid barrier between the slope partials and the
+// decision.
+__global__ void __launch_bounds__(256, 4) k_cert_tail(int64_t d, DevState* st, const DevParams* prm,
+                                                      const double* __restrict__ part, int chunks,
+                                                      const double* __restrict__ g, double* __restrict__ p,
+                                                      double* __restrict__ hd, double* blk, int ncert,
+                                                      unsigned long long* hv_ctr, unsigned long long* bar) {
     __shared__ double red[32];
-    double s = 0.0;
+    __shared__ double sc;
+    if (!st->it_act) return;
+    const bool cert = st->cert_act, failed = st->cg_failed;
+    const double lam = prm->lambda, rho = prm->rho;
+    const bool aug = prm->augmented;
+    if (cert && chunks > 0 && hv_ctr && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(hv_ctr, 1ULL);
+    double cacc = 0.0, sacc = 0.0;
     GRID_STRIDE(j, d) {
-        const double v = hp[j] + g[j];
-        s += v * v;
+        const double gj = g[j];
+        double pj = p[j];
+        if (cert) {
+            double hp;
+            if (chunks > 0) {
+                hp = sum_chunks(part, chunks, d, j);
+                if (lam > 0.0) hp = hp + lam * pj;
+                if (aug) hp = hp + rho * pj;
+                hd[j] = hp;
+            } else {
+                hp = hd[j];
+            }
+            const double v = hp + gj;
+            cacc += v * v;
+        }
+        if (failed) {
+            pj = -gj;
+            p[j] = pj;
+        }
+        sacc += pj * gj;
     }
-    const double t = block_sum(s, red);
-    if (threadIdx.x == 0) slot_ptr(blk, kSlotCert)[blockIdx.x] = t;
-}
-
-// CG failure fallback p = -g (src/newton.cpp:100-104), then partials of <p, g>.
-__global__ void k_fallback(int64_t d, const DevState* st, const double* __restrict__ g, double* __restrict__ p,
-                           double* blk, const int32_t* guard) {
-    if (guard && !*guard) return;
-    __shared__ double red[32];
-    const bool failed = st->cg_failed;
-    double s = 0.0;
-    GRID_STRIDE(j, d) {
-        if (failed) p[j] = -g[j];
-        s += p[j] * g[j];
-    }
-    const double t = block_sum(s, red);
+    double t = block_sum(cacc, red);
+    if (threadIdx.x == 0 && cert) slot_ptr(blk, kSlotCert)[blockIdx.x] = t;
+    t = block_sum(sacc, red);
     if (threadIdx.x == 0) slot_ptr(blk, kSlotSlope)[blockIdx.x] = t;
-}
-
-// Descent test (src/newton.cpp:105-109): p'g >= 0 -> p = -g; the line-search slope p'g.
-__global__ void k_slope(int64_t d, DevState* st, const double* __restrict__ g, double* __restrict__ p, double* blk,
-                        int nslope, int ncert, const int32_t* guard) {
-    if (guard && !*guard) return;
-    __shared__ double sl_s;
-    double slope = block_reduce_slot(blk, kSlotSlope, nslope, &sl_s);
+    ncert = gridDim.x;
+    grid_barrier(bar);
+    double slope = block_reduce_slot(blk, kSlotSlope, gridDim.x, &sc);
     const bool flip = slope >= 0.0;
     if (flip) GRID_STRIDE(j, d) p[j] = -g[j];
     if (blockIdx.x == 0 && threadIdx.x < 32) {
-        const double cert = st->cert_act ? reduce_partials(slot_ptr(blk, kSlotCert), ncert) : 0.0;
+        const double cv = cert ? reduce_partials(slot_ptr(blk, kSlotCert), ncert) : 0.0;
         if (threadIdx.x == 0) {
             if (flip) slope = -st->g_sq;  // (-g).g == -|g|^2 under the same reduction order
             st->slope = slope;
-            if (st->cert_act) st->cg_residual = sqrt(cert);
-            if (st->cg_failed || flip) st->fallback = 1;
+            if (cert) st->cg_residual = sqrt(cv);
+            if (failed || flip) st->fallback = 1;
         }
     }
 }
 
-// Batched Armijo candidates, row part: for every trial a_j = gamma^j the loss of logits L0 + a_j Lp
-// (stable_exp_cache + loss at x + a_j p, src/softmax.cpp:51-78), accumulated per candidate.
+// Batched Armijo candidates (src/newton.cpp:56-71), partial sums for every trial a_j = gamma^j:
+//   blocks [0, rows_blocks): row losses of logits L0 + a_j Lp (stable_exp_cache + loss at x + a_j p,
+//     src/softmax.cpp:51-78); warp w of a block owns candidates w, w+8, ..., lane l one row of the
+//     block's 32-row group, so every (row, candidate) pair is an independent thread task
+//   blocks [rows_blocks, +vec_blocks): |z - x_j + y/rho|^2 (augmented) and |x_j|^2 (ridge)
+constexpr int kLsWarps = 8;
 constexpr int kLsChunk = 16;
 
-__global__ void __launch_bounds__(256) k_ls_rows(int64_t n, int K, const double* __restrict__ L0,
-                                                 const double* __restrict__ Lp, const int32_t* __restrict__ labels,
-                                                 const DevParams* prm, double* blk, const int32_t* guard) {
+__device__ __forceinline__ double ls_alpha(double gamma, int j) {
+    double a = 1.0;
+    for (int q = 0; q < j; ++q) a *= gamma;  // alpha *= backtrack_gamma (src/newton.cpp:69)
+    return a;
+}
+
+__global__ void __launch_bounds__(256) k_ls_partials(int64_t n, int K, const double* __restrict__ L0,
+                                                     const double* __restrict__ Lp, const int32_t* __restrict__ labels,
+                                                     int rows_blocks, int64_t d, const double* __restrict__ x,
+                                                     const double* __restrict__ p, const double* __restrict__ z,
+                                                     const double* __restrict__ y, const DevParams* prm, double* blk,
+                                                     const int32_t* guard) {
     if (guard && !*guard) return;
     __shared__ double red[32];
     const int nc = prm->ls_max_iters + 1;
     const double gamma = prm->backtrack_gamma;
-    double a0 = 1.0;
-    for (int j0 = 0; j0 < nc; j0 += kLsChunk) {
-        double alpha[kLsChunk], acc[kLsChunk];
-        double a = a0;
-#pragma unroll
-        for (int q = 0; q < kLsChunk; ++q) {
-            alpha[q] = a;
-            acc[q] = 0.0;
-            a *= gamma;  // alpha *= backtrack_gamma (src/newton.cpp:69)
-        }
-        a0 = a;
-        GRID_STRIDE(i, n) {
-            const double* l0 = L0 + i * K;
-            const double* lp = Lp + i * K;
-            const int b = labels[i];
-#pragma unroll
-            for (int q = 0; q < kLsChunk; ++q) {
-                if (j0 + q >= nc) break;
-                double m = l0[0] + alpha[q] * lp[0];
+    if ((int)blockIdx.x < rows_blocks) {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int j = warp; j < nc; j += kLsWarps) {
+            const double a = ls_alpha(gamma, j);
+            double acc = 0.0;
+            for (int64_t i = (int64_t)blockIdx.x * 32 + lane; i < n; i += (int64_t)rows_blocks * 32) {
+                const double* l0 = L0 + i * K;
+                const double* lp = Lp + i * K;
+                const int b = labels[i];
+                double m = l0[0] + a * lp[0];
                 for (int c = 1; c < K; ++c) {
-                    const double l = l0[c] + alpha[q] * lp[c];
+                    const double l = l0[c] + a * lp[c];
                     if (l > m) m = l;
                 }
                 m = m > 0.0 ? m : 0.0;
                 double s = 0.0;
-                for (int c = 0; c < K; ++c) s += exp((l0[c] + alpha[q] * lp[c]) - m);
+                for (int c = 0; c < K; ++c) s += exp((l0[c] + a * lp[c]) - m);
                 const double al = exp(-m) + s;
-                acc[q] += (m + log(al)) - (b <= K ? l0[b - 1] + alpha[q] * lp[b - 1] : 0.0);
+                acc += (m + log(al)) - (b <= K ? l0[b - 1] + a * lp[b - 1] : 0.0);
             }
+            acc = warp_sum(acc);
+            if (lane == 0) slot_ptr(blk, kSlotLs + j)[blockIdx.x] = acc;
         }
-        for (int q = 0; q < kLsChunk && j0 + q < nc; ++q) {
-            const double t = block_sum(acc[q], red);
-            if (threadIdx.x == 0) slot_ptr(blk, kSlotLs + j0 + q)[blockIdx.x] = t;
-        }
+        return;
     }
-}
-
-// Vector part of each candidate: |z - x_j + y/rho|^2 (augmented) and |x_j|^2 (ridge), x_j = x + a_j p.
-__global__ void __launch_bounds__(256) k_ls_vec(int64_t d, const double* __restrict__ x, const double* __restrict__ p,
-                                                const double* __restrict__ z, const double* __restrict__ y,
-                                                const DevParams* prm, double* blk, const int32_t* guard) {
-    if (guard && !*guard) return;
-    __shared__ double red[32];
-    const int nc = prm->ls_max_iters + 1;
-    const double gamma = prm->backtrack_gamma, rho = prm->rho;
+    const int vb = blockIdx.x - rows_blocks, nvb = gridDim.x - rows_blocks;
+    const double rho = prm->rho;
     const bool aug = prm->augmented, ridge = prm->lambda > 0.0;
-    double a0 = 1.0;
     for (int j0 = 0; j0 < nc; j0 += kLsChunk) {
         double alpha[kLsChunk], at[kLsChunk], ax[kLsChunk];
-        double a = a0;
 #pragma unroll
         for (int q = 0; q < kLsChunk; ++q) {
-            alpha[q] = a;
+            alpha[q] = ls_alpha(gamma, j0 + q);
             at[q] = 0.0;
             ax[q] = 0.0;
-            a *= gamma;
         }
-        a0 = a;
-        GRID_STRIDE(j, d) {
+        for (int64_t j = (int64_t)vb * blockDim.x + threadIdx.x; j < d; j += (int64_t)nvb * blockDim.x) {
             const double xj = x[j], pj = p[j];
             const double zj = aug ? z[j] : 0.0, yr = aug ? y[j] / rho : 0.0;
 #pragma unroll
@@ -349,46 +396,136 @@ __global__ void __launch_bounds__(256) k_ls_vec(int64_t d, const double* __restr
         }
         for (int q = 0; q < kLsChunk && j0 + q < nc; ++q) {
             double t = block_sum(at[q], red);
-            if (threadIdx.x == 0) slot_ptr(blk, kSlotLsVec + 2 * (j0 + q))[blockIdx.x] = t;
+            if (threadIdx.x == 0) slot_ptr(blk, kSlotLsVec + 2 * (j0 + q))[vb] = t;
             t = block_sum(ax[q], red);
-            if (threadIdx.x == 0) slot_ptr(blk, kSlotLsVec + 2 * (j0 + q) + 1)[blockIdx.x] = t;
+            if (threadIdx.x == 0) slot_ptr(blk, kSlotLsVec + 2 * (j0 + q) + 1)[vb] = t;
         }
     }
 }
 
-// Accept the first trial satisfying Armijo, else the last one flagged capped (src/newton.cpp:61-70).
-__global__ void k_ls_select(DevState* st, const DevParams* prm, double* blk, int nrows, int nvec,
-                            const int32_t* guard) {
+// Armijo selection (src/newton.cpp:61-70): accept the first trial with F(x + a p) <= f_x + a beta p'g,
+// else the last one, flagged capped; then x += a p (src/newton.cpp:120). Every block evaluates all
+// candidates (one warp per candidate, in parallel) from the same partials and picks the same a.
+__global__ void __launch_bounds__(256) k_ls_step(int64_t d, DevState* st, const DevParams* prm, const double* blk,
+                                                 int nrows, int nvec, double* __restrict__ x,
+                                                 const double* __restrict__ p, const int32_t* guard) {
     if (guard && !*guard) return;
-    if (threadIdx.x >= 32) return;
+    __shared__ double fj[kMaxLs + 1];
+    __shared__ double a_s;
     const int nc = prm->ls_max_iters + 1;
-    double alpha = 1.0;
-    int evals = 0, capped = 0;
-    for (int j = 0; j < nc; ++j) {
-        double f = reduce_partials(slot_ptr(blk, kSlotLs + j), nrows);
-        if (prm->lambda > 0.0) f += 0.5 * prm->lambda * reduce_partials(slot_ptr(blk, kSlotLsVec + 2 * j + 1), nvec);
-        if (prm->augmented) f = f + 0.5 * prm->rho * reduce_partials(slot_ptr(blk, kSlotLsVec + 2 * j), nvec);
-        ++evals;
-        if (f <= st->f_x + alpha * prm->armijo_beta * st->slope) break;
-        if (j >= prm->ls_max_iters) {
-            capped = 1;
-            break;
-        }
-        alpha *= prm->backtrack_gamma;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = warp; j < nc; j += (int)(blockDim.x >> 5)) {
+        double f = reduce_partials(slot_ptr(const_cast<double*>(blk), kSlotLs + j), nrows);
+        if (prm->lambda > 0.0)
+            f += 0.5 * prm->lambda * reduce_partials(slot_ptr(const_cast<double*>(blk), kSlotLsVec + 2 * j + 1), nvec);
+        if (prm->augmented)
+            f = f + 0.5 * prm->rho * reduce_partials(slot_ptr(const_cast<double*>(blk), kSlotLsVec + 2 * j), nvec);
+        if (lane == 0) fj[j] = f;
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
-        st->ls_alpha = alpha;
-        st->ls_evals = evals;
-        st->ls_capped = capped;
+        double alpha = 1.0;
+        int evals = 0, capped = 0;
+        for (int j = 0; j < nc; ++j) {
+            ++evals;
+            if (fj[j] <= st->f_x + alpha * prm->armijo_beta * st->slope) break;
+            if (j >= prm->ls_max_iters) {
+                capped = 1;
+                break;
+            }
+            alpha *= prm->backtrack_gamma;
+        }
+        a_s = alpha;
+        if (blockIdx.x == 0) {
+            st->ls_alpha = alpha;
+            st->ls_evals = evals;
+            st->ls_capped = capped;
+        }
     }
+    __syncthreads();
+    const double a = a_s;
+    GRID_STRIDE(j, d) x[j] += a * p[j];
 }
 
-// x += alpha p (src/newton.cpp:120).
-__global__ void k_step(int64_t d, const DevState* st, double* __restrict__ x, const double* __restrict__ p,
-                       const int32_t* guard) {
+// End of a Newton iteration after the cache pass at the new x (src/newton.cpp:121-127 with the memo
+// of src/objective.cpp:9-39): gbase = X^T(P - Y) + lambda x from the split-K partials (chunks > 0),
+// <x, x> for the ridge, t = z - x + y/rho and g = gbase - rho t (src/objective.cpp:47-51) with
+// <g,g>, <t,t> partials; after one grid barrier block 0 forms the base loss, f, |g| and the trace
+// row (k_value_finish semantics).
+__global__ void __launch_bounds__(256, 4) k_newton_tail(int64_t d, DevState* st, const DevParams* prm,
+                                                        const double* __restrict__ part, int chunks,
+                                                        const double* __restrict__ x, const double* __restrict__ z,
+                                                        const double* __restrict__ y, double* __restrict__ gbase,
+                                                        double* __restrict__ g, double* __restrict__ t, double* blk,
+                                                        int nloss, double* scal, DevTrace* trace, int trace_cap,
+                                                        unsigned long long* bar, const int32_t* guard) {
     if (guard && !*guard) return;
-    const double a = st->ls_alpha;
-    GRID_STRIDE(j, d) x[j] += a * p[j];
+    __shared__ double red[32];
+    const double lam = prm->lambda, rho = prm->rho;
+    const bool aug = prm->augmented;
+    double xx = 0.0, gg = 0.0, tt = 0.0;
+    GRID_STRIDE(j, d) {
+        const double xj = x[j];
+        double gb;
+        if (chunks > 0) {
+            gb = sum_chunks(part, chunks, d, j);
+            if (lam > 0.0) gb = gb + lam * xj;  // src/softmax.cpp:93
+            gbase[j] = gb;
+        } else {
+            gb = gbase[j];
+        }
+        xx += xj * xj;
+        double gj = gb;
+        if (aug) {
+            const double tj = (z[j] - xj) + y[j] / rho;
+            t[j] = tj;
+            tt += tj * tj;
+            gj = gj - rho * tj;
+        }
+        g[j] = gj;
+        gg += gj * gj;
+    }
+    double sres = block_sum(xx, red);
+    if (threadIdx.x == 0) slot_ptr(blk, kSlotRidge)[blockIdx.x] = sres;
+    sres = block_sum(gg, red);
+    if (threadIdx.x == 0) slot_ptr(blk, kSlotGg)[blockIdx.x] = sres;
+    sres = block_sum(tt, red);
+    if (threadIdx.x == 0) slot_ptr(blk, kSlotTt)[blockIdx.x] = sres;
+    grid_barrier(bar);
+    if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+    const int nvec = gridDim.x;
+    double base = reduce_partials(slot_ptr(blk, kSlotLoss), nloss);
+    if (lam > 0.0) base += 0.5 * lam * reduce_partials(slot_ptr(blk, kSlotRidge), nvec);  // src/softmax.cpp:76
+    const double g_sq = reduce_partials(slot_ptr(blk, kSlotGg), nvec);
+    const double t_sq = reduce_partials(slot_ptr(blk, kSlotTt), nvec);
+    if (threadIdx.x != 0) return;
+    scal[0] = base;
+    double f = base;
+    if (aug) f = f + 0.5 * rho * t_sq;
+    st->f_base = base;
+    st->f_x = f;
+    st->g_sq = g_sq;
+    st->g_norm = sqrt(g_sq);
+    const int k = st->iter;
+    if (k < trace_cap) {
+        DevTrace rr;
+        rr.iter = k;
+        rr.grad_norm = st->rec_gnorm;
+        rr.step = st->ls_alpha;
+        rr.cg_iters = st->cg_failed ? 0 : st->cg_iters;
+        rr.cg_residual = st->cg_failed ? 0.0 : st->cg_residual;
+        rr.objective = f;
+        rr.ls_capped = st->ls_capped;
+        rr.cg_fallback = st->fallback;
+        rr.fn_evals = st->ls_evals;
+        rr.pad = 0;
+        trace[k] = rr;
+    }
+    st->iter = k + 1;
+    if (!isfinite(f)) {  // "non-finite objective at iteration k"
+        st->error = NADMM_ESOLVER;
+        st->active = 0;
+    }
 }
 
 __global__ void k_set_int(int32_t* dst, int v) {
@@ -414,43 +551,53 @@ void launch_value_finish(Shard& s, int nvec, int prologue, const int32_t* guard)
     LAUNCH_COUNT(s);
 }
 
+// One Newton iteration (src/newton.cpp:80-127) as a fixed launch sequence (captured once into a
+// CUDA graph): per CG iteration one data pass + one fused tail; the certificate Hv + one tail; the
+// Lp pass + batched Armijo partials + selection/step; the cache pass at the new x + one tail.
+// Iterations that are not needed are switched off by device flags (guards), not by the host.
 void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
     (void)ls_max;
     cudaStream_t st = s.ctx->stream;
     const int grid = vec_grid(*s.ctx, s.d);
     const int32_t* it_act = &s.st->it_act;
-    k_newton_begin<<<1, 32, 0, st>>>(s.st, s.prm);
-    k_cg_init<<<grid, 256, 0, st>>>(s.d, s.g, s.pd, s.r, s.dv, it_act);
-    s.ctx->stats.kernel_launches += 2;
+    k_begin_init<<<grid, 256, 0, st>>>(s.d, s.st, s.prm, s.g, s.pd, s.r, s.dv);
+    tl_mark(s, "begin_init");
+    LAUNCH_COUNT(s);
     for (int it = 0; it < cg_max; ++it) {
         s.hv_timer_site = it;
-        const int ncurv = op_hv(s, s.dv, s.hd, s.dv, kSlotCurv, &s.st->cg_act[it]);
+        int chunks = 0;
+        const int ncurv = op_hv_split(s, s.dv, s.hd, s.dv, kSlotCurv, &s.st->cg_act[it], &chunks);
         s.hv_timer_site = -1;
-        k_cg_step<<<grid, 256, 0, st>>>(it, s.d, s.st, s.g, s.pd, s.r, s.dv, s.hd, s.blk, ncurv);
-        k_cg_dir<<<grid, 256, 0, st>>>(it, s.d, s.st, s.r, s.dv, s.blk, grid);
-        s.ctx->stats.kernel_launches += 2;
+        k_cg_tail<<<grid, 256, 0, st>>>(it, s.d, s.st, s.prm, s.part, chunks, s.g, s.pd, s.r, s.dv, s.hd, s.blk, ncurv,
+                                        chunks > 0 ? s.ctx->dctr : nullptr, s.gbar + 0);
+        tl_mark(s, "cg_tail");
+        LAUNCH_COUNT(s);
     }
-    k_after_cg<<<1, 32, 0, st>>>(s.st);
-    LAUNCH_COUNT(s);
     s.hv_timer_site = cg_max;
-    op_hv(s, s.pd, s.hd, nullptr, 0, &s.st->cert_act);  // certificate Hv (src/newton.cpp:52)
+    int chunks = 0;
+    op_hv_split(s, s.pd, s.hd, nullptr, 0, &s.st->cert_act, &chunks);  // certificate Hv (src/newton.cpp:52)
     s.hv_timer_site = -1;
-    k_cert<<<grid, 256, 0, st>>>(s.d, s.hd, s.g, s.blk, &s.st->cert_act);
-    k_fallback<<<grid, 256, 0, st>>>(s.d, s.st, s.g, s.pd, s.blk, it_act);
-    k_slope<<<grid, 256, 0, st>>>(s.d, s.st, s.g, s.pd, s.blk, grid, grid, it_act);
-    s.ctx->stats.kernel_launches += 3;
+    k_cert_tail<<<grid, 256, 0, st>>>(s.d, s.st, s.prm, s.part, chunks, s.g, s.pd, s.hd, s.blk, grid,
+                                      chunks > 0 ? s.ctx->dctr : nullptr, s.gbar + 1);
+    tl_mark(s, "cert_tail");
+    LAUNCH_COUNT(s);
     op_lp(s, s.pd, it_act);  // Lp = X p: one data pass serves every Armijo trial
-    const int rgrid = std::max(1, (int)std::min<int64_t>((s.n + 255) / 256, std::min<int64_t>(kBlockPartials, 4LL * s.ctx->num_sms)));
-    k_ls_rows<<<rgrid, 256, 0, st>>>(s.n, s.K, s.L0, s.Lp, s.labels, s.prm, s.blk, it_act);
-    k_ls_vec<<<grid, 256, 0, st>>>(s.d, s.x, s.pd, s.z, s.y, s.prm, s.blk, it_act);
-    k_ls_select<<<1, 32, 0, st>>>(s.st, s.prm, s.blk, rgrid, grid, it_act);
-    k_step<<<grid, 256, 0, st>>>(s.d, s.st, s.x, s.pd, it_act);
-    s.ctx->stats.kernel_launches += 4;
+    tl_mark(s, "lp_pass");
+    const int rblocks = std::max(1, (int)std::min<int64_t>((s.n + 31) / 32, kBlockPartials));
+    k_ls_partials<<<rblocks + grid, 256, 0, st>>>(s.n, s.K, s.L0, s.Lp, s.labels, rblocks, s.d, s.x, s.pd, s.z, s.y,
+                                                  s.prm, s.blk, it_act);
+    tl_mark(s, "ls_partials");
+    k_ls_step<<<grid, 256, 0, st>>>(s.d, s.st, s.prm, s.blk, rblocks, grid, s.x, s.pd, it_act);
+    tl_mark(s, "ls_step");
+    s.ctx->stats.kernel_launches += 2;
     NADMM_LAUNCH_CHECK();
-    op_cache_grad(s, s.x, it_act);
-    int nvec = 0;
-    launch_grad_aug(s, it_act, &nvec);
-    launch_value_finish(s, nvec, 0, it_act);
+    chunks = op_cache_split(s, s.x, it_act);
+    tl_mark(s, "cache_pass");
+    k_newton_tail<<<grid, 256, 0, st>>>(s.d, s.st, s.prm, s.part, chunks, s.x, s.z, s.y, s.gbase, s.g, s.t, s.blk,
+                                        s.rows_grid, s.scal, s.trace, kTraceCap, s.gbar + 2, it_act);
+    tl_mark(s, "newton_tail");
+    LAUNCH_COUNT(s);
+    NADMM_LAUNCH_CHECK();
 }
 
 void launch_set_int(Shard& s, int32_t* dst, int v) {

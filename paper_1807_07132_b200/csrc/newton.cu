@@ -4,6 +4,7 @@
 // iteration (CG with device-side stop flags, certificate Hv, fallbacks, batched Armijo search,
 // step, fused cache+gradient pass at the new point), replayed per iteration. The host synchronises
 // once per Newton iteration (once per outer ADMM iteration with inner_iters = 1).
+#include <cstdlib>
 #include <cstring>
 
 #include "solver.h"
@@ -25,6 +26,28 @@ void op_cache_grad(Shard& s, const double* w, const int32_t* guard) {
     loss_finalize(s, w, 1, s.scal + 0, guard);
 }
 
+int op_cache_split(Shard& s, const double* w, const int32_t* guard) {
+    if (dmma_supported(s)) {
+        dmma_pass(s, kModeCache, w, guard);
+        return s.last_chunks;
+    }
+    rows_pass(s, kModeCache, w, guard);
+    xtu_pass(s, kXtuGrad, w, s.gbase, nullptr, 0, guard);
+    return 0;
+}
+
+void tl_mark(Shard& s, const char* name) {
+    if (!s.tl_capture) return;
+    const size_t i = s.tl_names.size();
+    if (i >= s.tl_events.size()) {
+        cudaEvent_t e;
+        NADMM_CUDA(cudaEventCreate(&e));
+        s.tl_events.push_back(e);
+    }
+    NADMM_CUDA(cudaEventRecordWithFlags(s.tl_events[i], s.ctx->stream, cudaEventRecordExternal));
+    s.tl_names.push_back(name);
+}
+
 int op_hv(Shard& s, const double* v, double* out, const double* dotvec, int dot_slot, const int32_t* guard) {
     HvTimer* tm = (s.capture_timing && s.hv_timer_site >= 0 && s.hv_timer_site < (int)s.hv_timers.size())
                       ? &s.hv_timers[s.hv_timer_site]
@@ -34,13 +57,32 @@ int op_hv(Shard& s, const double* v, double* out, const double* dotvec, int dot_
     if (dmma_supported(s)) {
         dmma_pass(s, kModeHv, v, guard);
         if (tm) NADMM_CUDA(cudaEventRecordWithFlags(tm->stop, s.ctx->stream, cudaEventRecordExternal));
-        finalize_partials(s, s.last_chunks,kXtuHv, v, out, dotvec, dot_slot, guard, &g);
+        tl_mark(s, "hv_dmma_pass");
+        finalize_partials(s, s.last_chunks, kXtuHv, v, out, dotvec, dot_slot, guard, &g);
+        tl_mark(s, "hv_finalize");
     } else {
         rows_pass(s, kModeHv, v, guard);
+        tl_mark(s, "hv_rows_pass");
         g = xtu_pass(s, kXtuHv, v, out, dotvec, dot_slot, guard);
         if (tm) NADMM_CUDA(cudaEventRecordWithFlags(tm->stop, s.ctx->stream, cudaEventRecordExternal));
+        tl_mark(s, "hv_xtu_pass");
     }
     return g;
+}
+
+int op_hv_split(Shard& s, const double* v, double* out, const double* dotvec, int dot_slot, const int32_t* guard,
+                int* chunks) {
+    *chunks = 0;
+    if (!dmma_supported(s)) return op_hv(s, v, out, dotvec, dot_slot, guard);
+    HvTimer* tm = (s.capture_timing && s.hv_timer_site >= 0 && s.hv_timer_site < (int)s.hv_timers.size())
+                      ? &s.hv_timers[s.hv_timer_site]
+                      : nullptr;
+    if (tm) NADMM_CUDA(cudaEventRecordWithFlags(tm->start, s.ctx->stream, cudaEventRecordExternal));
+    dmma_pass(s, kModeHv, v, guard);
+    if (tm) NADMM_CUDA(cudaEventRecordWithFlags(tm->stop, s.ctx->stream, cudaEventRecordExternal));
+    tl_mark(s, "hv_dmma_pass");
+    *chunks = s.last_chunks;
+    return 0;
 }
 
 void op_lp(Shard& s, const double* p, const int32_t* guard) {
@@ -122,10 +164,16 @@ static void capture_iteration_graph(Shard& s, int cg_max, int ls_max) {
     NADMM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     try {
         s.capture_timing = s.ctx->timing;
+        static const bool tl = getenv("NADMM_GRAPH_TIMELINE") != nullptr;
+        s.tl_capture = tl;
+        s.tl_names.clear();
+        tl_mark(s, "start");
         launch_newton_iteration(s, cg_max, ls_max);
         s.capture_timing = false;
+        s.tl_capture = false;
     } catch (...) {
         s.capture_timing = false;
+        s.tl_capture = false;
         cudaStreamEndCapture(st, &graph);
         if (graph) cudaGraphDestroy(graph);
         throw;
@@ -140,9 +188,12 @@ static void capture_iteration_graph(Shard& s, int cg_max, int ls_max) {
     s.g_timing = s.ctx->timing;
 }
 
-// Reads back the solver state; accumulates the Hv timers of the Hv passes that actually ran.
+// Reads back the solver state and trace (one async copy each, one sync); accumulates the Hv timers
+// of the Hv passes that actually ran.
 static void readback(Shard& s, int cg_max) {
     NADMM_CUDA(cudaMemcpyAsync(s.st_host, s.st, sizeof(DevState), cudaMemcpyDeviceToHost, s.ctx->stream));
+    NADMM_CUDA(cudaMemcpyAsync(s.trace_host, s.trace, sizeof(DevTrace) * kTraceCap, cudaMemcpyDeviceToHost,
+                               s.ctx->stream));
     NADMM_CUDA(cudaStreamSynchronize(s.ctx->stream));
     if (s.g_timing && !s.hv_timers.empty()) {
         const DevState& h = *s.st_host;
@@ -158,8 +209,7 @@ static void readback(Shard& s, int cg_max) {
     }
 }
 
-SolveResult device_newton_solve(Shard& s, const nadmm_newton_cfg& cfg, double lambda, bool aug, double rho,
-                                int newton_max) {
+bool solve_launch(Shard& s, const nadmm_newton_cfg& cfg, double lambda, bool aug, double rho, int newton_max) {
     validate_newton_cfg(cfg);
     if (aug && rho <= 0.0) raise(NADMM_ECONFIG, "augmented objective requires rho > 0");
     set_params(s, cfg, lambda, aug, rho);
@@ -168,7 +218,13 @@ SolveResult device_newton_solve(Shard& s, const nadmm_newton_cfg& cfg, double la
     int nvec = 0;
     launch_grad_aug(s, nullptr, &nvec);
     launch_value_finish(s, nvec, 1, nullptr);
-    SolveResult res;
+    s.cache_at = Shard::kAtX;
+    s.cache_lambda = lambda;
+    if (newton_max == 1) {  // no host decision needed: the caller collects after enqueueing other work
+        NADMM_CUDA(cudaGraphLaunch(s.g_iter, s.ctx->stream));
+        s.ctx->stats.kernel_launches += s.g_nodes;
+        return false;
+    }
     for (int k = 0; k < newton_max; ++k) {
         NADMM_CUDA(cudaGraphLaunch(s.g_iter, s.ctx->stream));
         s.ctx->stats.kernel_launches += s.g_nodes;
@@ -176,9 +232,13 @@ SolveResult device_newton_solve(Shard& s, const nadmm_newton_cfg& cfg, double la
         if (!s.st_host->active) break;
     }
     if (newton_max == 0) readback(s, cfg.cg_max_iters);
+    return true;
+}
+
+SolveResult solve_collect(Shard& s, const nadmm_newton_cfg& cfg, bool pending) {
+    if (pending) readback(s, cfg.cg_max_iters);
     const DevState& h = *s.st_host;
-    s.cache_at = Shard::kAtX;
-    s.cache_lambda = lambda;
+    SolveResult res;
     if (h.error) {
         res.error = h.error;
         return res;
@@ -186,12 +246,7 @@ SolveResult device_newton_solve(Shard& s, const nadmm_newton_cfg& cfg, double la
     res.iterations = h.iter;
     res.final_grad_norm = h.g_norm;
     res.converged = h.g_norm < cfg.grad_tol;  // src/newton.cpp:128-130 (or the early return at 83-86)
-    res.trace.resize(std::min(h.iter, kTraceCap));
-    if (!res.trace.empty())
-        NADMM_CUDA(cudaMemcpy(res.trace.data(), s.trace, sizeof(DevTrace) * res.trace.size(), cudaMemcpyDeviceToHost));
-    res.cg_sum = 0;
-    res.fe_sum = 0;
-    res.flags = 0;
+    res.trace.assign(s.trace_host, s.trace_host + std::min(h.iter, kTraceCap));
     for (const auto& t : res.trace) {
         res.cg_sum += t.cg_iters;
         res.fe_sum += t.fn_evals;
@@ -199,6 +254,12 @@ SolveResult device_newton_solve(Shard& s, const nadmm_newton_cfg& cfg, double la
         if (t.cg_fallback) res.flags |= 2;
     }
     return res;
+}
+
+SolveResult device_newton_solve(Shard& s, const nadmm_newton_cfg& cfg, double lambda, bool aug, double rho,
+                                int newton_max) {
+    const bool done = solve_launch(s, cfg, lambda, aug, rho, newton_max);
+    return solve_collect(s, cfg, !done);
 }
 
 }  // namespace nadmm

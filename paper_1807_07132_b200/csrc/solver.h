@@ -21,6 +21,11 @@ void set_params(Shard& s, const nadmm_newton_cfg& c, double lambda, bool aug, do
 void set_lambda_only(Shard& s, double lambda);
 void ensure_cache_at_x(Shard& s, double lambda);
 // newton_solve (src/newton.cpp:73-132) from s.x with z/y in s.z/s.y; result x left in s.x.
+// Split form for callers that run several shards back to back: solve_launch enqueues the solve
+// (returns false when the result is still pending: newton_max == 1 needs no host decision) and
+// solve_collect reads it back.
+bool solve_launch(Shard& s, const nadmm_newton_cfg& cfg, double lambda, bool aug, double rho, int newton_max);
+SolveResult solve_collect(Shard& s, const nadmm_newton_cfg& cfg, bool pending);
 SolveResult device_newton_solve(Shard& s, const nadmm_newton_cfg& cfg, double lambda, bool aug, double rho,
                                 int newton_max);
 

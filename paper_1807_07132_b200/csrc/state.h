@@ -128,6 +128,7 @@ struct Shard {
     double* part = nullptr;
     int part_chunks = 0;
     double* blk = nullptr;
+    unsigned long long* gbar = nullptr;  // grid-barrier counters of the persistent vector kernels
     int rows_grid = 0;  // blocks of the last rows pass (partials count)
     int last_chunks = 0;    // split-K partial chunks written by the last fused DMMA pass
     int dmma_clusters = 0;  // co-resident clusters of the fused DMMA pass (0: path unavailable)
@@ -149,6 +150,7 @@ struct Shard {
     int32_t* pred = nullptr;
     DevParams* prm_host = nullptr;  // pinned staging
     DevState* st_host = nullptr;    // pinned readback
+    DevTrace* trace_host = nullptr; // pinned readback (kTraceCap rows)
     // captured solver graph (one Newton iteration)
     cudaGraphExec_t g_iter = nullptr;
     int g_cg_max = -1, g_ls_max = -1;
@@ -158,6 +160,10 @@ struct Shard {
     std::vector<HvTimer> hv_timers;
     int hv_timer_site = -1;
     bool capture_timing = false;
+    // optional per-node timeline of the captured iteration graph (NADMM_GRAPH_TIMELINE=1, profiling)
+    bool tl_capture = false;
+    std::vector<const char*> tl_names;
+    std::vector<cudaEvent_t> tl_events;
     void ensure_timers(int n);
     ~Shard();
 };
@@ -179,11 +185,23 @@ void finalize_partials(Shard& s, int chunks, XtuKind kind, const double* vin, do
                        int dot_slot, const int32_t* guard, int* dot_grid);
 
 // ---- composite ops (ops.cu) ----
-void op_cache_grad(Shard& s, const double* w, const int32_t* guard);   // L0,P,M,alpha,loss,gbase at w
+void op_cache_grad(Shard& s, const double* w, const int32_t* guard);
+// Cache pass only (the caller finalizes gbase / loss): returns the split-K chunk count of the fused
+// dense pass, or 0 when gbase was written directly (SIMT / sparse path).
+int op_cache_split(Shard& s, const double* w, const int32_t* guard);   // L0,P,M,alpha,loss,gbase at w
 int op_hv(Shard& s, const double* v, double* out, const double* dotvec, int dot_slot, const int32_t* guard);
 void op_lp(Shard& s, const double* p, const int32_t* guard);
 void op_value(Shard& s, const double* w, double* dst, int add_ridge, const int32_t* guard);
 void op_predict(Shard& s, const double* w);
+
+// Timeline mark: during a profiling capture, record an event node named `name` (the time since the
+// previous mark is attributed to it). No-op otherwise.
+void tl_mark(Shard& s, const char* name);
+// Hv for the CG loop: with the fused dense pass only the pass kernel is launched and its split-K
+// partial count is returned in *chunks (the caller finalizes); otherwise the full Hv is written to
+// `out` with <out, dotvec> partials (returned count) and *chunks = 0.
+int op_hv_split(Shard& s, const double* v, double* out, const double* dotvec, int dot_slot, const int32_t* guard,
+                int* chunks);
 
 // ---- dense fast path (kernels_dmma.cu) ----
 bool dmma_supported(const Shard& s);
