@@ -55,7 +55,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                 "--format=csv,noheader,nounits", "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                 text=True)
         except Exception:
             self.proc = None
@@ -229,16 +229,19 @@ def main():
 
     # ---------------- value: device-resident consensus loop ----------------
     sess = nadmm.AdmmSession(shards, cfg, nadmm.EvalContext(eval_objective=True, ignore_convergence=True), comm)
+    # clocks are sampled from the warm-up on (the timed region alone can be shorter than a sample)
+    clk = Clocks(local).__enter__()
+    time.sleep(0.5)  # nvidia-smi start-up
     sess.step(args.warmup)
     ctx.set_timing(True)
     barrier()
     ctx.reset_stats()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
-        e0.record(stream)
-        done = sess.step(args.steps)
-        e1.record(stream)
-        e1.synchronize()
+    e0.record(stream)
+    done = sess.step(args.steps)
+    e1.record(stream)
+    e1.synchronize()
+    clk.__exit__(None, None, None)
     ms = max_over_ranks(e0.elapsed_time(e1))
     st = ctx.stats()
     barrier()
