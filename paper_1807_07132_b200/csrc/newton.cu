@@ -15,9 +15,20 @@ namespace nadmm {
 // ---------------------------------------------------------------------------------------------
 // Composite ops (one or two data passes each)
 // ---------------------------------------------------------------------------------------------
+// The single-pass fused kernels (X read once per product, split-K partials per block / cluster):
+// the small-p row-per-thread kernel, else the DMMA cluster kernel; otherwise the SIMT two-pass path.
+bool fused_supported(const Shard& s) { return smallp_supported(s) || dmma_supported(s); }
+
+void fused_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
+    if (smallp_supported(s))
+        smallp_pass(s, mode, W, guard);
+    else
+        dmma_pass(s, mode, W, guard);
+}
+
 void op_cache_grad(Shard& s, const double* w, const int32_t* guard) {
-    if (dmma_supported(s)) {
-        dmma_pass(s, kModeCache, w, guard);
+    if (fused_supported(s)) {
+        fused_pass(s, kModeCache, w, guard);
         finalize_partials(s, s.last_chunks,kXtuGrad, w, s.gbase, nullptr, 0, guard, nullptr);
     } else {
         rows_pass(s, kModeCache, w, guard);
@@ -27,8 +38,8 @@ void op_cache_grad(Shard& s, const double* w, const int32_t* guard) {
 }
 
 int op_cache_split(Shard& s, const double* w, const int32_t* guard) {
-    if (dmma_supported(s)) {
-        dmma_pass(s, kModeCache, w, guard);
+    if (fused_supported(s)) {
+        fused_pass(s, kModeCache, w, guard);
         return s.last_chunks;
     }
     rows_pass(s, kModeCache, w, guard);
@@ -54,10 +65,10 @@ int op_hv(Shard& s, const double* v, double* out, const double* dotvec, int dot_
                       : nullptr;
     if (tm) NADMM_CUDA(cudaEventRecordWithFlags(tm->start, s.ctx->stream, cudaEventRecordExternal));
     int g = 0;
-    if (dmma_supported(s)) {
-        dmma_pass(s, kModeHv, v, guard);
+    if (fused_supported(s)) {
+        fused_pass(s, kModeHv, v, guard);
         if (tm) NADMM_CUDA(cudaEventRecordWithFlags(tm->stop, s.ctx->stream, cudaEventRecordExternal));
-        tl_mark(s, "hv_dmma_pass");
+        tl_mark(s, "hv_fused_pass");
         finalize_partials(s, s.last_chunks, kXtuHv, v, out, dotvec, dot_slot, guard, &g);
         tl_mark(s, "hv_finalize");
     } else {
@@ -73,34 +84,39 @@ int op_hv(Shard& s, const double* v, double* out, const double* dotvec, int dot_
 int op_hv_split(Shard& s, const double* v, double* out, const double* dotvec, int dot_slot, const int32_t* guard,
                 int* chunks) {
     *chunks = 0;
-    if (!dmma_supported(s)) return op_hv(s, v, out, dotvec, dot_slot, guard);
+    if (!fused_supported(s)) return op_hv(s, v, out, dotvec, dot_slot, guard);
     HvTimer* tm = (s.capture_timing && s.hv_timer_site >= 0 && s.hv_timer_site < (int)s.hv_timers.size())
                       ? &s.hv_timers[s.hv_timer_site]
                       : nullptr;
     if (tm) NADMM_CUDA(cudaEventRecordWithFlags(tm->start, s.ctx->stream, cudaEventRecordExternal));
-    dmma_pass(s, kModeHv, v, guard);
+    fused_pass(s, kModeHv, v, guard);
     if (tm) NADMM_CUDA(cudaEventRecordWithFlags(tm->stop, s.ctx->stream, cudaEventRecordExternal));
-    tl_mark(s, "hv_dmma_pass");
+    tl_mark(s, "hv_fused_pass");
     *chunks = s.last_chunks;
     return 0;
 }
 
 void op_lp(Shard& s, const double* p, const int32_t* guard) {
-    if (dmma_supported(s))
-        dmma_pass(s, kModeLp, p, guard);
+    if (fused_supported(s))
+        fused_pass(s, kModeLp, p, guard);
     else
         rows_pass(s, kModeLp, p, guard);
 }
 
 void op_value(Shard& s, const double* w, double* dst, int add_ridge, const int32_t* guard) {
-    if (dmma_supported(s))
-        dmma_pass(s, kModeValue, w, guard);
+    if (fused_supported(s))
+        fused_pass(s, kModeValue, w, guard);
     else
         rows_pass(s, kModeValue, w, guard);
     loss_finalize(s, w, add_ridge, dst, guard);
 }
 
-void op_predict(Shard& s, const double* w) { rows_pass(s, kModePredict, w, nullptr); }
+void op_predict(Shard& s, const double* w) {
+    if (smallp_supported(s))
+        smallp_pass(s, kModePredict, w, nullptr);
+    else
+        rows_pass(s, kModePredict, w, nullptr);
+}
 
 // ---------------------------------------------------------------------------------------------
 // Solver driver

@@ -203,6 +203,12 @@ void tl_mark(Shard& s, const char* name);
 int op_hv_split(Shard& s, const double* v, double* out, const double* dotvec, int dot_slot, const int32_t* guard,
                 int* chunks);
 
+// ---- small-p dense path (kernels_smallp.cu): p*(C-1) <= 64 ----
+bool smallp_supported(const Shard& s);
+void smallp_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
+bool fused_supported(const Shard& s);
+void fused_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
+
 // ---- dense fast path (kernels_dmma.cu) ----
 bool dmma_supported(const Shard& s);
 // Once per shard, outside stream capture: kernel attributes + co-resident cluster count.

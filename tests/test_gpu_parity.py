@@ -16,7 +16,8 @@ TOL_KERNEL = 1e-12
 TOL_NEWTON = 1e-10
 TOL_ADMM = 1e-9
 
-DENSE_SHAPES = [(50, 7, 4), (200, 33, 10), (129, 5, 2), (300, 28, 2), (1000, 784, 10), (96, 3072, 10), (77, 65, 21)]
+DENSE_SHAPES = [(50, 7, 4), (200, 33, 10), (129, 5, 2), (300, 28, 2), (1000, 784, 10), (96, 3072, 10), (77, 65, 21),
+                (64, 31, 3), (100, 60, 2), (3000, 28, 2)]
 
 
 def shards(nadmm, X, y, C):
