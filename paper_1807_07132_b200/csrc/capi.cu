@@ -90,6 +90,7 @@ void alloc_work(Shard& s) {
         s.part = dev_alloc<double>(s, s.part_chunks * s.d);
     }
     dmma_setup(s);
+    gemm_setup(s);
     s.blk = dev_alloc<double>(s, (int64_t)kSlotCount * kBlockPartials);
     NADMM_CUDA(cudaMemsetAsync(s.blk, 0, sizeof(double) * kSlotCount * kBlockPartials, s.ctx->stream));
     for (double** v : {&s.x, &s.g, &s.pd, &s.r, &s.dv, &s.hd, &s.z, &s.y, &s.t, &s.tmp, &s.gbase, &s.cache_x}) {
@@ -230,6 +231,7 @@ nadmm_status nadmm_ctx_destroy(nadmm_ctx ctx) {
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
         if (ctx->dctr) cudaFree(ctx->dctr);
+        gemm_teardown(*ctx);
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });

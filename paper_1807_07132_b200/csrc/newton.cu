@@ -17,13 +17,15 @@ namespace nadmm {
 // ---------------------------------------------------------------------------------------------
 // The single-pass fused kernels (X read once per product, split-K partials per block / cluster):
 // the small-p row-per-thread kernel, else the DMMA cluster kernel; otherwise the SIMT two-pass path.
-bool fused_supported(const Shard& s) { return smallp_supported(s) || dmma_supported(s); }
+bool fused_supported(const Shard& s) { return smallp_supported(s) || dmma_supported(s) || gemm_supported(s); }
 
 void fused_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
     if (smallp_supported(s))
         smallp_pass(s, mode, W, guard);
-    else
+    else if (dmma_supported(s))
         dmma_pass(s, mode, W, guard);
+    else
+        gemm_pass(s, mode, W, guard);
 }
 
 void op_cache_grad(Shard& s, const double* w, const int32_t* guard) {
@@ -114,6 +116,8 @@ void op_value(Shard& s, const double* w, double* dst, int add_ridge, const int32
 void op_predict(Shard& s, const double* w) {
     if (smallp_supported(s))
         smallp_pass(s, kModePredict, w, nullptr);
+    else if (!dmma_supported(s) && gemm_supported(s))
+        gemm_pass(s, kModePredict, w, nullptr);
     else
         rows_pass(s, kModePredict, w, nullptr);
 }

@@ -71,6 +71,8 @@ struct Ctx {
     nadmm_stats stats{};
     bool timing = false;
     unsigned long long* dctr = nullptr;  // device counters: [0] Hv products applied
+    void* blas = nullptr;     // cublasHandle_t of the GEMM path (created with the first dense shard)
+    void* blas_ws = nullptr;  // its fixed workspace
 };
 
 struct HvTimer {
@@ -206,6 +208,11 @@ int op_hv_split(Shard& s, const double* v, double* out, const double* dotvec, in
 // ---- small-p dense path (kernels_smallp.cu): p*(C-1) <= 64 ----
 bool smallp_supported(const Shard& s);
 void smallp_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
+// ---- GEMM path (kernels_gemm.cu): dense shards outside the fused passes' shapes ----
+void gemm_setup(Shard& s);
+void gemm_teardown(Ctx& c);
+bool gemm_supported(const Shard& s);
+void gemm_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
 bool fused_supported(const Shard& s);
 void fused_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
 
