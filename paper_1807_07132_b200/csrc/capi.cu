@@ -91,6 +91,7 @@ void alloc_work(Shard& s) {
     }
     dmma_setup(s);
     gemm_setup(s);
+    if (s.sparse && s.K <= 32) s.wt = dev_alloc<double>(s, s.d);
     s.blk = dev_alloc<double>(s, (int64_t)kSlotCount * kBlockPartials);
     NADMM_CUDA(cudaMemsetAsync(s.blk, 0, sizeof(double) * kSlotCount * kBlockPartials, s.ctx->stream));
     for (double** v : {&s.x, &s.g, &s.pd, &s.r, &s.dv, &s.hd, &s.z, &s.y, &s.t, &s.tmp, &s.gbase, &s.cache_x}) {
@@ -156,7 +157,7 @@ Shard::~Shard() {
         if (t.stop) cudaEventDestroy(t.stop);
     }
     for (cudaEvent_t e : tl_events) cudaEventDestroy(e);
-    for (double** v : {&X, &vals, &cval, &L0, &P, &U, &Lp, &rowM, &rowA, &part, &blk, &cache_x, &gbase, &scal, &x, &g,
+    for (double** v : {&X, &wt, &vals, &cval, &L0, &P, &U, &Lp, &rowM, &rowA, &part, &blk, &cache_x, &gbase, &scal, &x, &g,
                        &pd, &r, &dv, &hd, &z, &y, &t, &tmp})
         dev_free(*v);
     dev_free(indptr);

@@ -323,6 +323,7 @@ int vec_grid(const Ctx& c, int64_t d) {
 }
 
 void rows_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
+    if (sparse_lanes_supported(s)) return sparse_rows_pass(s, mode, W, guard);
     RowsArgs a{};
     a.X = s.X;
     a.ldx = s.ldx;
@@ -387,6 +388,7 @@ void finalize_partials(Shard& s, int chunks, XtuKind kind, const double* vin, do
 int xtu_pass(Shard& s, XtuKind kind, const double* vin, double* out, const double* dotvec, int dot_slot,
              const int32_t* guard) {
     cudaStream_t st = s.ctx->stream;
+    if (sparse_lanes_supported(s)) return sparse_cols_pass(s, kind, vin, out, dotvec, dot_slot, guard);
     if (s.sparse) {
         const int grid = (int)std::min<int64_t>((s.p + 7) / 8, std::min<int64_t>(kBlockPartials, 8LL * s.ctx->num_sms));
         csc_xtu_kernel<<<std::max(grid, 1), 256, 0, st>>>(s.cptr, s.crow, s.cval, s.p, s.K, s.U, vin, s.prm, kind, out,

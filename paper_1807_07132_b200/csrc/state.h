@@ -119,6 +119,7 @@ struct Shard {
     int64_t* indptr = nullptr;
     int32_t* indices = nullptr;
     double* vals = nullptr;
+    double* wt = nullptr;  // p x K interleaved copy of the pass operand (class-per-lane sparse passes)
     int64_t* cptr = nullptr;
     int32_t* crow = nullptr;
     double* cval = nullptr;
@@ -204,6 +205,12 @@ void tl_mark(Shard& s, const char* name);
 // `out` with <out, dotvec> partials (returned count) and *chunks = 0.
 int op_hv_split(Shard& s, const double* v, double* out, const double* dotvec, int dot_slot, const int32_t* guard,
                 int* chunks);
+
+// ---- class-per-lane sparse passes (kernels_sparse.cu): CSR shards with C - 1 <= 32 ----
+bool sparse_lanes_supported(const Shard& s);
+void sparse_rows_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
+int sparse_cols_pass(Shard& s, XtuKind kind, const double* vin, double* out, const double* dotvec, int dot_slot,
+                     const int32_t* guard);
 
 // ---- small-p dense path (kernels_smallp.cu): p*(C-1) <= 64 ----
 bool smallp_supported(const Shard& s);
