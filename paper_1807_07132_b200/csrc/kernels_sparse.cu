@@ -19,12 +19,23 @@ namespace nadmm {
 namespace {
 
 constexpr int kSpRowsThreads = 256;
+constexpr int kGather = 8;  // independent gathers in flight per warp
 
-__global__ void transpose_w_kernel(const double* __restrict__ W, int64_t p, int K, double* __restrict__ wt,
-                                   const int32_t* guard) {
+// wt (p x K) = transpose of the block-major W (K x p): 32-column tiles through shared memory so both
+// the reads (along p) and the writes (32*K contiguous doubles) are coalesced.
+__global__ void __launch_bounds__(256) transpose_w_kernel(const double* __restrict__ W, int64_t p, int K,
+                                                          double* __restrict__ wt, const int32_t* guard) {
     if (guard && !*guard) return;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p; j += (int64_t)gridDim.x * blockDim.x)
-        for (int c = 0; c < K; ++c) wt[j * K + c] = W[(int64_t)c * p + j];
+    __shared__ double tile[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
+    for (int64_t j0 = (int64_t)blockIdx.x * 32; j0 < p; j0 += (int64_t)gridDim.x * 32) {
+        for (int c = ty; c < K; c += 8) tile[c][tx] = (j0 + tx < p) ? W[(int64_t)c * p + j0 + tx] : 0.0;
+        __syncthreads();
+        const int64_t base = j0 * K;
+        const int64_t total = (p - j0 < 32 ? p - j0 : 32) * K;
+        for (int q = threadIdx.x; q < total; q += 256) wt[base + q] = tile[q % K][q / K];
+        __syncthreads();
+    }
 }
 
 struct SpArgs {
@@ -62,18 +73,18 @@ __global__ void __launch_bounds__(kSpRowsThreads) sparse_rows_kernel(SpArgs a) {
         const int64_t q0 = a.indptr[i], q1 = a.indptr[i + 1];
         double lg = 0.0;
         int64_t q = q0;
-        for (; q + 4 <= q1; q += 4) {  // four independent gathers in flight, accumulated in CSR order
-            int j[4];
-            double v[4], w[4];
+        for (; q + kGather <= q1; q += kGather) {  // kGather gathers in flight, accumulated in CSR order
+            int j[kGather];
+            double v[kGather], w[kGather];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < kGather; ++k) {
                 j[k] = __ldg(a.indices + q + k);
                 v[k] = __ldg(a.vals + q + k);
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) w[k] = on ? __ldg(a.wt + (int64_t)j[k] * K + lane) : 0.0;
+            for (int k = 0; k < kGather; ++k) w[k] = on ? __ldg(a.wt + (int64_t)j[k] * K + lane) : 0.0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) lg += v[k] * w[k];
+            for (int k = 0; k < kGather; ++k) lg += v[k] * w[k];
         }
         for (; q < q1; ++q) {
             const double w = on ? __ldg(a.wt + (int64_t)__ldg(a.indices + q) * K + lane) : 0.0;
@@ -155,18 +166,18 @@ __global__ void __launch_bounds__(256) csc_cols_kernel(const int64_t* __restrict
         const int64_t q0 = cptr[j], q1 = cptr[j + 1];
         double acc = 0.0;
         int64_t q = q0;
-        for (; q + 4 <= q1; q += 4) {
-            int r[4];
-            double v[4], u[4];
+        for (; q + kGather <= q1; q += kGather) {
+            int r[kGather];
+            double v[kGather], u[kGather];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < kGather; ++k) {
                 r[k] = __ldg(crow + q + k);
                 v[k] = __ldg(cval + q + k);
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) u[k] = on ? U[(int64_t)r[k] * K + lane] : 0.0;
+            for (int k = 0; k < kGather; ++k) u[k] = on ? U[(int64_t)r[k] * K + lane] : 0.0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) acc += v[k] * u[k];
+            for (int k = 0; k < kGather; ++k) acc += v[k] * u[k];
         }
         for (; q < q1; ++q) acc += __ldg(cval + q) * (on ? U[(int64_t)__ldg(crow + q) * K + lane] : 0.0);
         if (on) {
@@ -190,7 +201,7 @@ bool sparse_lanes_supported(const Shard& s) { return s.sparse && s.K <= 32 && s.
 
 void sparse_rows_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
     cudaStream_t st = s.ctx->stream;
-    const int tg = (int)std::max<int64_t>(1, std::min<int64_t>((s.p + 255) / 256, 4LL * s.ctx->num_sms));
+    const int tg = (int)std::max<int64_t>(1, std::min<int64_t>((s.p + 31) / 32, 8LL * s.ctx->num_sms));
     transpose_w_kernel<<<tg, 256, 0, st>>>(W, s.p, s.K, s.wt, guard);
     NADMM_LAUNCH_CHECK();
     SpArgs a{};
