@@ -116,6 +116,15 @@ __device__ __forceinline__ void st_async_v2(uint32_t remote_addr, double x, doub
                  : "memory");
 }
 
+// Bulk copy of a local shared-memory buffer into a peer CTA's shared memory (cluster addresses for
+// the destination and its mbarrier), completing `bytes` on that mbarrier: one instruction per peer.
+__device__ __forceinline__ void bulk_s2cluster(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     dst),
+                 "r"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
 // Fixed-topology pairwise sum of v[0..n) (n <= N): depth log2(N) instead of a serial chain. The
 // auxiliary warps share the FP64 pipe with the compute warps' DMMAs, so every dependent FP64 op on
 // their critical path costs a pipe turn; trees keep those paths short. Deterministic by construction.
@@ -177,7 +186,7 @@ __device__ long long g_dmma_trace[64][16];  // per-tile clock64 stamps of CTA 0 
 #endif
 
 #ifndef NADMM_DMMA_PREFETCH
-#define NADMM_DMMA_PREFETCH 8
+#define NADMM_DMMA_PREFETCH 0
 #endif
 constexpr int kDmmaPrefetch = NADMM_DMMA_PREFETCH;  // L2 prefetch distance in tiles (0: off)
 #ifndef NADMM_DMMA_CHAINS
@@ -185,7 +194,38 @@ constexpr int kDmmaPrefetch = NADMM_DMMA_PREFETCH;  // L2 prefetch distance in t
 #endif
 constexpr int kDmmaChains = NADMM_DMMA_CHAINS;  // phase-A accumulator chains per warp
 
-constexpr int kDmmaRecvBufs = 4;  // receive buffers per CTA, flow-controlled by remote credits
+#ifdef NADMM_EXP_NOA
+constexpr bool kExpNoA = true;  // timing experiments only (wrong results)
+#else
+constexpr bool kExpNoA = false;
+#endif
+#ifdef NADMM_EXP_NOB
+constexpr bool kExpNoB = true;
+#else
+constexpr bool kExpNoB = false;
+#endif
+#ifdef NADMM_EXP_NOXCHG
+constexpr bool kExpNoXchg = true;
+#else
+constexpr bool kExpNoXchg = false;
+#endif
+#ifdef NADMM_EXP_NOREM
+constexpr bool kExpNoRem = true;
+#else
+constexpr bool kExpNoRem = false;
+#endif
+#ifndef NADMM_DMMA_RECV_BUFS
+#define NADMM_DMMA_RECV_BUFS 4
+#endif
+#ifndef NADMM_DMMA_EXTRA_STAGES
+#define NADMM_DMMA_EXTRA_STAGES 2
+#endif
+#ifndef NADMM_DMMA_BULK_PUSH
+#define NADMM_DMMA_BULK_PUSH 1
+#endif
+constexpr bool kDmmaBulkPush = NADMM_DMMA_BULK_PUSH;  // exchange by bulk smem->peer copies (else st.async)
+constexpr int kDmmaRecvBufs = NADMM_DMMA_RECV_BUFS;  // receive buffers per CTA, flow-controlled by remote credits
+constexpr int kDmmaExtraStages = NADMM_DMMA_EXTRA_STAGES;  // ring stages beyond the LAG tiles held for phase B
 constexpr int kDmmaRedBufs = 2;   // compute-warp partial buffers (pusher frees them)
 constexpr int kDmmaEpiWarps = 2;  // epilogue warps
 constexpr int kDmmaAux = kDmmaEpiWarps + 2;  // + pusher + producer
@@ -201,7 +241,8 @@ struct DmmaSmem {
 __host__ __device__ inline size_t dmma_smem_bytes(int stages, int bm, int nc, int S, int K, int cs) {
     const int KS = ((K + 15) / 16) * 16 + 4, KP = (K + 1) & ~1, KE = (K + 1) & ~1;
     const size_t dbl = (size_t)stages * bm * S + (size_t)stages * bm * KE + (size_t)kDmmaRedBufs * nc * bm * KP +
-                       (size_t)kDmmaRecvBufs * cs * bm * KP + (size_t)stages * bm * KS + (size_t)kDmmaEpiWarps * bm * KP + 128;
+                       (size_t)kDmmaRecvBufs * cs * bm * KP + (size_t)kDmmaRecvBufs * bm * KP + (size_t)stages * bm * KS +
+                       (size_t)kDmmaEpiWarps * bm * KP + 128;
     const int nbars = 2 * stages + 2 * kDmmaRedBufs + 2 * kDmmaRecvBufs + stages;
     return sizeof(double) * dbl + 4 * ((size_t)stages * bm + 4) + 8 * (nbars + 1);
 }
@@ -210,7 +251,7 @@ __host__ __device__ inline size_t dmma_smem_bytes(int stages, int bm, int nc, in
 template <int MT, int KT, int R, int BM, int LAG, int MODE>
 __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
     using namespace dmma_detail;
-    constexpr int STAGES = LAG + 2;
+    constexpr int STAGES = LAG + kDmmaExtraStages;
     constexpr int K = 8 * KT + R;
     static_assert(BM % 8 == 0 && BM <= 32, "row tile");
     constexpr int KS = DmmaSmem<K>::KS;
@@ -241,7 +282,8 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
     double* ps = xs + (size_t)STAGES * BM * S;                       // STAGES x BM x KE (P rows)
     double* red = ps + (size_t)STAGES * BM * KE;                     // kDmmaRedBufs x nc x PART
     double* recv = red + (size_t)kDmmaRedBufs * nc * PART;           // kDmmaRecvBufs x CS x PART (peers)
-    double* ut = recv + (size_t)kDmmaRecvBufs * csize * PART;        // STAGES x BM x KS
+    double* sendb = recv + (size_t)kDmmaRecvBufs * csize * PART;     // kDmmaRecvBufs x PART (own partial)
+    double* ut = sendb + (size_t)kDmmaRecvBufs * PART;               // STAGES x BM x KS
     double* lgb = ut + (size_t)STAGES * BM * KS;                     // kDmmaEpiWarps x BM x KP logits
     double* misc = lgb + (size_t)kDmmaEpiWarps * BM * KP;           // 128 doubles
     int32_t* ys = reinterpret_cast<int32_t*>(misc + 128);            // STAGES x BM labels
@@ -320,7 +362,7 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
             mbar_wait(&red_full[b], (uint32_t)((i / kDmmaRedBufs) & 1));
             DMMA_TRACE(i, 2);
             // every CTA of the cluster released receive buffer br (its previous tile's epilogue is done)
-            if (i >= kDmmaRecvBufs) mbar_wait(&credit[br], (uint32_t)(((i / kDmmaRecvBufs) - 1) & 1));
+            if (!kExpNoXchg && i >= kDmmaRecvBufs) mbar_wait(&credit[br], (uint32_t)(((i / kDmmaRecvBufs) - 1) & 1));
             const double* rd = red + (size_t)b * nc * PART;
             const uint32_t dst_local = smem_u32(recv + ((size_t)br * csize + crank) * PART);
             const uint32_t bar_local = smem_u32(&rbar[br]);
@@ -333,9 +375,25 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                     v0[w] = v.x;
                     v1[w] = v.y;
                 }
+#ifdef NADMM_EXP_NOPUSHSUM
+                const double s0 = v0[0], s1 = v1[0];  // timing experiment only (wrong results)
+#else
                 const double s0 = tree_sum(v0, nc), s1 = tree_sum(v1, nc);
-                for (uint32_t q = 0; q < csize; ++q)
-                    st_async_v2(mapa(dst_local + 16u * i2, q), s0, s1, mapa(bar_local, q));
+#endif
+                if (kDmmaBulkPush)
+                    *reinterpret_cast<double2*>(sendb + (size_t)br * PART + 2 * i2) = make_double2(s0, s1);
+                else
+                    for (uint32_t q = 0; q < csize; ++q)
+                        st_async_v2(mapa(dst_local + 16u * i2, q), s0, s1, mapa(bar_local, q));
+            }
+            if (kDmmaBulkPush && !kExpNoXchg) {
+                // the summed partial goes to every peer as one bulk copy each (lane q -> CTA q); the
+                // send buffer br is rewritten only after every peer returned its credit for br
+                fence_proxy_async();
+                __syncwarp();
+                if (lane < (int)csize)
+                    bulk_s2cluster(mapa(dst_local, (uint32_t)lane), smem_u32(sendb + (size_t)br * PART), PART * 8u,
+                                   mapa(bar_local, (uint32_t)lane));
             }
             __syncwarp();
             DMMA_TRACE(i, 3);
@@ -353,8 +411,10 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
         for (int i = ew; i < T; i += kDmmaEpiWarps) {
             const int stage = i % STAGES, br = i % kDmmaRecvBufs;
             const int64_t r0 = tile_of(i) * BM;
-            if (lane == 0) mbar_expect_tx(&rbar[br], (uint32_t)csize * PART * 8u);
-            mbar_wait(&rbar[br], (uint32_t)((i / kDmmaRecvBufs) & 1));
+            if (!kExpNoXchg) {
+                if (lane == 0) mbar_expect_tx(&rbar[br], (uint32_t)csize * PART * 8u);
+                mbar_wait(&rbar[br], (uint32_t)((i / kDmmaRecvBufs) & 1));
+            }
             if (ew == 0) DMMA_TRACE(i, 4);
             if (NEED_P || NEED_Y) mbar_wait(&full[stage], (uint32_t)((i / STAGES) & 1));
             if (ew == 0) DMMA_TRACE(i, 8);
@@ -374,14 +434,18 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
 #pragma unroll
                 for (int j = 0; j < NE; ++j) {
                     const int e = lane + 32 * j;
+#ifdef NADMM_EXP_NOEPI
+                    const double s = v[j][0];  // timing experiment only (wrong results)
+#else
                     const double s = tree_sum(v[j], (int)csize);
+#endif
                     if (e < BM * K) lgw[(e / K) * KP + (e % K)] = s;
                 }
             }
             __syncwarp();
             if (ew == 0) DMMA_TRACE(i, 9);
             // receive buffer br consumed: return one credit to every CTA of the cluster
-            if (lane == 0)
+            if (lane == 0 && !kExpNoXchg)
                 for (uint32_t q = 0; q < csize; ++q) mbar_arrive_remote(&credit[br], q);
             if (ew == 0) DMMA_TRACE(i, 11);
             // (2) row epilogue, one lane per row
@@ -405,7 +469,11 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                             }
                             vt[c] = vw[c];
                         }
+#ifdef NADMM_EXP_NOEPI
+                        const double rs = vt[0];  // timing experiment only (wrong results)
+#else
                         const double rs = tree_sum(vt, K);  // row_sum(V o P)
+#endif
 #pragma unroll
                         for (int c = 0; c < K; ++c) urow[c] = vw[c] - pv[c] * rs;
                     } else {
@@ -546,9 +614,9 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                 for (int g = 0; g < G; ++g) {
                     const double x = xt[(g * 8 + gq) * S + fw + 4 * s + tq];
 #pragma unroll
-                    for (int kt = 0; kt < KT; ++kt) dmma(acca[s % NCH][g][kt], x, bv[s][kt]);
+                    for (int kt = 0; kt < KT; ++kt) if (!kExpNoA) dmma(acca[s % NCH][g][kt], x, bv[s][kt]);
 #pragma unroll
-                    for (int r = 0; r < R; ++r) accar[s % RC][g][r] = fma(x, vr[s][r], accar[s % RC][g][r]);
+                    for (int r = 0; r < R; ++r) if (!kExpNoRem) accar[s % RC][g][r] = fma(x, vr[s][r], accar[s % RC][g][r]);
                 }
             }
 #pragma unroll
@@ -612,12 +680,12 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                     for (int mp = 0; mp < MT / 2; ++mp) {
                         const double2 x2 = *reinterpret_cast<const double2*>(xr + mp * 16 + 2 * gq);
 #pragma unroll
-                        for (int kt = 0; kt < KT; ++kt) {
+                        for (int kt = 0; kt < KT; ++kt) if (!kExpNoB) {
                             dmma(accb[2 * mp][kt], x2.x, ub[kt]);
                             dmma(accb[2 * mp + 1][kt], x2.y, ub[kt]);
                         }
 #pragma unroll
-                        for (int r = 0; r < R; ++r) {
+                        for (int r = 0; r < R; ++r) if (!kExpNoRem) {
                             accbr[2 * mp][r] = fma(x2.x, ur[r], accbr[2 * mp][r]);
                             accbr[2 * mp + 1][r] = fma(x2.y, ur[r], accbr[2 * mp + 1][r]);
                         }

@@ -41,8 +41,11 @@ namespace nadmm {
 namespace {
 
 constexpr int kBM = 8;
-constexpr int kLag = 4;
-constexpr int kStages = kLag + 2;
+#ifndef NADMM_DMMA_LAG
+#define NADMM_DMMA_LAG 4
+#endif
+constexpr int kLag = NADMM_DMMA_LAG;
+constexpr int kStages = kLag + kDmmaExtraStages;
 
 struct Layout {
     bool ok = false;
