@@ -91,6 +91,7 @@ void alloc_work(Shard& s) {
     }
     dmma_setup(s);
     gemm_setup(s);
+    tail_setup(s);
     if (s.sparse && s.K <= 32) s.wt = dev_alloc<double>(s, s.d);
     s.blk = dev_alloc<double>(s, (int64_t)kSlotCount * kBlockPartials);
     NADMM_CUDA(cudaMemsetAsync(s.blk, 0, sizeof(double) * kSlotCount * kBlockPartials, s.ctx->stream));

@@ -9,6 +9,8 @@
 // scalars every block derives are bit-identical and branch decisions are consistent grid-wide.
 // Flags that a kernel both reads and decides live in per-iteration slots (cg_act / cg_mid), so no
 // block ever observes a flag written by another block of the same launch.
+#include <cooperative_groups.h>
+
 #include "solver_kernels.h"
 
 namespace nadmm {
@@ -143,19 +145,18 @@ __global__ void __launch_bounds__(256) k_begin_init(int64_t d, DevState* st, con
     }
 }
 
-// Sum of the fused dense pass's split-K partials at element j, in cluster order (loads batched so
-// they are in flight together; the additions keep the sequential order).
+// Sum of the fused dense pass's split-K partials at element j, in chunk order: loads are issued in
+// predicated batches of 8 so they are in flight together; the additions keep the sequential order.
 __device__ __forceinline__ double sum_chunks(const double* __restrict__ part, int chunks, int64_t d, int64_t j) {
     double s = 0.0;
-    int ch = 0;
-    for (; ch + 8 <= chunks; ch += 8) {
+    for (int ch = 0; ch < chunks; ch += 8) {
         double v[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = part[(int64_t)(ch + q) * d + j];
+        for (int q = 0; q < 8; ++q) v[q] = (ch + q < chunks) ? part[(int64_t)(ch + q) * d + j] : 0.0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) s += v[q];
+        for (int q = 0; q < 8; ++q)
+            if (ch + q < chunks) s += v[q];
     }
-    for (; ch < chunks; ++ch) s += part[(int64_t)ch * d + j];
     return s;
 }
 
@@ -166,8 +167,12 @@ __device__ __forceinline__ double sum_chunks(const double* __restrict__ part, in
 //   (1) step:       curvature test, p += a d, r -= a Hd, <r, r> partials   (src/newton.cpp:31-45)
 //   (2) direction:  stop test, d = r + b d                                  (src/newton.cpp:46-50)
 // Every block reduces the same partials in the same order, so all blocks take the same branches.
-// Block 0 also refreshes cert_act (= the Newton iteration runs and CG did not fail) on every exit:
-// the last tail's value guards the certificate Hv.
+// The kernel is a chain of dependent L2 round trips (partials -> barrier -> reduction -> ...), so each
+// thread keeps its (at most EPT) elements of d, p, r, Hd in registers across the phases and loads
+// everything it will need before the first barrier. Block 0 also refreshes cert_act (= the Newton
+// iteration runs and CG did not fail) on every exit: the last tail's value guards the certificate Hv.
+constexpr int kTailEpt = 2;
+
 __global__ void __launch_bounds__(256, 4) k_cg_tail(int it, int64_t d, DevState* st, const DevParams* prm,
                                                     const double* __restrict__ part, int chunks,
                                                     const double* __restrict__ g, double* __restrict__ p,
@@ -188,19 +193,50 @@ __global__ void __launch_bounds__(256, 4) k_cg_tail(int it, int64_t d, DevState*
         done(0);
         return;
     }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool cached = d <= stride * kTailEpt;  // grid-uniform
+    double vd[kTailEpt], vp[kTailEpt], vr[kTailEpt], vh[kTailEpt];
+    const double r_sq = st->r_sq[it], cg_stop = st->cg_stop;
+    if (cached) {
+#pragma unroll
+        for (int e = 0; e < kTailEpt; ++e) {
+            const int64_t j = j0 + e * stride;
+            const bool in = j < d;
+            vd[e] = in ? dv[j] : 0.0;
+            vp[e] = in ? p[j] : 0.0;
+            vr[e] = in ? r[j] : 0.0;
+            vh[e] = (in && chunks == 0) ? hd[j] : 0.0;
+        }
+    }
     if (chunks > 0) {
         if (hv_ctr && lead) atomicAdd(hv_ctr, 1ULL);
         const double lam = prm->lambda;
         const bool aug = prm->augmented;
         const double rho = prm->rho;
         double dacc = 0.0;
-        GRID_STRIDE(j, d) {
-            double s = sum_chunks(part, chunks, d, j);
-            const double vj = dv[j];
-            if (lam > 0.0) s = s + lam * vj;
-            if (aug) s = s + rho * vj;
-            hd[j] = s;
-            dacc += s * vj;
+        if (cached) {
+#pragma unroll
+            for (int e = 0; e < kTailEpt; ++e) {
+                const int64_t j = j0 + e * stride;
+                if (j < d) {
+                    double s = sum_chunks(part, chunks, d, j);
+                    if (lam > 0.0) s = s + lam * vd[e];
+                    if (aug) s = s + rho * vd[e];
+                    hd[j] = s;
+                    vh[e] = s;
+                    dacc += s * vd[e];
+                }
+            }
+        } else {
+            GRID_STRIDE(j, d) {
+                double s = sum_chunks(part, chunks, d, j);
+                const double vj = dv[j];
+                if (lam > 0.0) s = s + lam * vj;
+                if (aug) s = s + rho * vj;
+                hd[j] = s;
+                dacc += s * vj;
+            }
         }
         const double t = block_sum(dacc, red);
         if (threadIdx.x == 0) slot_ptr(blk, kSlotCurv)[blockIdx.x] = t;
@@ -226,14 +262,27 @@ __global__ void __launch_bounds__(256, 4) k_cg_tail(int it, int64_t d, DevState*
         done(0);
         return;
     }
-    const double r_sq = st->r_sq[it];
     const double alpha = r_sq / curv;
     double rr = 0.0;
-    GRID_STRIDE(j, d) {
-        p[j] += alpha * dv[j];
-        const double rj = r[j] - alpha * hd[j];
-        r[j] = rj;
-        rr += rj * rj;
+    if (cached) {
+#pragma unroll
+        for (int e = 0; e < kTailEpt; ++e) {
+            const int64_t j = j0 + e * stride;
+            if (j < d) {
+                vp[e] += alpha * vd[e];
+                vr[e] = vr[e] - alpha * vh[e];
+                p[j] = vp[e];
+                r[j] = vr[e];
+                rr += vr[e] * vr[e];
+            }
+        }
+    } else {
+        GRID_STRIDE(j, d) {
+            p[j] += alpha * dv[j];
+            const double rj = r[j] - alpha * hd[j];
+            r[j] = rj;
+            rr += rj * rj;
+        }
     }
     {
         const double t = block_sum(rr, red);
@@ -252,12 +301,157 @@ __global__ void __launch_bounds__(256, 4) k_cg_tail(int it, int64_t d, DevState*
         done(0);
         return;
     }
-    if (sqrt(r_sq_next) <= st->cg_stop) {
+    if (sqrt(r_sq_next) <= cg_stop) {
         done(0);
         return;
     }
     const double beta = r_sq_next / r_sq;
-    GRID_STRIDE(j, d) dv[j] = r[j] + beta * dv[j];
+    if (cached) {
+#pragma unroll
+        for (int e = 0; e < kTailEpt; ++e) {
+            const int64_t j = j0 + e * stride;
+            if (j < d) dv[j] = vr[e] + beta * vd[e];
+        }
+    } else {
+        GRID_STRIDE(j, d) dv[j] = r[j] + beta * dv[j];
+    }
+    if (lead) st->r_sq[it + 1] = r_sq_next;
+    done(1);
+}
+
+// The same CG tail on ONE thread-block cluster (up to 16 CTAs x 1024 threads) for the d of the dense
+// shards: the two grid-wide exchanges become hardware cluster barriers, and the block partials are
+// summed through distributed shared memory (every CTA reads the CS partials in rank order, so all
+// CTAs derive bit-identical scalars). Each thread keeps its <= kClEpt elements in registers.
+constexpr int kClThreads = 1024;
+constexpr int kClEpt = 2;
+
+__device__ __forceinline__ double cluster_sum(cooperative_groups::cluster_group& cl, double* slot, double v,
+                                              double* red) {
+    // block sum in fixed order -> this CTA's slot; cluster barrier; every CTA sums the slots in rank order
+    const double t = block_sum(v, red);
+    if (threadIdx.x == 0) *slot = t;
+    cl.sync();
+    __shared__ double res;
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (unsigned q = 0; q < cl.num_blocks(); ++q) s += *cl.map_shared_rank(slot, q);
+        res = s;
+    }
+    __syncthreads();
+    return res;
+}
+
+__global__ void __launch_bounds__(kClThreads, 1) k_cg_tail_cl(int it, int64_t d, DevState* st, const DevParams* prm,
+                                                              const double* __restrict__ part, int chunks,
+                                                              const double* __restrict__ g, double* __restrict__ p,
+                                                              double* __restrict__ r, double* __restrict__ dv,
+                                                              double* __restrict__ hd, const double* blk, int ncurv,
+                                                              unsigned long long* hv_ctr) {
+    namespace cgs = cooperative_groups;
+    cgs::cluster_group cl = cgs::this_cluster();
+    __shared__ double red[32];
+    __shared__ double slots[3];  // curvature, <r,r> (read by peers through DSMEM)
+    __shared__ double sc;
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    auto done = [&](int act_next) {
+        if (lead) {
+            st->cg_act[it + 1] = act_next;
+            st->cert_act = st->it_act && !st->cg_failed;
+        }
+        cl.sync();  // no CTA exits while peers may still read its slots
+    };
+    if (!st->cg_act[it]) {
+        if (lead) st->cg_mid[it] = 0;
+        done(0);
+        return;
+    }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double vd[kClEpt], vp[kClEpt], vr[kClEpt], vh[kClEpt];
+    const double r_sq = st->r_sq[it], cg_stop = st->cg_stop;
+    const double lam = prm->lambda, rho = prm->rho;
+    const bool aug = prm->augmented;
+#pragma unroll
+    for (int e = 0; e < kClEpt; ++e) {
+        const int64_t j = j0 + e * stride;
+        const bool in = j < d;
+        vd[e] = in ? dv[j] : 0.0;
+        vp[e] = in ? p[j] : 0.0;
+        vr[e] = in ? r[j] : 0.0;
+        vh[e] = (in && chunks == 0) ? hd[j] : 0.0;
+    }
+    double curv;
+    if (chunks > 0) {
+        if (hv_ctr && lead) atomicAdd(hv_ctr, 1ULL);
+        double dacc = 0.0;
+#pragma unroll
+        for (int e = 0; e < kClEpt; ++e) {
+            const int64_t j = j0 + e * stride;
+            if (j < d) {
+                double s = sum_chunks(part, chunks, d, j);
+                if (lam > 0.0) s = s + lam * vd[e];
+                if (aug) s = s + rho * vd[e];
+                hd[j] = s;
+                vh[e] = s;
+                dacc += s * vd[e];
+            }
+        }
+        curv = cluster_sum(cl, &slots[0], dacc, red);
+    } else {
+        curv = block_reduce_slot(const_cast<double*>(blk), kSlotCurv, ncurv, &sc);
+    }
+    if (!isfinite(curv)) {
+        if (lead) {
+            st->cg_failed = 1;
+            st->cg_mid[it] = 0;
+        }
+        done(0);
+        return;
+    }
+    if (curv <= 0.0) {
+        if (it == 0)
+            for (int64_t j = j0; j < d; j += stride) p[j] = -g[j];
+        if (lead) {
+            st->cg_neg = 1;
+            st->cg_mid[it] = 0;
+        }
+        done(0);
+        return;
+    }
+    const double alpha = r_sq / curv;
+    double rr = 0.0;
+#pragma unroll
+    for (int e = 0; e < kClEpt; ++e) {
+        const int64_t j = j0 + e * stride;
+        if (j < d) {
+            vp[e] += alpha * vd[e];
+            vr[e] = vr[e] - alpha * vh[e];
+            p[j] = vp[e];
+            r[j] = vr[e];
+            rr += vr[e] * vr[e];
+        }
+    }
+    if (lead) {
+        st->cg_iters = it + 1;
+        st->cg_mid[it] = 1;
+    }
+    const double r_sq_next = cluster_sum(cl, &slots[1], rr, red);
+    if (!isfinite(r_sq_next)) {
+        if (lead) st->cg_failed = 1;
+        done(0);
+        return;
+    }
+    if (sqrt(r_sq_next) <= cg_stop) {
+        done(0);
+        return;
+    }
+    const double beta = r_sq_next / r_sq;
+#pragma unroll
+    for (int e = 0; e < kClEpt; ++e) {
+        const int64_t j = j0 + e * stride;
+        if (j < d) dv[j] = vr[e] + beta * vd[e];
+    }
     if (lead) st->r_sq[it + 1] = r_sq_next;
     done(1);
 }
@@ -568,8 +762,25 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
         int chunks = 0;
         const int ncurv = op_hv_split(s, s.dv, s.hd, s.dv, kSlotCurv, &s.st->cg_act[it], &chunks);
         s.hv_timer_site = -1;
-        k_cg_tail<<<grid, 256, 0, st>>>(it, s.d, s.st, s.prm, s.part, chunks, s.g, s.pd, s.r, s.dv, s.hd, s.blk, ncurv,
-                                        chunks > 0 ? s.ctx->dctr : nullptr, s.gbar + 0);
+        if (s.tail_cluster > 0) {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute attr[1];
+            cfg.gridDim = dim3(s.tail_cluster, 1, 1);
+            cfg.blockDim = dim3(kClThreads, 1, 1);
+            cfg.stream = st;
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = s.tail_cluster;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            NADMM_CUDA(cudaLaunchKernelEx(&cfg, k_cg_tail_cl, it, s.d, s.st, (const DevParams*)s.prm,
+                                          (const double*)s.part, chunks, (const double*)s.g, s.pd, s.r, s.dv, s.hd,
+                                          (const double*)s.blk, ncurv, chunks > 0 ? s.ctx->dctr : nullptr));
+        } else {
+            k_cg_tail<<<grid, 256, 0, st>>>(it, s.d, s.st, s.prm, s.part, chunks, s.g, s.pd, s.r, s.dv, s.hd, s.blk,
+                                            ncurv, chunks > 0 ? s.ctx->dctr : nullptr, s.gbar + 0);
+        }
         tl_mark(s, "cg_tail");
         LAUNCH_COUNT(s);
     }
@@ -598,6 +809,35 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
     tl_mark(s, "newton_tail");
     LAUNCH_COUNT(s);
     NADMM_LAUNCH_CHECK();
+}
+
+// Once per shard, outside stream capture: can the CG tail run as one cluster (d small enough for the
+// cluster's registers, 16-CTA clusters co-resident)? 0 selects the grid-barrier kernel.
+void tail_setup(Shard& s) {
+    s.tail_cluster = 0;
+    for (int cs : {16, 8}) {
+        if (s.d > (int64_t)cs * kClThreads * kClEpt) continue;
+        if (cs > 8 && cudaFuncSetAttribute(k_cg_tail_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        cfg.gridDim = dim3(cs, 1, 1);
+        cfg.blockDim = dim3(kClThreads, 1, 1);
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cs;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k_cg_tail_cl, &cfg) == cudaSuccess && n >= 1) {
+            s.tail_cluster = cs;
+            return;
+        }
+        cudaGetLastError();
+    }
 }
 
 void launch_set_int(Shard& s, int32_t* dst, int v) {

@@ -135,6 +135,7 @@ struct Shard {
     int rows_grid = 0;  // blocks of the last rows pass (partials count)
     int last_chunks = 0;    // split-K partial chunks written by the last fused DMMA pass
     int dmma_clusters = 0;  // co-resident clusters of the fused DMMA pass (0: path unavailable)
+    int tail_cluster = 0;   // CTAs of the single-cluster CG tail (0: grid-barrier tail)
     // memo: the point the device cache (L0, P, rowM, rowA, gbase, loss) was built at: the solver
     // iterate s.x, or s.cache_x holding the host vector of the last model-level call
     enum CachePoint { kNone = 0, kAtX = 1, kAtHost = 2 } cache_at = kNone;
