@@ -257,8 +257,15 @@ def main():
     except Exception:
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None  # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
+    try:
+        prof = json.loads((ROOT / "profiles" / "r1_hv_kernel.json").read_text())
+        if n_loc == 6250 and P == 3072:
+            traffic = int(prof["traffic_bytes_per_launch"])
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "dense Hv pass (shard 6250x3072)", "hv_pass_ms": hv_ms,
+                "traffic": traffic, "traffic_source": "profiles/r1_hv_kernel.json (ncu dram__bytes_read+write)", "kernel": "dense Hv pass (shard 6250x3072)", "hv_pass_ms": hv_ms,
                 "bytes_per_hv": hv_bytes(n_loc), "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"}
     sess_res = sess.result()
     sess.close()
