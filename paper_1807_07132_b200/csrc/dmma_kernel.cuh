@@ -159,6 +159,7 @@ struct DmmaArgs {
     double* rowM;
     double* rowA;
     int32_t* pred;
+    double* lp_out;  // Hv mode: also store the X*v logits (the certificate Hv's logits are the Armijo Lp)
     double* part;  // split-K partials, cluster-major: part[cluster * d + c*p + f]
     double* blk;   // block partial slots (loss / hits), one entry per cluster
     const int32_t* guard;
@@ -476,6 +477,9 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
 #endif
 #pragma unroll
                         for (int c = 0; c < K; ++c) urow[c] = vw[c] - pv[c] * rs;
+                        if (a.lp_out && crank == 0)
+#pragma unroll
+                            for (int c = 0; c < K; ++c) a.lp_out[gi * K + c] = lg[c];
                     } else {
 #pragma unroll
                         for (int c = 0; c < K; ++c) urow[c] = 0.0;

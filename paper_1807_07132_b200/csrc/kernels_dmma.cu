@@ -182,6 +182,7 @@ void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
     a.rowM = s.rowM;
     a.rowA = s.rowA;
     a.pred = s.pred;
+    a.lp_out = (mode == kModeHv && s.hv_write_lp) ? s.Lp : nullptr;
     a.part = s.part;
     a.blk = s.blk;
     a.guard = guard;

@@ -31,6 +31,7 @@ struct SmallArgs {
     const int32_t* labels;
     double *L0, *P, *Lp, *rowM, *rowA;
     int32_t* pred;
+    double* lp_out;  // Hv mode: also store the X*v logits (see DmmaArgs::lp_out)
     double* part;
     double* blk;
     const int32_t* guard;
@@ -99,6 +100,10 @@ __global__ void __launch_bounds__(kSpThreads) smallp_kernel(SmallArgs a) {
             }
 #pragma unroll
             for (int c = 0; c < KT; ++c) u[c] = c < K ? e[c] - pv[c] * rs : 0.0;
+            if (a.lp_out)
+#pragma unroll
+                for (int c = 0; c < KT; ++c)
+                    if (c < K) a.lp_out[i * K + c] = lg[c];
         } else {
             double m = lg[0];
 #pragma unroll
@@ -219,6 +224,7 @@ void smallp_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard)
     a.rowM = s.rowM;
     a.rowA = s.rowA;
     a.pred = s.pred;
+    a.lp_out = (mode == kModeHv && s.hv_write_lp) ? s.Lp : nullptr;
     a.part = s.part;
     a.blk = s.blk;
     a.guard = guard;

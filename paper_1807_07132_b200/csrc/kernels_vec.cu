@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(256) k_begin_init(int64_t d, DevState* st, con
         st->ls_evals = 0;
         st->ls_capped = 0;
         st->cert_act = run;
+        st->lp_need = run;
     }
     if (!run) return;
     GRID_STRIDE(j, d) {
@@ -461,7 +462,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cg_tail_cl(int it, int64_t d,
 // (105-109) and the line-search slope p'g. One grid barrier between the slope partials and the
 // decision.
 __global__ void __launch_bounds__(256, 4) k_cert_tail(int64_t d, DevState* st, const DevParams* prm,
-                                                      const double* __restrict__ part, int chunks,
+                                                      const double* __restrict__ part, int chunks, int lp_from_cert,
                                                       const double* __restrict__ g, double* __restrict__ p,
                                                       double* __restrict__ hd, double* blk, int ncert,
                                                       unsigned long long* hv_ctr, unsigned long long* bar) {
@@ -511,6 +512,8 @@ __global__ void __launch_bounds__(256, 4) k_cert_tail(int64_t d, DevState* st, c
             st->slope = slope;
             if (cert) st->cg_residual = sqrt(cv);
             if (failed || flip) st->fallback = 1;
+            // the certificate pass stored Lp = X p (when it ran); only a changed p needs the Lp pass
+            st->lp_need = (!cert || failed || flip || !lp_from_cert) ? 1 : 0;
         }
     }
 }
@@ -786,13 +789,17 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
     }
     s.hv_timer_site = cg_max;
     int chunks = 0;
-    op_hv_split(s, s.pd, s.hd, nullptr, 0, &s.st->cert_act, &chunks);  // certificate Hv (src/newton.cpp:52)
+    // certificate Hv (src/newton.cpp:52); its X p logits are stored as the Armijo Lp on the fused paths
+    const bool lp_from_cert = dmma_supported(s) || smallp_supported(s);
+    s.hv_write_lp = lp_from_cert;
+    op_hv_split(s, s.pd, s.hd, nullptr, 0, &s.st->cert_act, &chunks);
+    s.hv_write_lp = false;
     s.hv_timer_site = -1;
-    k_cert_tail<<<grid, 256, 0, st>>>(s.d, s.st, s.prm, s.part, chunks, s.g, s.pd, s.hd, s.blk, grid,
-                                      chunks > 0 ? s.ctx->dctr : nullptr, s.gbar + 1);
+    k_cert_tail<<<grid, 256, 0, st>>>(s.d, s.st, s.prm, s.part, chunks, lp_from_cert ? 1 : 0, s.g, s.pd, s.hd,
+                                      s.blk, grid, chunks > 0 ? s.ctx->dctr : nullptr, s.gbar + 1);
     tl_mark(s, "cert_tail");
     LAUNCH_COUNT(s);
-    op_lp(s, s.pd, it_act);  // Lp = X p: one data pass serves every Armijo trial
+    op_lp(s, s.pd, &s.st->lp_need);  // Lp = X p, only when p changed after the certificate pass
     tl_mark(s, "lp_pass");
     const int rblocks = std::max(1, (int)std::min<int64_t>((s.n + 31) / 32, kBlockPartials));
     k_ls_partials<<<rblocks + grid, 256, 0, st>>>(s.n, s.K, s.L0, s.Lp, s.labels, rblocks, s.d, s.x, s.pd, s.z, s.y,

@@ -54,6 +54,7 @@ struct DevState {
     int32_t ls_evals;
     int32_t ls_capped;
     int32_t cert_act;   // certificate Hv runs (CG did not fail)
+    int32_t lp_need;    // the Armijo Lp must be recomputed (p changed after, or without, the certificate Hv)
 };
 
 // Trace row written on device (NewtonIterRecord, inc/newton.hpp:47-57).
@@ -136,6 +137,7 @@ struct Shard {
     int last_chunks = 0;    // split-K partial chunks written by the last fused DMMA pass
     int dmma_clusters = 0;  // co-resident clusters of the fused DMMA pass (0: path unavailable)
     int tail_cluster = 0;   // CTAs of the single-cluster CG tail (0: grid-barrier tail)
+    bool hv_write_lp = false;  // capture-time switch: the next fused Hv pass also stores Lp = X v
     // memo: the point the device cache (L0, P, rowM, rowA, gbase, loss) was built at: the solver
     // iterate s.x, or s.cache_x holding the host vector of the last model-level call
     enum CachePoint { kNone = 0, kAtX = 1, kAtHost = 2 } cache_at = kNone;
