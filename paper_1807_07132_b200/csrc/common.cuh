@@ -101,6 +101,31 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
     __syncthreads();
 }
 
+// Programmatic dependent launch: kernels of the Newton-iteration graph are launched with
+// programmatic stream serialisation, so a kernel's launch and prologue overlap its predecessor's
+// tail; every such kernel calls pdl_wait() before touching memory its predecessor writes (a no-op
+// when the launch was not programmatic).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+#ifndef NADMM_PDL
+#define NADMM_PDL 0  // measured: no gain on the Newton graph (kept switchable)
+#endif
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = NADMM_PDL;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    NADMM_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 
 }  // namespace nadmm

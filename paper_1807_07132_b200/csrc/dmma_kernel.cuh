@@ -266,8 +266,6 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
     constexpr int G = BM / 8;      // row groups in phase A
     constexpr int PART = BM * KP;  // doubles per CTA partial
     constexpr int EPI_THREADS = 32 * kDmmaEpiWarps;
-    if (a.guard && !*a.guard) return;  // uniform across the grid: nothing is pending yet
-
     extern __shared__ __align__(128) double smem[];
     const int nc = (int)(blockDim.x >> 5) - kDmmaAux;  // compute warps
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -322,6 +320,10 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
     }
     __syncthreads();
     fence_proxy_async();
+    // everything above overlaps the predecessor kernel (programmatic launch); from here on we read
+    // what it wrote (the guard flag, V, P)
+    pdl_wait();
+    if (a.guard && !*a.guard) return;  // uniform across the grid: no remote traffic has started
     if (csize > 1) cluster_sync_all();  // peers' barriers are initialised before any remote traffic
 
     auto tile_of = [&](int i) -> int64_t { return (int64_t)cid + (int64_t)i * ncl; };

@@ -81,7 +81,7 @@ Layout choose_layout(int64_t p, int K) {
     return best;
 }
 
-cudaLaunchConfig_t make_cfg(Shard& s, const Layout& L, int clusters, cudaLaunchAttribute* attr) {
+cudaLaunchConfig_t make_cfg(Shard& s, const Layout& L, int clusters, cudaLaunchAttribute* attr) {  // attr[2]
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(clusters * L.cs, 1, 1);
     cfg.blockDim = dim3(32 * (L.nw + kDmmaAux), 1, 1);
@@ -91,8 +91,10 @@ cudaLaunchConfig_t make_cfg(Shard& s, const Layout& L, int clusters, cudaLaunchA
     attr[0].val.clusterDim.x = L.cs;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = NADMM_PDL;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cfg;
 }
 
@@ -103,7 +105,7 @@ int setup_mt(Shard& s, const Layout& L) {
     auto kern = dmma_pass_kernel<MT, 1, 1, kBM, kLag, MODE>;
     NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = make_cfg(s, L, 1, attr);
     int nc = 0;
     NADMM_CUDA(cudaOccupancyMaxActiveClusters(&nc, kern, &cfg));
@@ -123,7 +125,7 @@ int setup_modes(Shard& s, const Layout& L) {
 template <int MT, int MODE>
 void launch_mt(Shard& s, const Layout& L, const DmmaArgs& a, int clusters) {
     auto kern = dmma_pass_kernel<MT, 1, 1, kBM, kLag, MODE>;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = make_cfg(s, L, clusters, attr);
     NADMM_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
 }

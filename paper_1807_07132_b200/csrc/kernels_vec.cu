@@ -110,6 +110,7 @@ __global__ void k_value_finish(DevState* st, const DevParams* prm, const double*
 __global__ void __launch_bounds__(256) k_begin_init(int64_t d, DevState* st, const DevParams* prm,
                                                     const double* __restrict__ g, double* __restrict__ p,
                                                     double* __restrict__ r, double* __restrict__ dv) {
+    pdl_wait();
     const double gn = st->g_norm;
     const bool run = st->active && !(gn < prm->grad_tol) && gn > 0.0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_tail(int it, int64_t d, DevState*
                                                     double* __restrict__ r, double* __restrict__ dv,
                                                     double* __restrict__ hd, double* blk, int ncurv,
                                                     unsigned long long* hv_ctr, unsigned long long* bar) {
+    pdl_wait();
     __shared__ double red[32];
     __shared__ double sc;
     const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
@@ -349,6 +351,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cg_tail_cl(int it, int64_t d,
                                                               double* __restrict__ r, double* __restrict__ dv,
                                                               double* __restrict__ hd, const double* blk, int ncurv,
                                                               unsigned long long* hv_ctr) {
+    pdl_wait();
     namespace cgs = cooperative_groups;
     cgs::cluster_group cl = cgs::this_cluster();
     __shared__ double red[32];
@@ -466,6 +469,7 @@ __global__ void __launch_bounds__(256, 4) k_cert_tail(int64_t d, DevState* st, c
                                                       const double* __restrict__ g, double* __restrict__ p,
                                                       double* __restrict__ hd, double* blk, int ncert,
                                                       unsigned long long* hv_ctr, unsigned long long* bar) {
+    pdl_wait();
     __shared__ double red[32];
     __shared__ double sc;
     if (!st->it_act) return;
@@ -538,6 +542,7 @@ __global__ void __launch_bounds__(256) k_ls_partials(int64_t n, int K, const dou
                                                      const double* __restrict__ p, const double* __restrict__ z,
                                                      const double* __restrict__ y, const DevParams* prm, double* blk,
                                                      const int32_t* guard) {
+    pdl_wait();
     if (guard && !*guard) return;
     __shared__ double red[32];
     const int nc = prm->ls_max_iters + 1;
@@ -606,6 +611,7 @@ __global__ void __launch_bounds__(256) k_ls_partials(int64_t n, int K, const dou
 __global__ void __launch_bounds__(256) k_ls_step(int64_t d, DevState* st, const DevParams* prm, const double* blk,
                                                  int nrows, int nvec, double* __restrict__ x,
                                                  const double* __restrict__ p, const int32_t* guard) {
+    pdl_wait();
     if (guard && !*guard) return;
     __shared__ double fj[kMaxLs + 1];
     __shared__ double a_s;
@@ -656,6 +662,7 @@ __global__ void __launch_bounds__(256, 4) k_newton_tail(int64_t d, DevState* st,
                                                         double* __restrict__ g, double* __restrict__ t, double* blk,
                                                         int nloss, double* scal, DevTrace* trace, int trace_cap,
                                                         unsigned long long* bar, const int32_t* guard) {
+    pdl_wait();
     if (guard && !*guard) return;
     __shared__ double red[32];
     const double lam = prm->lambda, rho = prm->rho;
@@ -757,7 +764,7 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
     cudaStream_t st = s.ctx->stream;
     const int grid = vec_grid(*s.ctx, s.d);
     const int32_t* it_act = &s.st->it_act;
-    k_begin_init<<<grid, 256, 0, st>>>(s.d, s.st, s.prm, s.g, s.pd, s.r, s.dv);
+    launch_pdl(k_begin_init, grid, 256, 0, st, s.d, s.st, s.prm, s.g, s.pd, s.r, s.dv);
     tl_mark(s, "begin_init");
     LAUNCH_COUNT(s);
     for (int it = 0; it < cg_max; ++it) {
@@ -767,7 +774,7 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
         s.hv_timer_site = -1;
         if (s.tail_cluster > 0) {
             cudaLaunchConfig_t cfg = {};
-            cudaLaunchAttribute attr[1];
+            cudaLaunchAttribute attr[2];
             cfg.gridDim = dim3(s.tail_cluster, 1, 1);
             cfg.blockDim = dim3(kClThreads, 1, 1);
             cfg.stream = st;
@@ -775,14 +782,16 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
             attr[0].val.clusterDim.x = s.tail_cluster;
             attr[0].val.clusterDim.y = 1;
             attr[0].val.clusterDim.z = 1;
+            attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[1].val.programmaticStreamSerializationAllowed = NADMM_PDL;
             cfg.attrs = attr;
-            cfg.numAttrs = 1;
+            cfg.numAttrs = 2;
             NADMM_CUDA(cudaLaunchKernelEx(&cfg, k_cg_tail_cl, it, s.d, s.st, (const DevParams*)s.prm,
                                           (const double*)s.part, chunks, (const double*)s.g, s.pd, s.r, s.dv, s.hd,
                                           (const double*)s.blk, ncurv, chunks > 0 ? s.ctx->dctr : nullptr));
         } else {
-            k_cg_tail<<<grid, 256, 0, st>>>(it, s.d, s.st, s.prm, s.part, chunks, s.g, s.pd, s.r, s.dv, s.hd, s.blk,
-                                            ncurv, chunks > 0 ? s.ctx->dctr : nullptr, s.gbar + 0);
+            launch_pdl(k_cg_tail, grid, 256, 0, st, it, s.d, s.st, s.prm, s.part, chunks, s.g, s.pd, s.r, s.dv, s.hd,
+                       s.blk, ncurv, chunks > 0 ? s.ctx->dctr : nullptr, s.gbar + 0);
         }
         tl_mark(s, "cg_tail");
         LAUNCH_COUNT(s);
@@ -795,24 +804,24 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
     op_hv_split(s, s.pd, s.hd, nullptr, 0, &s.st->cert_act, &chunks);
     s.hv_write_lp = false;
     s.hv_timer_site = -1;
-    k_cert_tail<<<grid, 256, 0, st>>>(s.d, s.st, s.prm, s.part, chunks, lp_from_cert ? 1 : 0, s.g, s.pd, s.hd,
-                                      s.blk, grid, chunks > 0 ? s.ctx->dctr : nullptr, s.gbar + 1);
+    launch_pdl(k_cert_tail, grid, 256, 0, st, s.d, s.st, s.prm, s.part, chunks, lp_from_cert ? 1 : 0, s.g, s.pd,
+               s.hd, s.blk, grid, chunks > 0 ? s.ctx->dctr : nullptr, s.gbar + 1);
     tl_mark(s, "cert_tail");
     LAUNCH_COUNT(s);
     op_lp(s, s.pd, &s.st->lp_need);  // Lp = X p, only when p changed after the certificate pass
     tl_mark(s, "lp_pass");
     const int rblocks = std::max(1, (int)std::min<int64_t>((s.n + 31) / 32, kBlockPartials));
-    k_ls_partials<<<rblocks + grid, 256, 0, st>>>(s.n, s.K, s.L0, s.Lp, s.labels, rblocks, s.d, s.x, s.pd, s.z, s.y,
-                                                  s.prm, s.blk, it_act);
+    launch_pdl(k_ls_partials, rblocks + grid, 256, 0, st, s.n, s.K, s.L0, s.Lp, s.labels, rblocks, s.d, s.x, s.pd,
+               s.z, s.y, s.prm, s.blk, it_act);
     tl_mark(s, "ls_partials");
-    k_ls_step<<<grid, 256, 0, st>>>(s.d, s.st, s.prm, s.blk, rblocks, grid, s.x, s.pd, it_act);
+    launch_pdl(k_ls_step, grid, 256, 0, st, s.d, s.st, s.prm, s.blk, rblocks, grid, s.x, s.pd, it_act);
     tl_mark(s, "ls_step");
     s.ctx->stats.kernel_launches += 2;
     NADMM_LAUNCH_CHECK();
     chunks = op_cache_split(s, s.x, it_act);
     tl_mark(s, "cache_pass");
-    k_newton_tail<<<grid, 256, 0, st>>>(s.d, s.st, s.prm, s.part, chunks, s.x, s.z, s.y, s.gbase, s.g, s.t, s.blk,
-                                        s.rows_grid, s.scal, s.trace, kTraceCap, s.gbar + 2, it_act);
+    launch_pdl(k_newton_tail, grid, 256, 0, st, s.d, s.st, s.prm, s.part, chunks, s.x, s.z, s.y, s.gbase, s.g, s.t,
+               s.blk, s.rows_grid, s.scal, s.trace, kTraceCap, s.gbar + 2, it_act);
     tl_mark(s, "newton_tail");
     LAUNCH_COUNT(s);
     NADMM_LAUNCH_CHECK();
