@@ -28,7 +28,9 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "dmma_kernel.cuh"
 
@@ -41,44 +43,42 @@ namespace nadmm {
 namespace {
 
 constexpr int kBM = 8;
-#ifndef NADMM_DMMA_LAG
-#define NADMM_DMMA_LAG 4
-#endif
-constexpr int kLag = NADMM_DMMA_LAG;
-constexpr int kStages = kLag + kDmmaExtraStages;
 
 struct Layout {
     bool ok = false;
-    int mt = 0, nw = 0, cs = 0, fs = 0, S = 0;
+    int mt = 0, nw = 0, cs = 0, fs = 0, S = 0, lag = 0;
     size_t smem = 0;
+    double waste = 0.0;
 };
 
-size_t smem_bytes(int nw, int S, int K, int cs) { return dmma_smem_bytes(kStages, kBM, nw, S, K, cs) + 64; }
+constexpr size_t kSmemLimit = 220 * 1024;
 
-Layout choose_layout(int64_t p, int K) {
-    Layout best;
-    if (K != 9) return best;  // instantiated class counts (KT = 1, R = 1)
-    double best_score = 1e30;
-    for (int mt : {6, 7, 4, 8}) {
-        for (int cs : {1, 2, 4, 8}) {
-            const int W = 8 * mt;
-            const int nw = (int)((p + (int64_t)cs * W - 1) / ((int64_t)cs * W));
-            if (nw < 2 || nw > 8) continue;  // compute warps; + kDmmaAux exchange/producer warps
-            const int fs = nw * W;
-            const double waste = (double)cs * fs / (double)p - 1.0;
-            if (waste > 0.15) continue;
-            int S = fs + 4;
-            while (S % 16 != 4) ++S;
-            const size_t smem = smem_bytes(nw, S, K, cs);
-            if (smem > 220 * 1024) continue;
-            const double score = waste * 10.0 + cs * 0.05 + (nw < 4 ? 1.0 : 0.0);
-            if (score < best_score) {
-                best_score = score;
-                best = Layout{true, mt, nw, cs, fs, S, smem};
+size_t smem_bytes(int lag, int nw, int S, int K, int cs) {
+    return dmma_smem_bytes(lag + kDmmaExtraStages, kBM, nw, S, K, cs) + 64;
+}
+
+// Feasible layouts for K = 9 (KT = 1, R = 1): the CTA slice fs = nw * 8 * mt features with 2..8
+// compute warps, a cluster of cs CTAs covering p with <= 15 % padding, and the ring (LAG + 2 stages)
+// within the shared-memory budget. dmma_setup picks among them by co-resident SMs.
+std::vector<Layout> candidate_layouts(int64_t p, int K) {
+    std::vector<Layout> out;
+    if (K != 9) return out;  // instantiated class counts
+    for (int lag : {4, 3})
+        for (int mt : {6, 7, 4, 8})
+            for (int cs = 1; cs <= 8; ++cs) {
+                const int W = 8 * mt;
+                const int nw = (int)((p + (int64_t)cs * W - 1) / ((int64_t)cs * W));
+                if (nw < 2 || nw > 8) continue;  // compute warps; + kDmmaAux exchange/producer warps
+                const int fs = nw * W;
+                const double waste = (double)cs * fs / (double)p - 1.0;
+                if (waste > 0.15) continue;
+                int S = fs + 4;
+                while (S % 16 != 4) ++S;
+                const size_t smem = smem_bytes(lag, nw, S, K, cs);
+                if (smem > kSmemLimit) continue;
+                out.push_back(Layout{true, mt, nw, cs, fs, S, lag, smem, waste});
             }
-        }
-    }
-    return best;
+    return out;
 }
 
 cudaLaunchConfig_t make_cfg(Shard& s, const Layout& L, int clusters, cudaLaunchAttribute* attr) {  // attr[2]
@@ -100,75 +100,134 @@ cudaLaunchConfig_t make_cfg(Shard& s, const Layout& L, int clusters, cudaLaunchA
 
 // Attributes are set once per instantiation, outside any stream capture (dmma_setup), and the
 // co-resident cluster count is queried there too.
-template <int MT, int MODE>
-int setup_mt(Shard& s, const Layout& L) {
-    auto kern = dmma_pass_kernel<MT, 1, 1, kBM, kLag, MODE>;
-    NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+template <int MT, int LAG, int MODE>
+int setup_one(Shard& s, const Layout& L) {
+    auto kern = dmma_pass_kernel<MT, 1, 1, kBM, LAG, MODE>;
+    NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit));
     NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = make_cfg(s, L, 1, attr);
     int nc = 0;
-    NADMM_CUDA(cudaOccupancyMaxActiveClusters(&nc, kern, &cfg));
+    if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
     return nc;
 }
 
-template <int MT>
+template <int MT, int LAG>
 int setup_modes(Shard& s, const Layout& L) {
-    int nc = setup_mt<MT, kModeCache>(s, L);
-    nc = std::min(nc, setup_mt<MT, kModeHv>(s, L));
-    nc = std::min(nc, setup_mt<MT, kModeLp>(s, L));
-    nc = std::min(nc, setup_mt<MT, kModeValue>(s, L));
-    nc = std::min(nc, setup_mt<MT, kModePredict>(s, L));
+    int nc = setup_one<MT, LAG, kModeCache>(s, L);
+    nc = std::min(nc, setup_one<MT, LAG, kModeHv>(s, L));
+    nc = std::min(nc, setup_one<MT, LAG, kModeLp>(s, L));
+    nc = std::min(nc, setup_one<MT, LAG, kModeValue>(s, L));
+    nc = std::min(nc, setup_one<MT, LAG, kModePredict>(s, L));
     return nc;
 }
 
-template <int MT, int MODE>
-void launch_mt(Shard& s, const Layout& L, const DmmaArgs& a, int clusters) {
-    auto kern = dmma_pass_kernel<MT, 1, 1, kBM, kLag, MODE>;
+template <int LAG>
+int setup_lag(Shard& s, const Layout& L) {
+    switch (L.mt) {
+        case 4: return setup_modes<4, LAG>(s, L);
+        case 6: return setup_modes<6, LAG>(s, L);
+        case 7: return setup_modes<7, LAG>(s, L);
+        case 8: return setup_modes<8, LAG>(s, L);
+        default: return 0;
+    }
+}
+
+int setup_layout(Shard& s, const Layout& L) { return L.lag == 4 ? setup_lag<4>(s, L) : setup_lag<3>(s, L); }
+
+template <int MT, int LAG, int MODE>
+void launch_one(Shard& s, const Layout& L, const DmmaArgs& a, int clusters) {
+    auto kern = dmma_pass_kernel<MT, 1, 1, kBM, LAG, MODE>;
     cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = make_cfg(s, L, clusters, attr);
     NADMM_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
 }
 
-template <int MODE>
-void launch_mode(Shard& s, const Layout& L, const DmmaArgs& a, int clusters) {
+template <int LAG, int MODE>
+void launch_lag(Shard& s, const Layout& L, const DmmaArgs& a, int clusters) {
     switch (L.mt) {
-        case 4: launch_mt<4, MODE>(s, L, a, clusters); break;
-        case 6: launch_mt<6, MODE>(s, L, a, clusters); break;
-        case 7: launch_mt<7, MODE>(s, L, a, clusters); break;
-        case 8: launch_mt<8, MODE>(s, L, a, clusters); break;
+        case 4: launch_one<4, LAG, MODE>(s, L, a, clusters); break;
+        case 6: launch_one<6, LAG, MODE>(s, L, a, clusters); break;
+        case 7: launch_one<7, LAG, MODE>(s, L, a, clusters); break;
+        case 8: launch_one<8, LAG, MODE>(s, L, a, clusters); break;
         default: raise(NADMM_ECONFIG, "dmma: unsupported layout");
     }
+}
+
+template <int MODE>
+void launch_mode(Shard& s, const Layout& L, const DmmaArgs& a, int clusters) {
+    if (L.lag == 4)
+        launch_lag<4, MODE>(s, L, a, clusters);
+    else
+        launch_lag<3, MODE>(s, L, a, clusters);
+}
+
+Layout shard_layout(const Shard& s) {
+    Layout L;
+    L.ok = s.dmma_clusters > 0;
+    L.mt = s.dmma_mt;
+    L.nw = s.dmma_nw;
+    L.cs = s.dmma_cs;
+    L.fs = s.dmma_fs;
+    L.S = s.dmma_S;
+    L.lag = s.dmma_lag;
+    L.smem = s.dmma_smem;
+    return L;
 }
 
 }  // namespace
 
 bool dmma_supported(const Shard& s) { return s.dmma_clusters > 0; }
 
+// Picks the layout that keeps the most SMs busy (co-resident clusters x cluster size, capped at the
+// SM count, discounted by feature padding); ties go to more compute warps, the deeper pipeline
+// (LAG 4) and the smaller cluster.
 void dmma_setup(Shard& s) {
     s.dmma_clusters = 0;
     static const bool disabled = getenv("NADMM_DISABLE_DMMA") != nullptr;
     if (disabled || s.sparse || s.ldx % 2 != 0) return;
-    const Layout L = choose_layout(s.p, s.K);
-    if (!L.ok) return;
-    int active = 0;
-    switch (L.mt) {
-        case 4: active = setup_modes<4>(s, L); break;
-        case 6: active = setup_modes<6>(s, L); break;
-        case 7: active = setup_modes<7>(s, L); break;
-        case 8: active = setup_modes<8>(s, L); break;
-        default: return;
+    const char* force_cs = getenv("NADMM_DMMA_CS");  // profiling: restrict the cluster size
+    Layout best;
+    int best_active = 0;
+    double best_score = -1.0;
+    for (const Layout& L : candidate_layouts(s.p, s.K)) {
+        if (force_cs && L.cs != atoi(force_cs)) continue;
+        const int active = setup_layout(s, L);
+        if (active < 1) continue;
+        // SMs kept busy (one CTA per SM by design), then the most compute warps per CTA (more work
+        // per tile and per barrier phase), the deeper pipeline, the smaller cluster
+        const int sms = std::min(active * L.cs, s.ctx->num_sms);
+        const double score = sms * (1.0 - L.waste) * 1000.0 + L.nw * 10.0 + (L.lag == 4 ? 5.0 : 0.0) - L.cs;
+        if (score > best_score) {
+            best_score = score;
+            best = L;
+            best_active = active;
+        }
     }
-    if (active < 1) return;
+    if (!best.ok) return;
+    s.dmma_mt = best.mt;
+    s.dmma_nw = best.nw;
+    s.dmma_cs = best.cs;
+    s.dmma_fs = best.fs;
+    s.dmma_S = best.S;
+    s.dmma_lag = best.lag;
+    s.dmma_smem = best.smem;
     const int64_t ntiles = (s.n + kBM - 1) / kBM;
     s.dmma_clusters = (int)std::max<int64_t>(
-        1, std::min<int64_t>({ntiles, (int64_t)active, (int64_t)s.part_chunks, (int64_t)kBlockPartials}));
+        1, std::min<int64_t>({ntiles, (int64_t)best_active, (int64_t)s.part_chunks, (int64_t)kBlockPartials}));
+    if (getenv("NADMM_DMMA_VERBOSE"))
+        fprintf(stderr, "[nadmm] dmma layout p=%lld: cluster %d x %d clusters (%d SMs), %d warps x %d features, lag %d, smem %zu\n",
+                (long long)s.p, best.cs, s.dmma_clusters, best.cs * s.dmma_clusters, best.nw, 8 * best.mt, best.lag,
+                best.smem);
 }
 
 int dmma_clusters(const Shard& s) { return s.dmma_clusters; }
 
 void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
-    const Layout L = choose_layout(s.p, s.K);
+    const Layout L = shard_layout(s);
     if (!L.ok) raise(NADMM_ECONFIG, "dmma: no layout for this shape");
     DmmaArgs a{};
     a.X = s.X;
