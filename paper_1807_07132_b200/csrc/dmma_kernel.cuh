@@ -163,6 +163,15 @@ struct DmmaArgs {
     double* part;  // split-K partials, cluster-major: part[cluster * d + c*p + f]
     double* blk;   // block partial slots (loss / hits), one entry per cluster
     const int32_t* guard;
+    // CG step fused into an Hv pass (cg_it >= 0): the last cluster to finish sums every cluster's
+    // split-K partial and runs the CG iteration's tail (see dmma_cg_tail)
+    int cg_it;
+    DevState* st;
+    const DevParams* prm;
+    const double* g;
+    double *cg_p, *cg_r, *cg_d, *cg_hd;
+    unsigned long long* hv_ctr;    // Hv products applied (device counter)
+    unsigned long long* done_ctr;  // clusters finished with this launch (reset by the last one)
     int fs;  // features per CTA (= NC * 8 * MT)
     int S;   // padded shared row stride (doubles, even)
 };
@@ -248,6 +257,100 @@ __host__ __device__ inline size_t dmma_smem_bytes(int stages, int bm, int nc, in
     return sizeof(double) * dbl + 4 * ((size_t)stages * bm + 4) + 8 * (nbars + 1);
 }
 
+// The CG iteration's tail (src/newton.cpp:31-50, as k_cg_tail) run by the whole persistent grid of
+// the Hv pass after its last tile: every CTA owns a slice of d, sums the per-cluster partials there
+// (cluster order) + lambda d (+ rho d), and the curvature / <r,r> reductions go through block slots
+// and software grid barriers (the grid is co-resident by construction). All blocks evaluate the same
+// scalars; block 0 / thread 0 writes the solver state.
+__device__ void dmma_cg_tail(const DmmaArgs& a, int K, int chunks, double* scratch, double* sc) {
+    const int it = a.cg_it;
+    DevState* st = a.st;
+    const int64_t d = (int64_t)K * a.p;
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    const double lam = a.prm->lambda, rho = a.prm->rho;
+    const bool aug = a.prm->augmented;
+    double* curv_slot = a.blk + (int64_t)kSlotCurv * kBlockPartials;
+    double* rr_slot = a.blk + (int64_t)kSlotRr * kBlockPartials;
+    if (lead && a.hv_ctr) atomicAdd(a.hv_ctr, 1ULL);
+    double dacc = 0.0;
+    for (int64_t j = tid; j < d; j += nth) {
+        double s = 0.0;
+        for (int ch = 0; ch < chunks; ch += 8) {
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = (ch + q < chunks) ? __ldcg(a.part + (int64_t)(ch + q) * d + j) : 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (ch + q < chunks) s += v[q];
+        }
+        const double vj = a.cg_d[j];
+        if (lam > 0.0) s = s + lam * vj;
+        if (aug) s = s + rho * vj;
+        a.cg_hd[j] = s;
+        dacc += s * vj;
+    }
+    double t = block_sum(dacc, scratch);
+    if (threadIdx.x == 0) curv_slot[blockIdx.x] = t;
+    grid_barrier(a.done_ctr);
+    if (threadIdx.x < 32) {
+        const double v = reduce_partials(curv_slot, gridDim.x);
+        if (threadIdx.x == 0) *sc = v;
+    }
+    __syncthreads();
+    const double curv = *sc;
+    int act_next = 0;
+    if (!isfinite(curv)) {
+        if (lead) {
+            st->cg_failed = 1;
+            st->cg_mid[it] = 0;
+        }
+    } else if (curv <= 0.0) {
+        if (it == 0)
+            for (int64_t j = tid; j < d; j += nth) a.cg_p[j] = -a.g[j];
+        if (lead) {
+            st->cg_neg = 1;
+            st->cg_mid[it] = 0;
+        }
+    } else {
+        const double r_sq = st->r_sq[it];
+        const double alpha = r_sq / curv;
+        double rr = 0.0;
+        for (int64_t j = tid; j < d; j += nth) {
+            a.cg_p[j] += alpha * a.cg_d[j];
+            const double rj = a.cg_r[j] - alpha * a.cg_hd[j];
+            a.cg_r[j] = rj;
+            rr += rj * rj;
+        }
+        t = block_sum(rr, scratch);
+        if (threadIdx.x == 0) rr_slot[blockIdx.x] = t;
+        if (lead) {
+            st->cg_iters = it + 1;
+            st->cg_mid[it] = 1;
+        }
+        grid_barrier(a.done_ctr);
+        __syncthreads();  // *sc reused
+        if (threadIdx.x < 32) {
+            const double v = reduce_partials(rr_slot, gridDim.x);
+            if (threadIdx.x == 0) *sc = v;
+        }
+        __syncthreads();
+        const double r_sq_next = *sc;
+        if (!isfinite(r_sq_next)) {
+            if (lead) st->cg_failed = 1;
+        } else if (!(sqrt(r_sq_next) <= st->cg_stop)) {
+            const double beta = r_sq_next / r_sq;
+            for (int64_t j = tid; j < d; j += nth) a.cg_d[j] = a.cg_r[j] + beta * a.cg_d[j];
+            if (lead) st->r_sq[it + 1] = r_sq_next;
+            act_next = 1;
+        }
+    }
+    if (lead) {
+        st->cg_act[it + 1] = act_next;
+        st->cert_act = st->it_act && !st->cg_failed;
+    }
+}
+
 // LAG: tiles of phase A in flight ahead of phase B; STAGES = LAG + 2 (A ring + one loading).
 template <int MT, int KT, int R, int BM, int LAG, int MODE>
 __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
@@ -323,7 +426,15 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
     // everything above overlaps the predecessor kernel (programmatic launch); from here on we read
     // what it wrote (the guard flag, V, P)
     pdl_wait();
-    if (a.guard && !*a.guard) return;  // uniform across the grid: no remote traffic has started
+    if (a.guard && !*a.guard) {  // uniform across the grid: no remote traffic has started
+        if (MODE == kModeHv && a.cg_it >= 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+            DevState* st = a.st;  // the CG iteration is switched off: its tail's bookkeeping
+            st->cg_mid[a.cg_it] = 0;
+            st->cg_act[a.cg_it + 1] = 0;
+            st->cert_act = st->it_act && !st->cg_failed;
+        }
+        return;
+    }
     if (csize > 1) cluster_sync_all();  // peers' barriers are initialised before any remote traffic
 
     auto tile_of = [&](int i) -> int64_t { return (int64_t)cid + (int64_t)i * ncl; };
@@ -739,6 +850,11 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
     }
     __syncthreads();
     if (csize > 1) cluster_sync_all();  // no CTA leaves while peers may still target its shared memory
+    if (MODE == kModeHv && a.cg_it >= 0) {
+        // all clusters' partials written -> the whole (co-resident) grid runs the CG tail
+        grid_barrier(a.done_ctr);
+        dmma_cg_tail(a, K, (int)ncl, misc, misc + 127);
+    }
 }
 
 }  // namespace nadmm

@@ -247,6 +247,18 @@ void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
     a.part = s.part;
     a.blk = s.blk;
     a.guard = guard;
+    a.cg_it = (mode == kModeHv) ? s.cg_fuse_it : -1;
+    if (a.cg_it >= 0) {
+        a.st = s.st;
+        a.prm = s.prm;
+        a.g = s.g;
+        a.cg_p = s.pd;
+        a.cg_r = s.r;
+        a.cg_d = s.dv;
+        a.cg_hd = s.hd;
+        a.hv_ctr = s.ctx->dctr;
+        a.done_ctr = s.gbar + 4;
+    }
     a.fs = L.fs;
     a.S = L.S;
     const int clusters = dmma_clusters(s);

@@ -767,12 +767,19 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
     launch_pdl(k_begin_init, grid, 256, 0, st, s.d, s.st, s.prm, s.g, s.pd, s.r, s.dv);
     tl_mark(s, "begin_init");
     LAUNCH_COUNT(s);
+    // DMMA shards: the CG tail runs inside the Hv pass (its last cluster to finish); otherwise one
+    // tail launch per iteration
+    const bool fused_tail = dmma_supported(s);
     for (int it = 0; it < cg_max; ++it) {
         s.hv_timer_site = it;
         int chunks = 0;
+        s.cg_fuse_it = fused_tail ? it : -1;
         const int ncurv = op_hv_split(s, s.dv, s.hd, s.dv, kSlotCurv, &s.st->cg_act[it], &chunks);
+        s.cg_fuse_it = -1;
         s.hv_timer_site = -1;
-        if (s.tail_cluster > 0) {
+        if (fused_tail) {
+            // nothing more to launch
+        } else if (s.tail_cluster > 0) {
             cudaLaunchConfig_t cfg = {};
             cudaLaunchAttribute attr[2];
             cfg.gridDim = dim3(s.tail_cluster, 1, 1);
