@@ -562,8 +562,9 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
             if (lane == 0 && !kExpNoXchg)
                 for (uint32_t q = 0; q < csize; ++q) mbar_arrive_remote(&credit[br], q);
             if (ew == 0) DMMA_TRACE(i, 11);
-            // (2) row epilogue, one lane per row
-            if (lane < BM) {
+            // (2) row epilogue. Hv / Lp: one lane per row.
+            if (MODE == kModeHv || MODE == kModeLp) {
+              if (lane < BM) {
                 const int row = lane;
                 const int64_t gi = r0 + row;
                 const bool valid = gi < n;
@@ -601,59 +602,78 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                     if (valid && crank == 0)
 #pragma unroll
                         for (int c = 0; c < K; ++c) a.Lp[gi * K + c] = lg[c];
-                } else if (valid) {
-                    double m = lg[0];
+                }
+              }
+            } else {
+                // stable softmax cache / loss / argmax (src/softmax.cpp:51-95, 118-139): four lanes
+                // per row, lane q owning classes q, q+4, ...; row max / sums by quad butterflies
+                const int row = lane >> 2, q = lane & 3;
+                const int64_t gi = r0 + row;
+                const bool valid = gi < n;
+                const double* lg = lgw + row * KP;
+                double* urow = ut + (size_t)stage * BM * KS + row * KS;
+                constexpr int CPL = (K + 3) / 4;
+                double lv[CPL], e[CPL];
+                double m = -INFINITY;
 #pragma unroll
-                    for (int c = 1; c < K; ++c) m = lg[c] > m ? lg[c] : m;
-                    m = m > 0.0 ? m : 0.0;
-                    constexpr int KT2 = K <= 2 ? 2 : K <= 4 ? 4 : K <= 8 ? 8 : K <= 16 ? 16 : 32;
-                    double e[KT2], et2[KT2];
+                for (int t = 0; t < CPL; ++t) {
+                    const int c = q + 4 * t;
+                    lv[t] = c < K ? lg[c] : -INFINITY;
+                    m = lv[t] > m ? lv[t] : m;
+                }
+                m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
+                m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+                m = m > 0.0 ? m : 0.0;
+                double es = 0.0;
 #pragma unroll
-                    for (int c = 0; c < KT2; ++c) {
-                        e[c] = c < K ? exp(lg[c] - m) : 0.0;
-                        et2[c] = e[c];
-                    }
-                    const double alpha = exp(-m) + tree_sum(et2, K);
-                    const int yb = ys[stage * BM + row];
-                    double lb = 0.0;
+                for (int t = 0; t < CPL; ++t) {
+                    e[t] = (q + 4 * t < K) ? exp(lv[t] - m) : 0.0;
+                    es += e[t];
+                }
+                es += __shfl_xor_sync(0xffffffffu, es, 1);
+                es += __shfl_xor_sync(0xffffffffu, es, 2);
+                const double alpha = exp(-m) + es;
+                const int yb = ys[stage * BM + row];
+                if (MODE == kModeCache || MODE == kModeValue) {
+                    if (q == 0 && valid && crank == 0)
+                        loss_acc += (m + log(alpha)) - (yb <= K ? lg[yb - 1] : 0.0);
+                    if (MODE == kModeCache) {
 #pragma unroll
-                    for (int c = 0; c < K; ++c)
-                        if (c == yb - 1) lb = lg[c];
-                    if (MODE == kModeCache || MODE == kModeValue) {
-                        if (crank == 0) loss_acc += (m + log(alpha)) - (yb <= K ? lb : 0.0);
-                        if (MODE == kModeCache) {
-#pragma unroll
-                            for (int c = 0; c < K; ++c) {
-                                const double pc = e[c] / alpha;
-                                urow[c] = (c == yb - 1) ? pc - 1.0 : pc;
-                                if (crank == 0) {
+                        for (int t = 0; t < CPL; ++t) {
+                            const int c = q + 4 * t;
+                            if (c < K) {
+                                const double pc = e[t] / alpha;
+                                urow[c] = valid ? ((c == yb - 1) ? pc - 1.0 : pc) : 0.0;
+                                if (valid && crank == 0) {
                                     a.L0[gi * K + c] = lg[c];
                                     a.P[gi * K + c] = pc;
                                 }
                             }
-                            if (crank == 0) {
-                                a.rowM[gi] = m;
-                                a.rowA[gi] = alpha;
-                            }
                         }
-                    } else if (MODE == kModePredict && crank == 0) {
-                        const double residual = exp(-m) / alpha;
-                        double best = e[0] / alpha;
+                        if (q == 0 && valid && crank == 0) {
+                            a.rowM[gi] = m;
+                            a.rowA[gi] = alpha;
+                        }
+                    }
+                } else if (MODE == kModePredict) {
+                    double best = -INFINITY;
 #pragma unroll
-                        for (int c = 1; c < K; ++c) best = (e[c] / alpha > best) ? e[c] / alpha : best;
-                        int arg = 0;
-                        for (int c = 0; c < K; ++c)
-                            if (e[c] / alpha == best) {
-                                arg = c + 1;
-                                break;
-                            }
-                        if (residual > best) arg = K + 1;
+                    for (int t = 0; t < CPL; ++t)
+                        if (q + 4 * t < K) best = fmax(best, e[t] / alpha);
+                    best = fmax(best, __shfl_xor_sync(0xffffffffu, best, 1));
+                    best = fmax(best, __shfl_xor_sync(0xffffffffu, best, 2));
+                    int arg = 1 << 20;  // first class attaining the max (src/softmax.cpp:127-135)
+#pragma unroll
+                    for (int t = CPL - 1; t >= 0; --t)
+                        if (q + 4 * t < K && e[t] / alpha == best) arg = q + 4 * t;
+                    arg = min(arg, __shfl_xor_sync(0xffffffffu, arg, 1));
+                    arg = min(arg, __shfl_xor_sync(0xffffffffu, arg, 2));
+                    arg += 1;
+                    if (exp(-m) / alpha > best) arg = K + 1;  // class C only if strictly greater
+                    if (q == 0 && valid && crank == 0) {
                         a.pred[gi] = arg;
                         loss_acc += (arg == yb) ? 1.0 : 0.0;
                     }
-                } else if (MODE == kModeCache) {
-#pragma unroll
-                    for (int c = 0; c < K; ++c) urow[c] = 0.0;
                 }
             }
             __syncwarp();  // U rows complete, lgw reusable
@@ -666,11 +686,11 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
         }
         // cluster's loss / hit partial (rank-0 CTA): rows of warp 0's tiles, then warp 1's, ...
         if (MODE == kModeCache || MODE == kModeValue || MODE == kModePredict) {
-            if (lane < BM) misc[ew * BM + lane] = loss_acc;
+            misc[ew * 32 + lane] = loss_acc;
             named_sync(1, 32 * kDmmaEpiWarps);
             if (ew == 0 && lane == 0 && crank == 0) {
                 double s = 0.0;
-                for (int q = 0; q < BM * kDmmaEpiWarps; ++q) s += misc[q];
+                for (int q = 0; q < 32 * kDmmaEpiWarps; ++q) s += misc[q];
                 const int slotid = MODE == kModePredict ? kSlotHits : kSlotLoss;
                 a.blk[(int64_t)slotid * kBlockPartials + cid] = s;
             }
