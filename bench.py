@@ -31,6 +31,8 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# rank 0 prints exactly one JSON line on stdout: keep NCCL's banner ("NCCL version ...") off it
+os.environ["NCCL_DEBUG"] = os.environ.get("NADMM_NCCL_DEBUG", "WARN")
 
 N_TOTAL, P, C, LAM = 55_556, 3072, 10, 1e-3  # floor(9n/10) = 50,000 train rows
 NODES = 8
