@@ -17,6 +17,7 @@
 
 #include <cuda.h>
 
+#include "solver_tails.cuh"
 #include "state.h"
 
 namespace nadmm {
@@ -163,12 +164,19 @@ struct DmmaArgs {
     double* part;  // split-K partials, cluster-major: part[cluster * d + c*p + f]
     double* blk;   // block partial slots (loss / hits), one entry per cluster
     const int32_t* guard;
-    // CG step fused into an Hv pass (cg_it >= 0): the last cluster to finish sums every cluster's
-    // split-K partial and runs the CG iteration's tail (see dmma_cg_tail)
+    // solver tail run by the whole grid after the last tile (DmmaTail): CG step (Hv pass inside the
+    // CG loop), certificate / fallback / slope (certificate Hv pass), gradient + value + trace (cache
+    // pass at the new iterate)
+    int tail;
     int cg_it;
+    int lp_from_cert;
+    const double *x, *z, *y;
+    double *gbase, *t, *scal;
+    DevTrace* trace;
+    int trace_cap;
     DevState* st;
     const DevParams* prm;
-    const double* g;
+    double* g;  // gradient (read by the CG / certificate tails, written by the Newton tail)
     double *cg_p, *cg_r, *cg_d, *cg_hd;
     unsigned long long* hv_ctr;    // Hv products applied (device counter)
     unsigned long long* done_ctr;  // clusters finished with this launch (reset by the last one)
@@ -399,7 +407,7 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
     uint64_t* u_full = credit + kDmmaRecvBufs;     // STAGES: U tile ready (epilogue warps)
 
     const int64_t ntiles = (n + BM - 1) / BM;
-    const int T = cid < ntiles ? (int)((ntiles - 1 - cid) / ncl + 1) : 0;  // this cluster's tiles
+    int T = cid < ntiles ? (int)((ntiles - 1 - cid) / ncl + 1) : 0;  // this cluster's tiles
     const int64_t rem_f = p - f_cta;
     const int valid_f = rem_f <= 0 ? 0 : (rem_f < fs ? (int)rem_f : fs);  // valid features in slice
     const uint32_t row_bytes = (uint32_t)valid_f * 8u;
@@ -427,7 +435,7 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
     // what it wrote (the guard flag, V, P)
     pdl_wait();
     if (a.guard && !*a.guard) {  // uniform across the grid: no remote traffic has started
-        if (MODE == kModeHv && a.cg_it >= 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+        if (MODE == kModeHv && a.tail == kTailCg && blockIdx.x == 0 && threadIdx.x == 0) {
             DevState* st = a.st;  // the CG iteration is switched off: its tail's bookkeeping
             st->cg_mid[a.cg_it] = 0;
             st->cg_act[a.cg_it + 1] = 0;
@@ -435,6 +443,9 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
         }
         return;
     }
+    // certificate pass: the grid always runs the tail (fallback / slope); the product itself only when
+    // CG did not fail (src/newton.cpp:52)
+    if (MODE == kModeHv && a.tail == kTailCert && !a.st->cert_act) T = 0;
     if (csize > 1) cluster_sync_all();  // peers' barriers are initialised before any remote traffic
 
     auto tile_of = [&](int i) -> int64_t { return (int64_t)cid + (int64_t)i * ncl; };
@@ -870,10 +881,18 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
     }
     __syncthreads();
     if (csize > 1) cluster_sync_all();  // no CTA leaves while peers may still target its shared memory
-    if (MODE == kModeHv && a.cg_it >= 0) {
-        // all clusters' partials written -> the whole (co-resident) grid runs the CG tail
+    if (PHASE_B && a.tail != kTailNone) {
+        // all clusters' partials (and loss slots) written -> the whole (co-resident) grid runs the tail
         grid_barrier(a.done_ctr);
-        dmma_cg_tail(a, K, (int)ncl, misc, misc + 127);
+        const int64_t d = (int64_t)K * p;
+        if (MODE == kModeHv && a.tail == kTailCg)
+            dmma_cg_tail(a, K, (int)ncl, misc, misc + 127);
+        else if (MODE == kModeHv && a.tail == kTailCert)
+            cert_tail_body(d, a.st, a.prm, a.part, (int)ncl, a.lp_from_cert, a.g, a.cg_p, a.cg_hd, a.blk, (int)ncl,
+                           a.hv_ctr, a.done_ctr, misc, misc + 127);
+        else if (MODE == kModeCache && a.tail == kTailNewton)
+            newton_tail_body(d, a.st, a.prm, a.part, (int)ncl, a.x, a.z, a.y, a.gbase, a.g, a.t, a.blk, (int)ncl,
+                             a.scal, a.trace, a.trace_cap, a.done_ctr, misc);
     }
 }
 

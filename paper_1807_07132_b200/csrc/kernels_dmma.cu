@@ -247,8 +247,9 @@ void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
     a.part = s.part;
     a.blk = s.blk;
     a.guard = guard;
-    a.cg_it = (mode == kModeHv) ? s.cg_fuse_it : -1;
-    if (a.cg_it >= 0) {
+    a.tail = (mode == kModeHv || mode == kModeCache) ? s.dmma_tail : kTailNone;
+    a.cg_it = s.cg_fuse_it;
+    if (a.tail != kTailNone) {
         a.st = s.st;
         a.prm = s.prm;
         a.g = s.g;
@@ -258,6 +259,15 @@ void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
         a.cg_hd = s.hd;
         a.hv_ctr = s.ctx->dctr;
         a.done_ctr = s.gbar + 4;
+        a.lp_from_cert = 1;
+        a.x = s.x;
+        a.z = s.z;
+        a.y = s.y;
+        a.gbase = s.gbase;
+        a.t = s.t;
+        a.scal = s.scal;
+        a.trace = s.trace;
+        a.trace_cap = kTraceCap;
     }
     a.fs = L.fs;
     a.S = L.S;

@@ -12,23 +12,9 @@
 #include <cooperative_groups.h>
 
 #include "solver_kernels.h"
+#include "solver_tails.cuh"
 
 namespace nadmm {
-
-#define GRID_STRIDE(j, d) \
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < (d); j += (int64_t)gridDim.x * blockDim.x)
-
-__device__ __forceinline__ double* slot_ptr(double* blk, int slot) { return blk + (int64_t)slot * kBlockPartials; }
-
-// Reduce a slot with warp 0 and broadcast to the whole block.
-__device__ __forceinline__ double block_reduce_slot(double* blk, int slot, int n, double* sh) {
-    if (threadIdx.x < 32) {
-        const double v = reduce_partials(slot_ptr(blk, slot), n);
-        if (threadIdx.x == 0) *sh = v;
-    }
-    __syncthreads();
-    return *sh;
-}
 
 // t = z - x + y/rho and g = gbase - rho t (src/objective.cpp:47-51); partials of <g,g>, <t,t>.
 __global__ void k_grad_aug(int64_t d, const double* __restrict__ x, const double* __restrict__ z,
@@ -145,21 +131,6 @@ __global__ void __launch_bounds__(256) k_begin_init(int64_t d, DevState* st, con
         r[j] = -g[j];
         dv[j] = -g[j];
     }
-}
-
-// Sum of the fused dense pass's split-K partials at element j, in chunk order: loads are issued in
-// predicated batches of 8 so they are in flight together; the additions keep the sequential order.
-__device__ __forceinline__ double sum_chunks(const double* __restrict__ part, int chunks, int64_t d, int64_t j) {
-    double s = 0.0;
-    for (int ch = 0; ch < chunks; ch += 8) {
-        double v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = (ch + q < chunks) ? part[(int64_t)(ch + q) * d + j] : 0.0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-            if (ch + q < chunks) s += v[q];
-    }
-    return s;
 }
 
 // One fused CG tail per iteration (persistent grid, two software grid barriers), replacing the
@@ -472,54 +443,7 @@ __global__ void __launch_bounds__(256, 4) k_cert_tail(int64_t d, DevState* st, c
     pdl_wait();
     __shared__ double red[32];
     __shared__ double sc;
-    if (!st->it_act) return;
-    const bool cert = st->cert_act, failed = st->cg_failed;
-    const double lam = prm->lambda, rho = prm->rho;
-    const bool aug = prm->augmented;
-    if (cert && chunks > 0 && hv_ctr && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(hv_ctr, 1ULL);
-    double cacc = 0.0, sacc = 0.0;
-    GRID_STRIDE(j, d) {
-        const double gj = g[j];
-        double pj = p[j];
-        if (cert) {
-            double hp;
-            if (chunks > 0) {
-                hp = sum_chunks(part, chunks, d, j);
-                if (lam > 0.0) hp = hp + lam * pj;
-                if (aug) hp = hp + rho * pj;
-                hd[j] = hp;
-            } else {
-                hp = hd[j];
-            }
-            const double v = hp + gj;
-            cacc += v * v;
-        }
-        if (failed) {
-            pj = -gj;
-            p[j] = pj;
-        }
-        sacc += pj * gj;
-    }
-    double t = block_sum(cacc, red);
-    if (threadIdx.x == 0 && cert) slot_ptr(blk, kSlotCert)[blockIdx.x] = t;
-    t = block_sum(sacc, red);
-    if (threadIdx.x == 0) slot_ptr(blk, kSlotSlope)[blockIdx.x] = t;
-    ncert = gridDim.x;
-    grid_barrier(bar);
-    double slope = block_reduce_slot(blk, kSlotSlope, gridDim.x, &sc);
-    const bool flip = slope >= 0.0;
-    if (flip) GRID_STRIDE(j, d) p[j] = -g[j];
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
-        const double cv = cert ? reduce_partials(slot_ptr(blk, kSlotCert), ncert) : 0.0;
-        if (threadIdx.x == 0) {
-            if (flip) slope = -st->g_sq;  // (-g).g == -|g|^2 under the same reduction order
-            st->slope = slope;
-            if (cert) st->cg_residual = sqrt(cv);
-            if (failed || flip) st->fallback = 1;
-            // the certificate pass stored Lp = X p (when it ran); only a changed p needs the Lp pass
-            st->lp_need = (!cert || failed || flip || !lp_from_cert) ? 1 : 0;
-        }
-    }
+    cert_tail_body(d, st, prm, part, chunks, lp_from_cert, g, p, hd, blk, ncert, hv_ctr, bar, red, &sc);
 }
 
 // Batched Armijo candidates (src/newton.cpp:56-71), partial sums for every trial a_j = gamma^j:
@@ -665,71 +589,7 @@ __global__ void __launch_bounds__(256, 4) k_newton_tail(int64_t d, DevState* st,
     pdl_wait();
     if (guard && !*guard) return;
     __shared__ double red[32];
-    const double lam = prm->lambda, rho = prm->rho;
-    const bool aug = prm->augmented;
-    double xx = 0.0, gg = 0.0, tt = 0.0;
-    GRID_STRIDE(j, d) {
-        const double xj = x[j];
-        double gb;
-        if (chunks > 0) {
-            gb = sum_chunks(part, chunks, d, j);
-            if (lam > 0.0) gb = gb + lam * xj;  // src/softmax.cpp:93
-            gbase[j] = gb;
-        } else {
-            gb = gbase[j];
-        }
-        xx += xj * xj;
-        double gj = gb;
-        if (aug) {
-            const double tj = (z[j] - xj) + y[j] / rho;
-            t[j] = tj;
-            tt += tj * tj;
-            gj = gj - rho * tj;
-        }
-        g[j] = gj;
-        gg += gj * gj;
-    }
-    double sres = block_sum(xx, red);
-    if (threadIdx.x == 0) slot_ptr(blk, kSlotRidge)[blockIdx.x] = sres;
-    sres = block_sum(gg, red);
-    if (threadIdx.x == 0) slot_ptr(blk, kSlotGg)[blockIdx.x] = sres;
-    sres = block_sum(tt, red);
-    if (threadIdx.x == 0) slot_ptr(blk, kSlotTt)[blockIdx.x] = sres;
-    grid_barrier(bar);
-    if (blockIdx.x != 0 || threadIdx.x >= 32) return;
-    const int nvec = gridDim.x;
-    double base = reduce_partials(slot_ptr(blk, kSlotLoss), nloss);
-    if (lam > 0.0) base += 0.5 * lam * reduce_partials(slot_ptr(blk, kSlotRidge), nvec);  // src/softmax.cpp:76
-    const double g_sq = reduce_partials(slot_ptr(blk, kSlotGg), nvec);
-    const double t_sq = reduce_partials(slot_ptr(blk, kSlotTt), nvec);
-    if (threadIdx.x != 0) return;
-    scal[0] = base;
-    double f = base;
-    if (aug) f = f + 0.5 * rho * t_sq;
-    st->f_base = base;
-    st->f_x = f;
-    st->g_sq = g_sq;
-    st->g_norm = sqrt(g_sq);
-    const int k = st->iter;
-    if (k < trace_cap) {
-        DevTrace rr;
-        rr.iter = k;
-        rr.grad_norm = st->rec_gnorm;
-        rr.step = st->ls_alpha;
-        rr.cg_iters = st->cg_failed ? 0 : st->cg_iters;
-        rr.cg_residual = st->cg_failed ? 0.0 : st->cg_residual;
-        rr.objective = f;
-        rr.ls_capped = st->ls_capped;
-        rr.cg_fallback = st->fallback;
-        rr.fn_evals = st->ls_evals;
-        rr.pad = 0;
-        trace[k] = rr;
-    }
-    st->iter = k + 1;
-    if (!isfinite(f)) {  // "non-finite objective at iteration k"
-        st->error = NADMM_ESOLVER;
-        st->active = 0;
-    }
+    newton_tail_body(d, st, prm, part, chunks, x, z, y, gbase, g, t, blk, nloss, scal, trace, trace_cap, bar, red);
 }
 
 __global__ void k_set_int(int32_t* dst, int v) {
@@ -773,8 +633,10 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
     for (int it = 0; it < cg_max; ++it) {
         s.hv_timer_site = it;
         int chunks = 0;
-        s.cg_fuse_it = fused_tail ? it : -1;
+        s.cg_fuse_it = it;
+        s.dmma_tail = fused_tail ? kTailCg : kTailNone;
         const int ncurv = op_hv_split(s, s.dv, s.hd, s.dv, kSlotCurv, &s.st->cg_act[it], &chunks);
+        s.dmma_tail = kTailNone;
         s.cg_fuse_it = -1;
         s.hv_timer_site = -1;
         if (fused_tail) {
@@ -808,13 +670,21 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
     // certificate Hv (src/newton.cpp:52); its X p logits are stored as the Armijo Lp on the fused paths
     const bool lp_from_cert = dmma_supported(s) || smallp_supported(s);
     s.hv_write_lp = lp_from_cert;
-    op_hv_split(s, s.pd, s.hd, nullptr, 0, &s.st->cert_act, &chunks);
-    s.hv_write_lp = false;
-    s.hv_timer_site = -1;
-    launch_pdl(k_cert_tail, grid, 256, 0, st, s.d, s.st, s.prm, s.part, chunks, lp_from_cert ? 1 : 0, s.g, s.pd,
-               s.hd, s.blk, grid, chunks > 0 ? s.ctx->dctr : nullptr, s.gbar + 1);
+    if (fused_tail) {  // the certificate pass runs whenever the iteration does; its tail decides the rest
+        s.dmma_tail = kTailCert;
+        op_hv_split(s, s.pd, s.hd, nullptr, 0, it_act, &chunks);
+        s.dmma_tail = kTailNone;
+        s.hv_write_lp = false;
+        s.hv_timer_site = -1;
+    } else {
+        op_hv_split(s, s.pd, s.hd, nullptr, 0, &s.st->cert_act, &chunks);
+        s.hv_write_lp = false;
+        s.hv_timer_site = -1;
+        launch_pdl(k_cert_tail, grid, 256, 0, st, s.d, s.st, s.prm, s.part, chunks, lp_from_cert ? 1 : 0, s.g, s.pd,
+                   s.hd, s.blk, grid, chunks > 0 ? s.ctx->dctr : nullptr, s.gbar + 1);
+        LAUNCH_COUNT(s);
+    }
     tl_mark(s, "cert_tail");
-    LAUNCH_COUNT(s);
     op_lp(s, s.pd, &s.st->lp_need);  // Lp = X p, only when p changed after the certificate pass
     tl_mark(s, "lp_pass");
     const int rblocks = std::max(1, (int)std::min<int64_t>((s.n + 31) / 32, kBlockPartials));
@@ -825,12 +695,19 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
     tl_mark(s, "ls_step");
     s.ctx->stats.kernel_launches += 2;
     NADMM_LAUNCH_CHECK();
-    chunks = op_cache_split(s, s.x, it_act);
-    tl_mark(s, "cache_pass");
-    launch_pdl(k_newton_tail, grid, 256, 0, st, s.d, s.st, s.prm, s.part, chunks, s.x, s.z, s.y, s.gbase, s.g, s.t,
-               s.blk, s.rows_grid, s.scal, s.trace, kTraceCap, s.gbar + 2, it_act);
-    tl_mark(s, "newton_tail");
-    LAUNCH_COUNT(s);
+    if (fused_tail) {
+        s.dmma_tail = kTailNewton;
+        op_cache_split(s, s.x, it_act);
+        s.dmma_tail = kTailNone;
+        tl_mark(s, "cache_pass+newton_tail");
+    } else {
+        chunks = op_cache_split(s, s.x, it_act);
+        tl_mark(s, "cache_pass");
+        launch_pdl(k_newton_tail, grid, 256, 0, st, s.d, s.st, s.prm, s.part, chunks, s.x, s.z, s.y, s.gbase, s.g,
+                   s.t, s.blk, s.rows_grid, s.scal, s.trace, kTraceCap, s.gbar + 2, it_act);
+        tl_mark(s, "newton_tail");
+        LAUNCH_COUNT(s);
+    }
     NADMM_LAUNCH_CHECK();
 }
 

@@ -89,6 +89,9 @@ enum PassMode : int {
     kModePredict = 4,  // argmax with the reference tie rule; hit-count partials
 };
 
+// Solver tails a DMMA pass can run with its whole grid after its last tile.
+enum DmmaTail : int { kTailNone = 0, kTailCg = 1, kTailCert = 2, kTailNewton = 3 };
+
 // Partial slots (blk[slot * kBlockPartials + block]).
 enum Slot : int {
     kSlotLoss = 0,
@@ -140,7 +143,8 @@ struct Shard {
     size_t dmma_smem = 0;
     int tail_cluster = 0;   // CTAs of the single-cluster CG tail (0: grid-barrier tail)
     bool hv_write_lp = false;  // capture-time switch: the next fused Hv pass also stores Lp = X v
-    int cg_fuse_it = -1;       // capture-time switch: the next DMMA Hv pass runs CG iteration it's tail
+    int cg_fuse_it = -1;       // CG iteration index for a fused CG tail
+    int dmma_tail = 0;         // capture-time switch: solver tail the next DMMA pass runs (DmmaTail)
     // memo: the point the device cache (L0, P, rowM, rowA, gbase, loss) was built at: the solver
     // iterate s.x, or s.cache_x holding the host vector of the last model-level call
     enum CachePoint { kNone = 0, kAtX = 1, kAtHost = 2 } cache_at = kNone;
