@@ -520,12 +520,24 @@ __global__ void __launch_bounds__(256) k_ls_partials(int64_t n, int K, const dou
                 if (ridge) ax[q] += xt * xt;
             }
         }
-        for (int q = 0; q < kLsChunk && j0 + q < nc; ++q) {
-            double t = block_sum(at[q], red);
-            if (threadIdx.x == 0) slot_ptr(blk, kSlotLsVec + 2 * (j0 + q))[vb] = t;
-            t = block_sum(ax[q], red);
-            if (threadIdx.x == 0) slot_ptr(blk, kSlotLsVec + 2 * (j0 + q) + 1)[vb] = t;
+        // all 2 * kLsChunk block sums at once: butterflies per warp, one barrier, warps in fixed order
+        __shared__ double wred[kLsWarps][2 * kLsChunk];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+        for (int q = 0; q < kLsChunk; ++q) {
+            const double s0 = warp_sum(at[q]), s1 = warp_sum(ax[q]);
+            if (lane == 0) {
+                wred[warp][2 * q] = s0;
+                wred[warp][2 * q + 1] = s1;
+            }
         }
+        __syncthreads();
+        if (threadIdx.x < 2 * kLsChunk && j0 + (int)threadIdx.x / 2 < nc) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += wred[w][threadIdx.x];
+            slot_ptr(blk, kSlotLsVec + 2 * j0 + threadIdx.x)[vb] = t;
+        }
+        __syncthreads();
     }
 }
 
