@@ -357,14 +357,9 @@ struct AdmmRun {
             NADMM_CUDA(cudaMemcpyAsync(s.z, z, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
             pending[i] = !solve_launch(s, ncfg, 0.0, true, rho[i], cfg.inner_iters);
         }
-        for (int i = 0; i < n_local; ++i) {  // gather the workers' inner stats
-            SolveResult r = solve_collect(*shards[i], ncfg, pending[i]);
-            if (r.error) raise((nadmm_status)r.error, "worker inner solve failed");
-            inner += r.iterations;
-            cg_sum += r.cg_sum;
-            fe_sum += r.fe_sum;
-            flags |= r.flags;
-        }
+        // the workers' inner stats come back with the iteration's single synchronisation below
+        for (int i = 0; i < n_local; ++i)
+            if (pending[i]) solve_readback_async(*shards[i]);
         LocalPtrs lp{};  // (2) consensus sum + one allreduce
         lp.n = n_local;
         double rho_sum = 0.0;
@@ -399,10 +394,20 @@ struct AdmmRun {
         ctx->stats.kernel_launches++;
         NADMM_LAUNCH_CHECK();
         std::vector<double> hfz(n_local, 0.0);
+        NADMM_CUDA(cudaEventRecord(ev_now, st));  // z^k and F(z^k) are complete: the row's wall time
         NADMM_CUDA(cudaMemcpyAsync(hred.data(), wred, sizeof(double) * hred.size(), cudaMemcpyDeviceToHost, st));
         if (cfg.eval_objective)
             NADMM_CUDA(cudaMemcpyAsync(hfz.data(), fz, sizeof(double) * n_local, cudaMemcpyDeviceToHost, st));
         NADMM_CUDA(cudaStreamSynchronize(st));
+        for (int i = 0; i < n_local; ++i) {  // gather the workers' inner stats
+            Shard& s = *shards[i];
+            SolveResult r = pending[i] ? solve_result(s, ncfg) : solve_collect(s, ncfg, false);
+            if (r.error) raise((nadmm_status)r.error, "worker inner solve failed");
+            inner += r.iterations;
+            cg_sum += r.cg_sum;
+            fe_sum += r.fe_sum;
+            flags |= r.flags;
+        }
         // rank scalars: sum|x_i|^2, max|y_i|^2, max primal_i, max dual_i, sum primal^2, sum dual^2, sum F_i, |z|^2
         double rs[kStats] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (int i = 0; i < n_local; ++i) {
@@ -450,8 +455,6 @@ struct AdmmRun {
         const double eps_dual = std::sqrt((double)d) * cfg.eps_abs + cfg.eps_rel * c;
         conv = k >= 1 && pmax <= eps_pri && dmax <= eps_dual;  // has_converged
         if (sps && k - snap_it >= cfg.update_period) spectral();  // (4) SPS against the last snapshot
-        NADMM_CUDA(cudaEventRecord(ev_now, st));
-        NADMM_CUDA(cudaEventSynchronize(ev_now));
         float ms = 0.f;
         NADMM_CUDA(cudaEventElapsedTime(&ms, ev_start, ev_now));
         double theta = NAN;

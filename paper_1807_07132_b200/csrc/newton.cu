@@ -210,11 +210,14 @@ static void capture_iteration_graph(Shard& s, int cg_max, int ls_max) {
 
 // Reads back the solver state and trace (one async copy each, one sync); accumulates the Hv timers
 // of the Hv passes that actually ran.
-static void readback(Shard& s, int cg_max) {
+void solve_readback_async(Shard& s) {
     NADMM_CUDA(cudaMemcpyAsync(s.st_host, s.st, sizeof(DevState), cudaMemcpyDeviceToHost, s.ctx->stream));
     NADMM_CUDA(cudaMemcpyAsync(s.trace_host, s.trace, sizeof(DevTrace) * kTraceCap, cudaMemcpyDeviceToHost,
                                s.ctx->stream));
-    NADMM_CUDA(cudaStreamSynchronize(s.ctx->stream));
+}
+
+// After the stream has passed the readback copies: accumulate the Hv timers of the passes that ran.
+static void readback_finish(Shard& s, int cg_max) {
     if (s.g_timing && !s.hv_timers.empty()) {
         const DevState& h = *s.st_host;
         for (int it = 0; it <= cg_max && it < (int)s.hv_timers.size(); ++it) {
@@ -227,6 +230,13 @@ static void readback(Shard& s, int cg_max) {
             }
         }
     }
+}
+
+// Reads back the solver state and trace (one async copy each, one sync).
+static void readback(Shard& s, int cg_max) {
+    solve_readback_async(s);
+    NADMM_CUDA(cudaStreamSynchronize(s.ctx->stream));
+    readback_finish(s, cg_max);
 }
 
 bool solve_launch(Shard& s, const nadmm_newton_cfg& cfg, double lambda, bool aug, double rho, int newton_max) {
@@ -253,6 +263,11 @@ bool solve_launch(Shard& s, const nadmm_newton_cfg& cfg, double lambda, bool aug
     }
     if (newton_max == 0) readback(s, cfg.cg_max_iters);
     return true;
+}
+
+SolveResult solve_result(Shard& s, const nadmm_newton_cfg& cfg) {
+    readback_finish(s, cfg.cg_max_iters);
+    return solve_collect(s, cfg, false);
 }
 
 SolveResult solve_collect(Shard& s, const nadmm_newton_cfg& cfg, bool pending) {

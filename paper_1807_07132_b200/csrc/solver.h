@@ -26,6 +26,10 @@ void ensure_cache_at_x(Shard& s, double lambda);
 // solve_collect reads it back.
 bool solve_launch(Shard& s, const nadmm_newton_cfg& cfg, double lambda, bool aug, double rho, int newton_max);
 SolveResult solve_collect(Shard& s, const nadmm_newton_cfg& cfg, bool pending);
+// Fully asynchronous gather: enqueue the state/trace copies, synchronise elsewhere, then build the
+// result from the host copies with solve_result.
+void solve_readback_async(Shard& s);
+SolveResult solve_result(Shard& s, const nadmm_newton_cfg& cfg);
 SolveResult device_newton_solve(Shard& s, const nadmm_newton_cfg& cfg, double lambda, bool aug, double rho,
                                 int newton_max);
 
