@@ -267,10 +267,35 @@ def main():
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "traffic_source": "profiles/r1_hv_kernel.json (ncu dram__bytes_read+write)", "kernel": "dense Hv pass (shard 6250x3072)", "hv_pass_ms": hv_ms,
+                "traffic": traffic, "traffic_source": "profiles/r1_hv_kernel.json (ncu dram__bytes_read+write)", "kernel": "dense Hv pass with the fused CG step (shard 6250x3072), CUDA events around each launch",
+                "hv_pass_ms": hv_ms,
                 "bytes_per_hv": hv_bytes(n_loc), "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"}
     sess_res = sess.result()
     sess.close()
+
+    # stand-alone Hv pass (model-level device ABI, no fused CG step): the kernel's own roofline
+    import ctypes as _C
+    from paper_1807_07132_b200 import _lib as _L
+
+    d_ = (C - 1) * P
+    wv = torch.tensor(np.random.default_rng(2).normal(size=d_) * 0.01, device="cuda")
+    vv = torch.tensor(np.random.default_rng(1).normal(size=d_), device="cuda")
+    hv = torch.zeros(d_, dtype=torch.float64, device="cuda")
+    lib = _L.lib()
+    lib.nadmm_set_point_dev(shards[0].handle, _C.c_void_p(wv.data_ptr()))
+    for _ in range(3):
+        lib.nadmm_hessian_vec_dev(shards[0].handle, _C.c_void_p(vv.data_ptr()), 0.0, _C.c_void_p(hv.data_ptr()))
+    ctx.synchronize()
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0.record(stream)
+    for _ in range(20):
+        lib.nadmm_hessian_vec_dev(shards[0].handle, _C.c_void_p(vv.data_ptr()), 0.0, _C.c_void_p(hv.data_ptr()))
+    h1.record(stream)
+    h1.synchronize()
+    sa_ms = h0.elapsed_time(h1) / 20
+    roofline["standalone_hv"] = {"us": sa_ms * 1e3, "achieved": hv_bytes(n_loc) / (sa_ms * 1e-3) / 1e9,
+                                 "frac": hv_bytes(n_loc) / (sa_ms * 1e-3) / 1e9 / peak,
+                                 "note": "Hv pass + split-K finalize via nadmm_hessian_vec_dev, no fused CG step"}
 
     # ---------------- e2e: reference-facing worker ABI with host buffers ----------------
     import torch as _t
