@@ -89,9 +89,6 @@ void alloc_work(Shard& s) {
         s.part_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(2LL * s.ctx->num_sms, cap));
         s.part = dev_alloc<double>(s, s.part_chunks * s.d);
     }
-    dmma_setup(s);
-    gemm_setup(s);
-    tail_setup(s);
     if (s.sparse && s.K <= 32) s.wt = dev_alloc<double>(s, s.d);
     s.blk = dev_alloc<double>(s, (int64_t)kSlotCount * kBlockPartials);
     NADMM_CUDA(cudaMemsetAsync(s.blk, 0, sizeof(double) * kSlotCount * kBlockPartials, s.ctx->stream));
@@ -111,6 +108,10 @@ void alloc_work(Shard& s) {
     NADMM_CUDA(cudaMallocHost(&s.trace_host, sizeof(DevTrace) * kTraceCap));
     std::memset(s.prm_host, 0, sizeof(DevParams));
     NADMM_CUDA(cudaMemcpyAsync(s.prm, s.prm_host, sizeof(DevParams), cudaMemcpyHostToDevice, s.ctx->stream));
+    // pass implementations (the DMMA layout search times candidate passes on this shard's data)
+    dmma_setup(s);
+    gemm_setup(s);
+    tail_setup(s);
 }
 
 void upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {

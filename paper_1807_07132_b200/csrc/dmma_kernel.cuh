@@ -235,15 +235,11 @@ constexpr bool kExpNoRem = false;
 #ifndef NADMM_DMMA_RECV_BUFS
 #define NADMM_DMMA_RECV_BUFS 4
 #endif
-#ifndef NADMM_DMMA_EXTRA_STAGES
-#define NADMM_DMMA_EXTRA_STAGES 2
-#endif
 #ifndef NADMM_DMMA_BULK_PUSH
 #define NADMM_DMMA_BULK_PUSH 1
 #endif
 constexpr bool kDmmaBulkPush = NADMM_DMMA_BULK_PUSH;  // exchange by bulk smem->peer copies (else st.async)
 constexpr int kDmmaRecvBufs = NADMM_DMMA_RECV_BUFS;  // receive buffers per CTA, flow-controlled by remote credits
-constexpr int kDmmaExtraStages = NADMM_DMMA_EXTRA_STAGES;  // ring stages beyond the LAG tiles held for phase B
 constexpr int kDmmaRedBufs = 2;   // compute-warp partial buffers (pusher frees them)
 constexpr int kDmmaEpiWarps = 2;  // epilogue warps
 constexpr int kDmmaAux = kDmmaEpiWarps + 2;  // + pusher + producer
@@ -359,11 +355,12 @@ __device__ void dmma_cg_tail(const DmmaArgs& a, int K, int chunks, double* scrat
     }
 }
 
-// LAG: tiles of phase A in flight ahead of phase B; STAGES = LAG + 2 (A ring + one loading).
-template <int MT, int KT, int R, int BM, int LAG, int MODE>
+// LAG: tiles of phase A in flight ahead of phase B; STAGES >= LAG + 2 ring slots (the LAG tiles
+// waiting for phase B, the one in phase A, and the ones loading).
+template <int MT, int KT, int R, int BM, int LAG, int STAGES, int MODE>
 __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
     using namespace dmma_detail;
-    constexpr int STAGES = LAG + kDmmaExtraStages;
+    static_assert(STAGES >= LAG + 2, "ring depth");
     constexpr int K = 8 * KT + R;
     static_assert(BM % 8 == 0 && BM <= 32, "row tile");
     constexpr int KS = DmmaSmem<K>::KS;

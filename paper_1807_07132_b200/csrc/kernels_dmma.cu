@@ -44,26 +44,34 @@ namespace {
 
 constexpr int kBM = 8;
 
+// Pipeline shapes (phase-B lag, ring stages): deeper lag hides a slower exchange, more free stages
+// keep more bytes in flight per SM. Which wins depends on the slice width, so dmma_setup times them.
+struct Pipe {
+    int lag, stages;
+};
+constexpr Pipe kPipes[] = {{4, 6}, {3, 5}, {2, 5}};
+constexpr int kNumPipes = sizeof(kPipes) / sizeof(kPipes[0]);
+
 struct Layout {
     bool ok = false;
-    int mt = 0, nw = 0, cs = 0, fs = 0, S = 0, lag = 0;
+    int mt = 0, nw = 0, cs = 0, fs = 0, S = 0, pipe = 0;
     size_t smem = 0;
     double waste = 0.0;
 };
 
 constexpr size_t kSmemLimit = 220 * 1024;
 
-size_t smem_bytes(int lag, int nw, int S, int K, int cs) {
-    return dmma_smem_bytes(lag + kDmmaExtraStages, kBM, nw, S, K, cs) + 64;
+size_t smem_bytes(int pipe, int nw, int S, int K, int cs) {
+    return dmma_smem_bytes(kPipes[pipe].stages, kBM, nw, S, K, cs) + 64;
 }
 
 // Feasible layouts for K = 9 (KT = 1, R = 1): the CTA slice fs = nw * 8 * mt features with 2..8
-// compute warps, a cluster of cs CTAs covering p with <= 15 % padding, and the ring (LAG + 2 stages)
-// within the shared-memory budget. dmma_setup picks among them by co-resident SMs.
+// compute warps, a cluster of cs CTAs covering p with <= 15 % padding, and the ring within the
+// shared-memory budget. dmma_setup picks among them by co-resident SMs, then by measured time.
 std::vector<Layout> candidate_layouts(int64_t p, int K) {
     std::vector<Layout> out;
     if (K != 9) return out;  // instantiated class counts
-    for (int lag : {4, 3})
+    for (int pipe = 0; pipe < kNumPipes; ++pipe)
         for (int mt : {6, 7, 4, 8})
             for (int cs = 1; cs <= 8; ++cs) {
                 const int W = 8 * mt;
@@ -74,9 +82,9 @@ std::vector<Layout> candidate_layouts(int64_t p, int K) {
                 if (waste > 0.15) continue;
                 int S = fs + 4;
                 while (S % 16 != 4) ++S;
-                const size_t smem = smem_bytes(lag, nw, S, K, cs);
+                const size_t smem = smem_bytes(pipe, nw, S, K, cs);
                 if (smem > kSmemLimit) continue;
-                out.push_back(Layout{true, mt, nw, cs, fs, S, lag, smem, waste});
+                out.push_back(Layout{true, mt, nw, cs, fs, S, pipe, smem, waste});
             }
     return out;
 }
@@ -100,9 +108,9 @@ cudaLaunchConfig_t make_cfg(Shard& s, const Layout& L, int clusters, cudaLaunchA
 
 // Attributes are set once per instantiation, outside any stream capture (dmma_setup), and the
 // co-resident cluster count is queried there too.
-template <int MT, int LAG, int MODE>
+template <int MT, int PIPE, int MODE>
 int setup_one(Shard& s, const Layout& L) {
-    auto kern = dmma_pass_kernel<MT, 1, 1, kBM, LAG, MODE>;
+    auto kern = dmma_pass_kernel<MT, 1, 1, kBM, kPipes[PIPE].lag, kPipes[PIPE].stages, MODE>;
     NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit));
     NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchAttribute attr[2];
@@ -115,54 +123,63 @@ int setup_one(Shard& s, const Layout& L) {
     return nc;
 }
 
-template <int MT, int LAG>
+template <int MT, int PIPE>
 int setup_modes(Shard& s, const Layout& L) {
-    int nc = setup_one<MT, LAG, kModeCache>(s, L);
-    nc = std::min(nc, setup_one<MT, LAG, kModeHv>(s, L));
-    nc = std::min(nc, setup_one<MT, LAG, kModeLp>(s, L));
-    nc = std::min(nc, setup_one<MT, LAG, kModeValue>(s, L));
-    nc = std::min(nc, setup_one<MT, LAG, kModePredict>(s, L));
+    int nc = setup_one<MT, PIPE, kModeCache>(s, L);
+    nc = std::min(nc, setup_one<MT, PIPE, kModeHv>(s, L));
+    nc = std::min(nc, setup_one<MT, PIPE, kModeLp>(s, L));
+    nc = std::min(nc, setup_one<MT, PIPE, kModeValue>(s, L));
+    nc = std::min(nc, setup_one<MT, PIPE, kModePredict>(s, L));
     return nc;
 }
 
-template <int LAG>
-int setup_lag(Shard& s, const Layout& L) {
+template <int PIPE>
+int setup_pipe(Shard& s, const Layout& L) {
     switch (L.mt) {
-        case 4: return setup_modes<4, LAG>(s, L);
-        case 6: return setup_modes<6, LAG>(s, L);
-        case 7: return setup_modes<7, LAG>(s, L);
-        case 8: return setup_modes<8, LAG>(s, L);
+        case 4: return setup_modes<4, PIPE>(s, L);
+        case 6: return setup_modes<6, PIPE>(s, L);
+        case 7: return setup_modes<7, PIPE>(s, L);
+        case 8: return setup_modes<8, PIPE>(s, L);
         default: return 0;
     }
 }
 
-int setup_layout(Shard& s, const Layout& L) { return L.lag == 4 ? setup_lag<4>(s, L) : setup_lag<3>(s, L); }
+int setup_layout(Shard& s, const Layout& L) {
+    switch (L.pipe) {
+        case 0: return setup_pipe<0>(s, L);
+        case 1: return setup_pipe<1>(s, L);
+        case 2: return setup_pipe<2>(s, L);
+        default: return 0;
+    }
+}
 
-template <int MT, int LAG, int MODE>
+template <int MT, int PIPE, int MODE>
 void launch_one(Shard& s, const Layout& L, const DmmaArgs& a, int clusters) {
-    auto kern = dmma_pass_kernel<MT, 1, 1, kBM, LAG, MODE>;
+    auto kern = dmma_pass_kernel<MT, 1, 1, kBM, kPipes[PIPE].lag, kPipes[PIPE].stages, MODE>;
     cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = make_cfg(s, L, clusters, attr);
     NADMM_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
 }
 
-template <int LAG, int MODE>
-void launch_lag(Shard& s, const Layout& L, const DmmaArgs& a, int clusters) {
+template <int PIPE, int MODE>
+void launch_pipe(Shard& s, const Layout& L, const DmmaArgs& a, int clusters) {
     switch (L.mt) {
-        case 4: launch_one<4, LAG, MODE>(s, L, a, clusters); break;
-        case 6: launch_one<6, LAG, MODE>(s, L, a, clusters); break;
-        case 7: launch_one<7, LAG, MODE>(s, L, a, clusters); break;
-        case 8: launch_one<8, LAG, MODE>(s, L, a, clusters); break;
+        case 4: launch_one<4, PIPE, MODE>(s, L, a, clusters); break;
+        case 6: launch_one<6, PIPE, MODE>(s, L, a, clusters); break;
+        case 7: launch_one<7, PIPE, MODE>(s, L, a, clusters); break;
+        case 8: launch_one<8, PIPE, MODE>(s, L, a, clusters); break;
         default: raise(NADMM_ECONFIG, "dmma: unsupported layout");
     }
 }
 
 template <int MODE>
 void launch_mode(Shard& s, const Layout& L, const DmmaArgs& a, int clusters) {
-    if (L.lag == 4)
-        launch_lag<4, MODE>(s, L, a, clusters);
-    else
-        launch_lag<3, MODE>(s, L, a, clusters);
+    switch (L.pipe) {
+        case 0: launch_pipe<0, MODE>(s, L, a, clusters); break;
+        case 1: launch_pipe<1, MODE>(s, L, a, clusters); break;
+        case 2: launch_pipe<2, MODE>(s, L, a, clusters); break;
+        default: raise(NADMM_ECONFIG, "dmma: unsupported pipeline");
+    }
 }
 
 Layout shard_layout(const Shard& s) {
@@ -173,7 +190,7 @@ Layout shard_layout(const Shard& s) {
     L.cs = s.dmma_cs;
     L.fs = s.dmma_fs;
     L.S = s.dmma_S;
-    L.lag = s.dmma_lag;
+    L.pipe = s.dmma_pipe;
     L.smem = s.dmma_smem;
     return L;
 }
@@ -182,46 +199,96 @@ Layout shard_layout(const Shard& s) {
 
 bool dmma_supported(const Shard& s) { return s.dmma_clusters > 0; }
 
-// Picks the layout that keeps the most SMs busy (co-resident clusters x cluster size, capped at the
-// SM count, discounted by feature padding); ties go to more compute warps, the deeper pipeline
-// (LAG 4) and the smaller cluster.
+namespace {
+
+void apply_layout(Shard& s, const Layout& L, int active) {
+    s.dmma_mt = L.mt;
+    s.dmma_nw = L.nw;
+    s.dmma_cs = L.cs;
+    s.dmma_fs = L.fs;
+    s.dmma_S = L.S;
+    s.dmma_pipe = L.pipe;
+    s.dmma_smem = L.smem;
+    const int64_t ntiles = (s.n + kBM - 1) / kBM;
+    s.dmma_clusters = (int)std::max<int64_t>(
+        1, std::min<int64_t>({ntiles, (int64_t)active, (int64_t)s.part_chunks, (int64_t)kBlockPartials}));
+}
+
+// Device time of one Hv pass with the shard's current layout (scratch outputs only).
+float time_hv_pass(Shard& s) {
+    cudaEvent_t e0, e1;
+    NADMM_CUDA(cudaEventCreate(&e0));
+    NADMM_CUDA(cudaEventCreate(&e1));
+    dmma_pass(s, kModeHv, s.x, nullptr);  // warm-up
+    NADMM_CUDA(cudaEventRecord(e0, s.ctx->stream));
+    for (int r = 0; r < 3; ++r) dmma_pass(s, kModeHv, s.x, nullptr);
+    NADMM_CUDA(cudaEventRecord(e1, s.ctx->stream));
+    NADMM_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    NADMM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return ms;
+}
+
+}  // namespace
+
+// Layout choice: keep the feasible layouts that busy the most SMs (co-resident clusters x cluster
+// size, capped at the SM count, discounted by feature padding); among those, time one Hv pass of
+// each on the shard itself and keep the fastest (NADMM_DMMA_AUTOTUNE=0: tie-break by more compute
+// warps, then the deeper pipeline, then the smaller cluster). Runs once per shard, outside capture.
 void dmma_setup(Shard& s) {
     s.dmma_clusters = 0;
     static const bool disabled = getenv("NADMM_DISABLE_DMMA") != nullptr;
     if (disabled || s.sparse || s.ldx % 2 != 0) return;
     const char* force_cs = getenv("NADMM_DMMA_CS");  // profiling: restrict the cluster size
-    Layout best;
-    int best_active = 0;
-    double best_score = -1.0;
+    const char* force_pipe = getenv("NADMM_DMMA_PIPE");
+    const char* at = getenv("NADMM_DMMA_AUTOTUNE");
+    const bool autotune = !(at && at[0] == '0');
+    struct Cand {
+        Layout L;
+        int active;
+        double sms;
+    };
+    std::vector<Cand> cands;
+    double best_sms = 0.0;
     for (const Layout& L : candidate_layouts(s.p, s.K)) {
         if (force_cs && L.cs != atoi(force_cs)) continue;
+        if (force_pipe && L.pipe != atoi(force_pipe)) continue;
         const int active = setup_layout(s, L);
         if (active < 1) continue;
-        // SMs kept busy (one CTA per SM by design), then the most compute warps per CTA (more work
-        // per tile and per barrier phase), the deeper pipeline, the smaller cluster
-        const int sms = std::min(active * L.cs, s.ctx->num_sms);
-        const double score = sms * (1.0 - L.waste) * 1000.0 + L.nw * 10.0 + (L.lag == 4 ? 5.0 : 0.0) - L.cs;
-        if (score > best_score) {
-            best_score = score;
-            best = L;
-            best_active = active;
+        const double sms = std::min(active * L.cs, s.ctx->num_sms) * (1.0 - L.waste);
+        cands.push_back({L, active, sms});
+        best_sms = std::max(best_sms, sms);
+    }
+    std::vector<Cand> top;
+    for (const Cand& c : cands)
+        if (c.sms >= 0.98 * best_sms) top.push_back(c);
+    if (top.empty()) return;
+    std::sort(top.begin(), top.end(), [](const Cand& a, const Cand& b) {
+        const double sa = a.L.nw * 10.0 - a.L.pipe - a.L.cs * 0.1, sb = b.L.nw * 10.0 - b.L.pipe - b.L.cs * 0.1;
+        return sa > sb;
+    });
+    size_t pick = 0;
+    if (autotune && top.size() > 1) {
+        float best_ms = 1e30f;
+        for (size_t k = 0; k < top.size(); ++k) {
+            apply_layout(s, top[k].L, top[k].active);
+            const float ms = time_hv_pass(s);
+            if (ms < best_ms) {
+                best_ms = ms;
+                pick = k;
+            }
         }
     }
-    if (!best.ok) return;
-    s.dmma_mt = best.mt;
-    s.dmma_nw = best.nw;
-    s.dmma_cs = best.cs;
-    s.dmma_fs = best.fs;
-    s.dmma_S = best.S;
-    s.dmma_lag = best.lag;
-    s.dmma_smem = best.smem;
-    const int64_t ntiles = (s.n + kBM - 1) / kBM;
-    s.dmma_clusters = (int)std::max<int64_t>(
-        1, std::min<int64_t>({ntiles, (int64_t)best_active, (int64_t)s.part_chunks, (int64_t)kBlockPartials}));
+    const Layout& best = top[pick].L;
+    apply_layout(s, best, top[pick].active);
     if (getenv("NADMM_DMMA_VERBOSE"))
-        fprintf(stderr, "[nadmm] dmma layout p=%lld: cluster %d x %d clusters (%d SMs), %d warps x %d features, lag %d, smem %zu\n",
-                (long long)s.p, best.cs, s.dmma_clusters, best.cs * s.dmma_clusters, best.nw, 8 * best.mt, best.lag,
-                best.smem);
+        fprintf(stderr,
+                "[nadmm] dmma layout p=%lld: cluster %d x %d clusters (%d SMs), %d warps x %d features, lag %d, "
+                "%d stages, smem %zu (%zu candidates timed)\n",
+                (long long)s.p, best.cs, s.dmma_clusters, best.cs * s.dmma_clusters, best.nw, 8 * best.mt,
+                kPipes[best.pipe].lag, kPipes[best.pipe].stages, best.smem, autotune ? top.size() : (size_t)0);
 }
 
 int dmma_clusters(const Shard& s) { return s.dmma_clusters; }

@@ -139,7 +139,7 @@ struct Shard {
     int rows_grid = 0;  // blocks of the last rows pass (partials count)
     int last_chunks = 0;    // split-K partial chunks written by the last fused DMMA pass
     int dmma_clusters = 0;  // co-resident clusters of the fused DMMA pass (0: path unavailable)
-    int dmma_mt = 0, dmma_nw = 0, dmma_cs = 0, dmma_fs = 0, dmma_S = 0, dmma_lag = 0;  // chosen layout
+    int dmma_mt = 0, dmma_nw = 0, dmma_cs = 0, dmma_fs = 0, dmma_S = 0, dmma_pipe = 0;  // chosen layout
     size_t dmma_smem = 0;
     int tail_cluster = 0;   // CTAs of the single-cluster CG tail (0: grid-barrier tail)
     bool hv_write_lp = false;  // capture-time switch: the next fused Hv pass also stores Lp = X v
