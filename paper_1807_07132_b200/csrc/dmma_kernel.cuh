@@ -212,26 +212,6 @@ constexpr int kDmmaPrefetch = NADMM_DMMA_PREFETCH;  // L2 prefetch distance in t
 #endif
 constexpr int kDmmaChains = NADMM_DMMA_CHAINS;  // phase-A accumulator chains per warp
 
-#ifdef NADMM_EXP_NOA
-constexpr bool kExpNoA = true;  // timing experiments only (wrong results)
-#else
-constexpr bool kExpNoA = false;
-#endif
-#ifdef NADMM_EXP_NOB
-constexpr bool kExpNoB = true;
-#else
-constexpr bool kExpNoB = false;
-#endif
-#ifdef NADMM_EXP_NOXCHG
-constexpr bool kExpNoXchg = true;
-#else
-constexpr bool kExpNoXchg = false;
-#endif
-#ifdef NADMM_EXP_NOREM
-constexpr bool kExpNoRem = true;
-#else
-constexpr bool kExpNoRem = false;
-#endif
 #ifndef NADMM_DMMA_RECV_BUFS
 #define NADMM_DMMA_RECV_BUFS 4
 #endif
@@ -484,7 +464,7 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
             mbar_wait(&red_full[b], (uint32_t)((i / kDmmaRedBufs) & 1));
             DMMA_TRACE(i, 2);
             // every CTA of the cluster released receive buffer br (its previous tile's epilogue is done)
-            if (!kExpNoXchg && i >= kDmmaRecvBufs) mbar_wait(&credit[br], (uint32_t)(((i / kDmmaRecvBufs) - 1) & 1));
+            if (i >= kDmmaRecvBufs) mbar_wait(&credit[br], (uint32_t)(((i / kDmmaRecvBufs) - 1) & 1));
             const double* rd = red + (size_t)b * nc * PART;
             const uint32_t dst_local = smem_u32(recv + ((size_t)br * csize + crank) * PART);
             const uint32_t bar_local = smem_u32(&rbar[br]);
@@ -497,18 +477,14 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                     v0[w] = v.x;
                     v1[w] = v.y;
                 }
-#ifdef NADMM_EXP_NOPUSHSUM
-                const double s0 = v0[0], s1 = v1[0];  // timing experiment only (wrong results)
-#else
                 const double s0 = tree_sum(v0, nc), s1 = tree_sum(v1, nc);
-#endif
                 if (kDmmaBulkPush)
                     *reinterpret_cast<double2*>(sendb + (size_t)br * PART + 2 * i2) = make_double2(s0, s1);
                 else
                     for (uint32_t q = 0; q < csize; ++q)
                         st_async_v2(mapa(dst_local + 16u * i2, q), s0, s1, mapa(bar_local, q));
             }
-            if (kDmmaBulkPush && !kExpNoXchg) {
+            if (kDmmaBulkPush) {
                 // the summed partial goes to every peer as one bulk copy each (lane q -> CTA q); the
                 // send buffer br is rewritten only after every peer returned its credit for br
                 fence_proxy_async();
@@ -533,10 +509,8 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
         for (int i = ew; i < T; i += kDmmaEpiWarps) {
             const int stage = i % STAGES, br = i % kDmmaRecvBufs;
             const int64_t r0 = tile_of(i) * BM;
-            if (!kExpNoXchg) {
-                if (lane == 0) mbar_expect_tx(&rbar[br], (uint32_t)csize * PART * 8u);
-                mbar_wait(&rbar[br], (uint32_t)((i / kDmmaRecvBufs) & 1));
-            }
+            if (lane == 0) mbar_expect_tx(&rbar[br], (uint32_t)csize * PART * 8u);
+            mbar_wait(&rbar[br], (uint32_t)((i / kDmmaRecvBufs) & 1));
             if (ew == 0) DMMA_TRACE(i, 4);
             if (NEED_P || NEED_Y) mbar_wait(&full[stage], (uint32_t)((i / STAGES) & 1));
             if (ew == 0) DMMA_TRACE(i, 8);
@@ -556,18 +530,14 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
 #pragma unroll
                 for (int j = 0; j < NE; ++j) {
                     const int e = lane + 32 * j;
-#ifdef NADMM_EXP_NOEPI
-                    const double s = v[j][0];  // timing experiment only (wrong results)
-#else
                     const double s = tree_sum(v[j], (int)csize);
-#endif
                     if (e < BM * K) lgw[(e / K) * KP + (e % K)] = s;
                 }
             }
             __syncwarp();
             if (ew == 0) DMMA_TRACE(i, 9);
             // receive buffer br consumed: return one credit to every CTA of the cluster
-            if (lane == 0 && !kExpNoXchg)
+            if (lane == 0)
                 for (uint32_t q = 0; q < csize; ++q) mbar_arrive_remote(&credit[br], q);
             if (ew == 0) DMMA_TRACE(i, 11);
             // (2) row epilogue. Hv / Lp: one lane per row.
@@ -592,11 +562,7 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                             }
                             vt[c] = vw[c];
                         }
-#ifdef NADMM_EXP_NOEPI
-                        const double rs = vt[0];  // timing experiment only (wrong results)
-#else
                         const double rs = tree_sum(vt, K);  // row_sum(V o P)
-#endif
 #pragma unroll
                         for (int c = 0; c < K; ++c) urow[c] = vw[c] - pv[c] * rs;
                         if (a.lp_out && crank == 0)
@@ -759,9 +725,9 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                 for (int g = 0; g < G; ++g) {
                     const double x = xt[(g * 8 + gq) * S + fw + 4 * s + tq];
 #pragma unroll
-                    for (int kt = 0; kt < KT; ++kt) if (!kExpNoA) dmma(acca[s % NCH][g][kt], x, bv[s][kt]);
+                    for (int kt = 0; kt < KT; ++kt) dmma(acca[s % NCH][g][kt], x, bv[s][kt]);
 #pragma unroll
-                    for (int r = 0; r < R; ++r) if (!kExpNoRem) accar[s % RC][g][r] = fma(x, vr[s][r], accar[s % RC][g][r]);
+                    for (int r = 0; r < R; ++r) accar[s % RC][g][r] = fma(x, vr[s][r], accar[s % RC][g][r]);
                 }
             }
 #pragma unroll
@@ -825,12 +791,12 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                     for (int mp = 0; mp < MT / 2; ++mp) {
                         const double2 x2 = *reinterpret_cast<const double2*>(xr + mp * 16 + 2 * gq);
 #pragma unroll
-                        for (int kt = 0; kt < KT; ++kt) if (!kExpNoB) {
+                        for (int kt = 0; kt < KT; ++kt) {
                             dmma(accb[2 * mp][kt], x2.x, ub[kt]);
                             dmma(accb[2 * mp + 1][kt], x2.y, ub[kt]);
                         }
 #pragma unroll
-                        for (int r = 0; r < R; ++r) if (!kExpNoRem) {
+                        for (int r = 0; r < R; ++r) {
                             accbr[2 * mp][r] = fma(x2.x, ur[r], accbr[2 * mp][r]);
                             accbr[2 * mp + 1][r] = fma(x2.y, ur[r], accbr[2 * mp + 1][r]);
                         }
