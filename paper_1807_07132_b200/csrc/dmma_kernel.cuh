@@ -542,42 +542,42 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
             if (ew == 0) DMMA_TRACE(i, 11);
             // (2) row epilogue. Hv / Lp: one lane per row.
             if (MODE == kModeHv || MODE == kModeLp) {
-              if (lane < BM) {
-                const int row = lane;
-                const int64_t gi = r0 + row;
-                const bool valid = gi < n;
-                const double* lg = lgw + row * KP;
-                double* urow = ut + (size_t)stage * BM * KS + row * KS;
-                if (MODE == kModeHv) {
-                    const double* pr = ps + (size_t)stage * BM * KE + row * K;
-                    if (valid) {
-                        constexpr int KT2 = K <= 2 ? 2 : K <= 4 ? 4 : K <= 8 ? 8 : K <= 16 ? 16 : 32;
-                        double vw[KT2], pv[K], vt[KT2];
+                if (lane < BM) {
+                    const int row = lane;
+                    const int64_t gi = r0 + row;
+                    const bool valid = gi < n;
+                    const double* lg = lgw + row * KP;
+                    double* urow = ut + (size_t)stage * BM * KS + row * KS;
+                    if (MODE == kModeHv) {
+                        const double* pr = ps + (size_t)stage * BM * KE + row * K;
+                        if (valid) {
+                            constexpr int KT2 = K <= 2 ? 2 : K <= 4 ? 4 : K <= 8 ? 8 : K <= 16 ? 16 : 32;
+                            double vw[KT2], pv[K], vt[KT2];
 #pragma unroll
-                        for (int c = 0; c < KT2; ++c) {
-                            vw[c] = 0.0;
-                            if (c < K) {
-                                pv[c] = pr[c];
-                                vw[c] = lg[c] * pv[c];
+                            for (int c = 0; c < KT2; ++c) {
+                                vw[c] = 0.0;
+                                if (c < K) {
+                                    pv[c] = pr[c];
+                                    vw[c] = lg[c] * pv[c];
+                                }
+                                vt[c] = vw[c];
                             }
-                            vt[c] = vw[c];
+                            const double rs = tree_sum(vt, K);  // row_sum(V o P)
+#pragma unroll
+                            for (int c = 0; c < K; ++c) urow[c] = vw[c] - pv[c] * rs;
+                            if (a.lp_out && crank == 0)
+#pragma unroll
+                                for (int c = 0; c < K; ++c) a.lp_out[gi * K + c] = lg[c];
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < K; ++c) urow[c] = 0.0;
                         }
-                        const double rs = tree_sum(vt, K);  // row_sum(V o P)
+                    } else if (MODE == kModeLp) {
+                        if (valid && crank == 0)
 #pragma unroll
-                        for (int c = 0; c < K; ++c) urow[c] = vw[c] - pv[c] * rs;
-                        if (a.lp_out && crank == 0)
-#pragma unroll
-                            for (int c = 0; c < K; ++c) a.lp_out[gi * K + c] = lg[c];
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < K; ++c) urow[c] = 0.0;
+                            for (int c = 0; c < K; ++c) a.Lp[gi * K + c] = lg[c];
                     }
-                } else if (MODE == kModeLp) {
-                    if (valid && crank == 0)
-#pragma unroll
-                        for (int c = 0; c < K; ++c) a.Lp[gi * K + c] = lg[c];
                 }
-              }
             } else {
                 // stable softmax cache / loss / argmax (src/softmax.cpp:51-95, 118-139): four lanes
                 // per row, lane q owning classes q, q+4, ...; row max / sums by quad butterflies
