@@ -850,9 +850,14 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
         const int64_t d = (int64_t)K * p;
         if (MODE == kModeHv && a.tail == kTailCg)
             dmma_cg_tail(a, K, (int)ncl, misc, misc + 127);
-        else if (MODE == kModeHv && a.tail == kTailCert)
-            cert_tail_body(d, a.st, a.prm, a.part, (int)ncl, a.lp_from_cert, a.g, a.cg_p, a.cg_hd, a.blk, (int)ncl,
-                           a.hv_ctr, a.done_ctr, misc, misc + 127);
+        else if (MODE == kModeHv && a.tail == kTailCert) {
+            const bool lp_need = cert_tail_body(d, a.st, a.prm, a.part, (int)ncl, a.lp_from_cert, a.g, a.cg_p,
+                                                a.cg_hd, a.blk, (int)ncl, a.hv_ctr, a.done_ctr, misc, misc + 127);
+            // the Armijo search needs only L0 and this pass's Lp = X p: run it here unless p changed
+            if (a.st->it_act && !lp_need)
+                ls_fused_body(n, K, a.L0, a.Lp, a.labels, d, const_cast<double*>(a.x), a.cg_p, a.z, a.y, a.prm, a.st,
+                              a.blk, a.done_ctr, xs, misc + 126);  // the X ring is free: scratch
+        }
         else if (MODE == kModeCache && a.tail == kTailNewton)
             newton_tail_body(d, a.st, a.prm, a.part, (int)ncl, a.x, a.z, a.y, a.gbase, a.g, a.t, a.blk, (int)ncl,
                              a.scal, a.trace, a.trace_cap, a.done_ctr, misc);

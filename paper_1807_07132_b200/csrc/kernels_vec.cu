@@ -700,10 +700,12 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
     op_lp(s, s.pd, &s.st->lp_need);  // Lp = X p, only when p changed after the certificate pass
     tl_mark(s, "lp_pass");
     const int rblocks = std::max(1, (int)std::min<int64_t>((s.n + 31) / 32, kBlockPartials));
+    // DMMA shards run the line search inside the certificate pass unless p changed after it
+    const int32_t* ls_guard = fused_tail ? &s.st->lp_need : it_act;
     launch_pdl(k_ls_partials, rblocks + grid, 256, 0, st, s.n, s.K, s.L0, s.Lp, s.labels, rblocks, s.d, s.x, s.pd,
-               s.z, s.y, s.prm, s.blk, it_act);
+               s.z, s.y, s.prm, s.blk, ls_guard);
     tl_mark(s, "ls_partials");
-    launch_pdl(k_ls_step, grid, 256, 0, st, s.d, s.st, s.prm, s.blk, rblocks, grid, s.x, s.pd, it_act);
+    launch_pdl(k_ls_step, grid, 256, 0, st, s.d, s.st, s.prm, s.blk, rblocks, grid, s.x, s.pd, ls_guard);
     tl_mark(s, "ls_step");
     s.ctx->stats.kernel_launches += 2;
     NADMM_LAUNCH_CHECK();

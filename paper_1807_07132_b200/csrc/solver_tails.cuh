@@ -42,13 +42,13 @@ __device__ __forceinline__ double sum_chunks(const double* __restrict__ part, in
 // CG-failure fallback p = -g (src/newton.cpp:100-104), the descent test p'g >= 0 -> p = -g
 // (105-109) and the line-search slope p'g. One grid barrier between the slope partials and the
 // decision. Shared by k_cert_tail and the certificate DMMA pass (run by its whole grid).
-__device__ __forceinline__ void cert_tail_body(int64_t d, DevState* st, const DevParams* prm,
+__device__ __forceinline__ bool cert_tail_body(int64_t d, DevState* st, const DevParams* prm,
                                                const double* __restrict__ part, int chunks, int lp_from_cert,
                                                const double* __restrict__ g, double* __restrict__ p,
                                                double* __restrict__ hd, double* blk, int ncert,
                                                unsigned long long* hv_ctr, unsigned long long* bar, double* red,
                                                double* sc) {
-    if (!st->it_act) return;
+    if (!st->it_act) return false;
     const bool cert = st->cert_act, failed = st->cg_failed;
     const double lam = prm->lambda, rho = prm->rho;
     const bool aug = prm->augmented;
@@ -96,6 +96,7 @@ __device__ __forceinline__ void cert_tail_body(int64_t d, DevState* st, const De
             st->lp_need = (!cert || failed || flip || !lp_from_cert) ? 1 : 0;
         }
     }
+    return !cert || failed || flip || !lp_from_cert;  // the same in every block
 }
 
 // End of a Newton iteration after the cache pass at the new x (src/newton.cpp:121-127 with the memo
@@ -175,6 +176,127 @@ __device__ __forceinline__ void newton_tail_body(int64_t d, DevState* st, const 
         st->error = NADMM_ESOLVER;
         st->active = 0;
     }
+}
+
+// Batched Armijo line search (src/newton.cpp:56-71, as k_ls_partials + k_ls_step) run by a whole
+// co-resident grid: (row group, candidate) items -> one partial each in slot kSlotLs + j (group index),
+// vector candidate terms -> block partials, one grid barrier, then every block evaluates all
+// candidates from the same partials, applies the first-accept rule and steps x += a p.
+// `scratch` holds >= 32 * kLsFusedChunk doubles.
+constexpr int kLsFusedChunk = 16;
+
+__device__ __forceinline__ void ls_fused_body(int64_t n, int K, const double* __restrict__ L0, const double* __restrict__ Lp,
+                              const int32_t* __restrict__ labels, int64_t d, double* __restrict__ x,
+                              const double* __restrict__ p, const double* __restrict__ z,
+                              const double* __restrict__ y, const DevParams* prm, DevState* st, double* blk,
+                              unsigned long long* bar, double* scratch, double* sc) {
+    const int nc = prm->ls_max_iters + 1;
+    const double gamma = prm->backtrack_gamma;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    // rows: groups of rows_per_group rows (a multiple of 32, <= kBlockPartials groups)
+    int64_t rpg = ((n + kBlockPartials - 1) / kBlockPartials + 31) / 32 * 32;
+    if (rpg < 32) rpg = 32;
+    const int ngroups = (int)((n + rpg - 1) / rpg);
+    const int64_t items = (int64_t)ngroups * nc;
+    for (int64_t it = (int64_t)blockIdx.x * nwarps + warp; it < items; it += (int64_t)gridDim.x * nwarps) {
+        const int j = (int)(it % nc), grp = (int)(it / nc);
+        double a = 1.0;
+        for (int q = 0; q < j; ++q) a *= gamma;  // alpha *= backtrack_gamma (src/newton.cpp:69)
+        double acc = 0.0;
+        const int64_t r_end = (grp + 1) * rpg < n ? (grp + 1) * rpg : n;
+        for (int64_t i = grp * rpg + lane; i < r_end; i += 32) {
+            const double* l0 = L0 + i * K;
+            const double* lp = Lp + i * K;
+            const int b = labels[i];
+            double m = l0[0] + a * lp[0];
+            for (int c = 1; c < K; ++c) {
+                const double l = l0[c] + a * lp[c];
+                if (l > m) m = l;
+            }
+            m = m > 0.0 ? m : 0.0;
+            double s = 0.0;
+            for (int c = 0; c < K; ++c) s += exp((l0[c] + a * lp[c]) - m);
+            acc += (m + log(exp(-m) + s)) - (b <= K ? l0[b - 1] + a * lp[b - 1] : 0.0);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) slot_ptr(blk, kSlotLs + j)[grp] = acc;
+    }
+    // vector terms of every candidate: |z - x_j + y/rho|^2 and |x_j|^2, x_j = x + a_j p
+    const double rho = prm->rho;
+    const bool aug = prm->augmented, ridge = prm->lambda > 0.0;
+    for (int j0 = 0; j0 < nc; j0 += kLsFusedChunk) {
+        double alpha[kLsFusedChunk], at[kLsFusedChunk], ax[kLsFusedChunk];
+        double a = 1.0;
+        for (int q = 0; q < j0; ++q) a *= gamma;
+#pragma unroll
+        for (int q = 0; q < kLsFusedChunk; ++q) {
+            alpha[q] = a;
+            a *= gamma;
+            at[q] = 0.0;
+            ax[q] = 0.0;
+        }
+        GRID_STRIDE(jj, d) {
+            const double xj = x[jj], pj = p[jj];
+            const double zj = aug ? z[jj] : 0.0, yr = aug ? y[jj] / rho : 0.0;
+#pragma unroll
+            for (int q = 0; q < kLsFusedChunk; ++q) {
+                const double xt = xj + alpha[q] * pj;  // x + alpha * p (src/newton.cpp:62)
+                if (aug) {
+                    const double tq = (zj - xt) + yr;
+                    at[q] += tq * tq;
+                }
+                if (ridge) ax[q] += xt * xt;
+            }
+        }
+        __syncthreads();  // scratch reuse
+#pragma unroll
+        for (int q = 0; q < kLsFusedChunk; ++q) {
+            const double s0 = warp_sum(at[q]), s1 = warp_sum(ax[q]);
+            if (lane == 0) {
+                scratch[warp * 2 * kLsFusedChunk + 2 * q] = s0;
+                scratch[warp * 2 * kLsFusedChunk + 2 * q + 1] = s1;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < 2 * kLsFusedChunk && j0 + (int)threadIdx.x / 2 < nc) {
+            double t = 0.0;
+            for (int w = 0; w < nwarps; ++w) t += scratch[w * 2 * kLsFusedChunk + threadIdx.x];
+            slot_ptr(blk, kSlotLsVec + 2 * j0 + threadIdx.x)[blockIdx.x] = t;
+        }
+    }
+    grid_barrier(bar);
+    // every block: candidate objectives (one warp per candidate), first-accept rule, step
+    __syncthreads();
+    double* fj = scratch;  // nc <= kMaxLs + 1 doubles
+    for (int j = warp; j < nc; j += nwarps) {
+        double f = reduce_partials(slot_ptr(blk, kSlotLs + j), ngroups);
+        if (prm->lambda > 0.0) f += 0.5 * prm->lambda * reduce_partials(slot_ptr(blk, kSlotLsVec + 2 * j + 1), gridDim.x);
+        if (prm->augmented) f = f + 0.5 * prm->rho * reduce_partials(slot_ptr(blk, kSlotLsVec + 2 * j), gridDim.x);
+        if (lane == 0) fj[j] = f;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double alpha = 1.0;
+        int evals = 0, capped = 0;
+        for (int j = 0; j < nc; ++j) {
+            ++evals;
+            if (fj[j] <= st->f_x + alpha * prm->armijo_beta * st->slope) break;
+            if (j >= prm->ls_max_iters) {
+                capped = 1;
+                break;
+            }
+            alpha *= prm->backtrack_gamma;
+        }
+        *sc = alpha;
+        if (blockIdx.x == 0) {
+            st->ls_alpha = alpha;
+            st->ls_evals = evals;
+            st->ls_capped = capped;
+        }
+    }
+    __syncthreads();
+    const double a = *sc;
+    GRID_STRIDE(jj, d) x[jj] += a * p[jj];
 }
 
 }  // namespace nadmm
