@@ -584,10 +584,14 @@ nadmm_status nadmm_worker_solve(nadmm_worker w, double rho, const double* z, con
         c.newton_max_iters = inner_iters;  // src/worker.cpp:173
         upload(s.z, z, sizeof(double) * s.d, s.ctx->stream);
         upload(s.y, y, sizeof(double) * s.d, s.ctx->stream);
-        SolveResult r = device_newton_solve(s, c, 0.0, true, rho, inner_iters);  // base lambda 0 (src/worker.cpp:130)
+        // base lambda 0 (src/worker.cpp:130); x and the solver state come back with one synchronisation
+        const bool done = solve_launch(s, c, 0.0, true, rho, inner_iters);
+        if (x_out) NADMM_CUDA(cudaMemcpyAsync(x_out, s.x, sizeof(double) * s.d, cudaMemcpyDeviceToHost, s.ctx->stream));
+        if (!done) solve_readback_async(s);
+        NADMM_CUDA(cudaStreamSynchronize(s.ctx->stream));
+        SolveResult r = done ? solve_collect(s, c, false) : solve_result(s, c);
         if (r.error == NADMM_ESOLVER) raise(NADMM_ESOLVER, "newton_solve: non-finite objective");
         if (r.error == NADMM_ECONFIG) raise(NADMM_ECONFIG, "cg_solve requires ||g|| > 0");
-        if (x_out) download(x_out, s.x, sizeof(double) * s.d, s.ctx->stream);
         if (stats) *stats = nadmm_inner_stats{r.final_grad_norm, (uint32_t)r.iterations, (uint32_t)r.cg_sum,
                                               (uint32_t)r.fe_sum, (uint32_t)r.flags};
     });
