@@ -316,8 +316,7 @@ def main():
     def e2e_step():
         hv = 0
         for i, w in enumerate(workers):
-            x, s = w.solve(rho, zbuf, ybufs[i], cfg.newton, 1)
-            xbufs[i][:] = x
+            _, s = w.solve(rho, zbuf, ybufs[i], cfg.newton, 1, out=xbufs[i])  # x lands in pinned memory
             hv += s.cg_iters + s.inner_iters
         S = np.zeros(d + 1)
         for i in range(len(workers)):  # reference coordinator: z_update / y_update

@@ -403,11 +403,20 @@ class Worker:
         _check(L.lib().nadmm_worker_create(shard.handle, C.byref(h)))
         self.handle, self.shard = h, shard
 
-    def solve(self, rho: float, z, y, cfg: Optional[NewtonConfig] = None, inner_iters: int = 1):
+    def solve(self, rho: float, z, y, cfg: Optional[NewtonConfig] = None, inner_iters: int = 1, out=None):
+        """One scatter -> gather round; `out` (optional, e.g. a pinned float64 buffer of length d)
+        receives x directly."""
         cfg = cfg or NewtonConfig()
         z = _wvec(self.shard, z, "z")
         y = _wvec(self.shard, y, "y")
-        x = np.zeros(self.shard.weight_dim())
+        d = self.shard.weight_dim()
+        if out is not None:
+            if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.shape == (d,)
+                    and out.flags.c_contiguous):
+                raise ConfigError(f"out must be a contiguous float64 array of length {d}")
+            x = out
+        else:
+            x = np.zeros(d)
         st = L.InnerStats()
         c = cfg.to_c()
         _check(L.lib().nadmm_worker_solve(self.handle, float(rho), _dp(z), _dp(y), C.byref(c), int(inner_iters),

@@ -159,7 +159,13 @@ def test_worker_sequence_matches_reference(nadmm, ref):
     for k in range(4):
         z, yy = rng.normal(size=d) * 0.1, rng.normal(size=d) * 0.1
         rho = [1.0, 1.0, 0.5, 3.0][k]
-        xg, sg = w.solve(rho, z, yy)
+        if k % 2:
+            xg, sg = w.solve(rho, z, yy)
+        else:  # caller-provided output buffer
+            buf = np.full(d, np.nan)
+            xo, sg = w.solve(rho, z, yy, out=buf)
+            assert xo is buf
+            xg = buf
         xr, sr = rw.solve(rho, z, yy)
         assert rel(xg, xr) <= TOL_NEWTON
         assert sg.cg_iters == sr["cg_iters"] and sg.fn_evals == sr["fn_evals"] and sg.flags == sr["flags"]
