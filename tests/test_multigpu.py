@@ -1,0 +1,74 @@
+"""Two ranks on two GPUs (one process per GPU, NCCL communicator bootstrapped over gloo): the
+consensus loop over the union of the ranks' shards must match the single-process loop over the same
+shards (the only data-path collective is the per-iteration allreduce). Needs >= 2
+GPUs; skipped otherwise."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+NODES, N, P, C, LAM = 4, 1200, 40, 5, 1e-3
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _data():
+    import paper_1807_07132_b200 as nadmm
+
+    Xtr, ytr, _, _ = nadmm.generate_synthetic(N, P, C, 2.0, 1.0, 3)
+    owner = nadmm.partition_owner(len(ytr), NODES)
+    return Xtr, ytr, owner
+
+
+def _cfg(nadmm, penalty):
+    return nadmm.AdmmConfig(n_workers=NODES, lam=LAM, penalty=nadmm.PenaltyPolicy(kind=penalty),
+                            stopping=nadmm.StoppingConfig(max_outer_iters=25))
+
+
+def _rank(rank, world, port, penalty, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1807_07132_b200 as nadmm
+        from paper_1807_07132_b200 import dist as nd
+
+        torch.cuda.set_device(rank)
+        ctx = nadmm.Context(rank)
+        Xtr, ytr, owner = _data()
+        mine = nd.node_range(NODES, world, rank)
+        shards = [nadmm.Dataset.dense(Xtr[owner == i], ytr[owner == i], C, ctx=ctx) for i in mine]
+        uid = nd.share_unique_id(dist, rank, nadmm.Communicator.unique_id)
+        comm = nadmm.Communicator(ctx, uid, world, rank)
+        res = nadmm.run_admm(shards, _cfg(nadmm, penalty), nadmm.EvalContext(eval_objective=True), comm)
+        out[rank] = {"z": res.z, "it": res.iterations, "conv": res.converged,
+                     "F": [r["train_objective"] for r in res.metrics]}
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("penalty", ["fixed", "spectral"])
+def test_two_ranks_match_single_process(nadmm, penalty):
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    out = mp.Manager().dict()
+    mp.start_processes(_rank, args=(2, _free_port(), penalty, out), nprocs=2, join=True, start_method="spawn")
+    Xtr, ytr, owner = _data()
+    ctx = nadmm.Context(0)
+    shards = [nadmm.Dataset.dense(Xtr[owner == i], ytr[owner == i], C, ctx=ctx) for i in range(NODES)]
+    ref = nadmm.run_admm(shards, _cfg(nadmm, penalty), nadmm.EvalContext(eval_objective=True))
+    for r in range(2):
+        assert out[r]["it"] == ref.iterations and out[r]["conv"] == ref.converged
+        np.testing.assert_allclose(out[r]["z"], ref.z, rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(out[r]["F"], [m["train_objective"] for m in ref.metrics], rtol=1e-9)
+    np.testing.assert_array_equal(out[0]["z"], out[1]["z"])  # every rank holds the same z
