@@ -389,7 +389,10 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
     const int valid_f = rem_f <= 0 ? 0 : (rem_f < fs ? (int)rem_f : fs);  // valid features in slice
     const uint32_t row_bytes = (uint32_t)valid_f * 8u;
 
-    for (int i = threadIdx.x; i < STAGES * BM * S; i += blockDim.x) xs[i] = 0.0;  // padding reads 0
+    // feature padding of a partial last slice is read by phase A and must be 0 (stale or uninitialised
+    // shared memory could hold NaN bit patterns); rows beyond n are masked where they are read instead
+    if (valid_f < fs)
+        for (int i = threadIdx.x; i < STAGES * BM * S; i += blockDim.x) xs[i] = 0.0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
@@ -778,9 +781,11 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                 if (warp == 0) DMMA_TRACE(i, 6);
                 const double* xt = xs + (size_t)stage * BM * S;
                 const double* utb = ut + (size_t)stage * BM * KS;
+                const int64_t rows_left = n - tile_of(i) * BM;  // rows of this tile beyond n read as 0
 #pragma unroll
                 for (int s = 0; s < BM / 4; ++s) {
                     const int row = 4 * s + tq;
+                    const bool rv = row < rows_left;
                     double ub[KT > 0 ? KT : 1], ur[R > 0 ? R : 1];
 #pragma unroll
                     for (int kt = 0; kt < KT; ++kt) ub[kt] = utb[row * KS + kt * 8 + gq];
@@ -789,7 +794,8 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                     const double* xr = xt + (size_t)row * S + fw;
 #pragma unroll
                     for (int mp = 0; mp < MT / 2; ++mp) {
-                        const double2 x2 = *reinterpret_cast<const double2*>(xr + mp * 16 + 2 * gq);
+                        const double2 x2 =
+                            rv ? *reinterpret_cast<const double2*>(xr + mp * 16 + 2 * gq) : make_double2(0.0, 0.0);
 #pragma unroll
                         for (int kt = 0; kt < KT; ++kt) {
                             dmma(accb[2 * mp][kt], x2.x, ub[kt]);
@@ -802,7 +808,7 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
                         }
                     }
                     if (MT & 1) {
-                        const double x = xr[(MT - 1) * 8 + gq];
+                        const double x = rv ? xr[(MT - 1) * 8 + gq] : 0.0;
 #pragma unroll
                         for (int kt = 0; kt < KT; ++kt) dmma(accb[MT - 1][kt], x, ub[kt]);
 #pragma unroll

@@ -17,7 +17,8 @@ TOL_NEWTON = 1e-10
 TOL_ADMM = 1e-9
 
 DENSE_SHAPES = [(50, 7, 4), (200, 33, 10), (129, 5, 2), (300, 28, 2), (1000, 784, 10), (96, 3072, 10), (77, 65, 21),
-                (64, 31, 3), (100, 60, 2), (3000, 28, 2)]
+                (64, 31, 3), (100, 60, 2), (3000, 28, 2),
+                (1003, 784, 10), (101, 3072, 10)]  # DMMA shapes with a partial last row tile
 
 
 def shards(nadmm, X, y, C):
@@ -124,7 +125,8 @@ def _cmp_trace(a, b):
         assert abs(ra.grad_norm - rb["grad_norm"]) <= 1e-8 * max(rb["grad_norm"], 1e-12)
 
 
-@pytest.mark.parametrize("n,p,C,lam", [(400, 20, 4, 1e-3), (2000, 784, 10, 1e-3), (300, 28, 2, 1e-3)])
+@pytest.mark.parametrize("n,p,C,lam", [(400, 20, 4, 1e-3), (2000, 784, 10, 1e-3), (300, 28, 2, 1e-3),
+                                        (1235, 784, 10, 1e-3)])
 def test_newton_single_node(nadmm, port, n, p, C, lam):
     Xtr, ytr, _, _ = port.generate_synthetic(n + n // 9 + 2, p, C, separation=3.0, noise=1.0, seed=1)
     ds, sh = shards(nadmm, Xtr, ytr, C)
