@@ -110,6 +110,7 @@ void alloc_work(Shard& s) {
     NADMM_CUDA(cudaMemcpyAsync(s.prm, s.prm_host, sizeof(DevParams), cudaMemcpyHostToDevice, s.ctx->stream));
     // pass implementations (the DMMA layout search times candidate passes on this shard's data)
     dmma_setup(s);
+    smallp_setup(s);
     gemm_setup(s);
     tail_setup(s);
 }

@@ -246,7 +246,7 @@ __host__ __device__ inline size_t dmma_smem_bytes(int stages, int bm, int nc, in
 // (cluster order) + lambda d (+ rho d), and the curvature / <r,r> reductions go through block slots
 // and software grid barriers (the grid is co-resident by construction). All blocks evaluate the same
 // scalars; block 0 / thread 0 writes the solver state.
-__device__ void dmma_cg_tail(const DmmaArgs& a, int K, int chunks, double* scratch, double* sc) {
+__device__ __forceinline__ void dmma_cg_tail(const DmmaArgs& a, int K, int chunks, double* scratch, double* sc) {
     const int it = a.cg_it;
     DevState* st = a.st;
     const int64_t d = (int64_t)K * a.p;

@@ -14,6 +14,7 @@
 // The row arithmetic is the SIMT rows_kernel's, in the same ascending class order.
 #include <algorithm>
 
+#include "dmma_kernel.cuh"  // mbarrier / bulk-copy helpers (dmma_detail)
 #include "state.h"
 
 namespace nadmm {
@@ -37,9 +38,18 @@ struct SmallArgs {
     const int32_t* guard;
 };
 
-template <int PT, int KT, int MODE>
+// RING: rows are streamed through a ring of kSpStages tiles of kSpThreads contiguous rows in shared
+// memory by one bulk copy each (needs ldx == p with 16-byte rows), so the bytes in flight per SM do
+// not depend on how many rows the registers let each thread hold; the grid is persistent. Otherwise
+// each thread loads its row straight from global memory.
+constexpr int kSpStages = 3;
+
+template <int PT, int KT, int MODE, bool RING>
 __global__ void __launch_bounds__(kSpThreads) smallp_kernel(SmallArgs a) {
+    using namespace dmma_detail;
     if (a.guard && !*a.guard) return;
+    extern __shared__ __align__(128) double ring[];  // kSpStages x kSpThreads x p (RING only)
+    __shared__ uint64_t bars[kSpStages];
     constexpr bool PHASE_B = (MODE == kModeHv || MODE == kModeCache);
     __shared__ double vs[PT][KT];
     __shared__ double red[kSpThreads / 32][PHASE_B ? PT * KT : 1];
@@ -57,20 +67,69 @@ __global__ void __launch_bounds__(kSpThreads) smallp_kernel(SmallArgs a) {
 #pragma unroll
         for (int c = 0; c < KT; ++c) acc[f][c] = 0.0;
     double loss = 0.0;
+    const int64_t ntiles = (n + kSpThreads - 1) / kSpThreads;
+    auto tile_bytes = [&](int64_t t) -> uint32_t {
+        const int64_t r0 = t * kSpThreads;
+        const int64_t rows = (n - r0) < kSpThreads ? (n - r0) : kSpThreads;
+        return (uint32_t)(rows * p * 8);
+    };
+    auto issue = [&](int64_t t, int st) {  // thread 0: bulk copy of tile t into stage st
+        const uint32_t bytes = tile_bytes(t);
+        mbar_expect_tx(&bars[st], bytes);
+        tma_bulk_g2s(ring + (size_t)st * kSpThreads * p, a.X + t * kSpThreads * p, bytes, &bars[st]);
+    };
+    if (RING) {
+        if (threadIdx.x == 0) {
+            for (int st = 0; st < kSpStages; ++st) mbar_init(&bars[st], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            fence_proxy_async();
+            for (int st = 0; st < kSpStages; ++st)
+                if (blockIdx.x + (int64_t)st * gridDim.x < ntiles) issue(blockIdx.x + (int64_t)st * gridDim.x, st);
+        }
+    }
     const int64_t stride = (int64_t)gridDim.x * kSpThreads;
-    for (int64_t i = (int64_t)blockIdx.x * kSpThreads + threadIdx.x; i < n; i += stride) {
+    int k = 0;
+    for (int64_t i0 = (int64_t)blockIdx.x * kSpThreads; i0 < n; i0 += stride, ++k) {
+        const int64_t i = i0 + threadIdx.x;
+        const int st = k % kSpStages;
         double x[PT];
-        const double* xr = a.X + i * a.ldx;
-        const bool vec = (a.ldx & 1) == 0;  // rows 16-byte aligned
+        if (RING) {
+            mbar_wait(&bars[st], (uint32_t)((k / kSpStages) & 1));
+            const double* xr = ring + ((size_t)st * kSpThreads + threadIdx.x) * p;
 #pragma unroll
-        for (int f = 0; f < PT; f += 2) {
-            if (vec && f + 1 < p) {
-                const double2 v = __ldg(reinterpret_cast<const double2*>(xr + f));
-                x[f] = v.x;
-                x[f + 1] = v.y;
-            } else {
-                x[f] = f < p ? __ldg(xr + f) : 0.0;
-                x[f + 1] = f + 1 < p ? __ldg(xr + f + 1) : 0.0;
+            for (int f = 0; f < PT; f += 2) {
+                if (f + 1 < p) {
+                    const double2 v = *reinterpret_cast<const double2*>(xr + f);
+                    x[f] = v.x;
+                    x[f + 1] = v.y;
+                } else {
+                    x[f] = f < p ? xr[f] : 0.0;
+                    x[f + 1] = 0.0;
+                }
+            }
+            __syncthreads();  // every row of stage st is in registers: refill it
+            if (threadIdx.x == 0 && i0 + (int64_t)kSpStages * stride < n) {
+                fence_proxy_async();
+                issue((i0 + (int64_t)kSpStages * stride) / kSpThreads, st);
+            }
+            if (i >= n) continue;
+        } else {
+            if (i >= n) continue;
+            const double* xr = a.X + i * a.ldx;
+            const bool vec = (a.ldx & 1) == 0;  // rows 16-byte aligned
+#pragma unroll
+            for (int f = 0; f < PT; f += 2) {
+                if (vec && f + 1 < p) {
+                    const double2 v = __ldg(reinterpret_cast<const double2*>(xr + f));
+                    x[f] = v.x;
+                    x[f + 1] = v.y;
+                } else {
+                    x[f] = f < p ? __ldg(xr + f) : 0.0;
+                    x[f + 1] = f + 1 < p ? __ldg(xr + f + 1) : 0.0;
+                }
             }
         }
         double lg[KT];
@@ -190,22 +249,53 @@ __global__ void __launch_bounds__(kSpThreads) smallp_kernel(SmallArgs a) {
     }
 }
 
-template <int PT, int KT>
-void launch_pt(Shard& s, PassMode mode, const SmallArgs& a, int grid) {
+template <int PT, int KT, bool RING>
+void launch_ring(Shard& s, PassMode mode, const SmallArgs& a, int grid, size_t smem) {
     cudaStream_t st = s.ctx->stream;
     switch (mode) {
-        case kModeCache: smallp_kernel<PT, KT, kModeCache><<<grid, kSpThreads, 0, st>>>(a); break;
-        case kModeHv: smallp_kernel<PT, KT, kModeHv><<<grid, kSpThreads, 0, st>>>(a); break;
-        case kModeLp: smallp_kernel<PT, KT, kModeLp><<<grid, kSpThreads, 0, st>>>(a); break;
-        case kModeValue: smallp_kernel<PT, KT, kModeValue><<<grid, kSpThreads, 0, st>>>(a); break;
-        case kModePredict: smallp_kernel<PT, KT, kModePredict><<<grid, kSpThreads, 0, st>>>(a); break;
+        case kModeCache: smallp_kernel<PT, KT, kModeCache, RING><<<grid, kSpThreads, smem, st>>>(a); break;
+        case kModeHv: smallp_kernel<PT, KT, kModeHv, RING><<<grid, kSpThreads, smem, st>>>(a); break;
+        case kModeLp: smallp_kernel<PT, KT, kModeLp, RING><<<grid, kSpThreads, smem, st>>>(a); break;
+        case kModeValue: smallp_kernel<PT, KT, kModeValue, RING><<<grid, kSpThreads, smem, st>>>(a); break;
+        case kModePredict: smallp_kernel<PT, KT, kModePredict, RING><<<grid, kSpThreads, smem, st>>>(a); break;
     }
 }
+
+template <int PT, int KT, bool RING>
+void set_ring_smem(size_t smem) {
+    for (auto k : {smallp_kernel<PT, KT, kModeCache, RING>, smallp_kernel<PT, KT, kModeHv, RING>,
+                   smallp_kernel<PT, KT, kModeLp, RING>, smallp_kernel<PT, KT, kModeValue, RING>,
+                   smallp_kernel<PT, KT, kModePredict, RING>})
+        NADMM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
+template <int PT, int KT>
+void launch_pt(Shard& s, PassMode mode, const SmallArgs& a, int grid, bool ring, size_t smem) {
+    if (ring)
+        launch_ring<PT, KT, true>(s, mode, a, grid, smem);
+    else
+        launch_ring<PT, KT, false>(s, mode, a, grid, 0);
+}
+
+// Ring staging is used for contiguous 16-byte rows whose kSpStages tiles fit in shared memory.
+size_t ring_smem(const Shard& s) { return (size_t)kSpStages * kSpThreads * s.p * sizeof(double); }
+bool ring_ok(const Shard& s) { return s.ldx == s.p && s.p % 2 == 0 && ring_smem(s) <= 200 * 1024; }
 
 }  // namespace
 
 bool smallp_supported(const Shard& s) {
     return !s.sparse && s.part && ((s.p <= 32 && s.K <= 2) || (s.p <= 64 && s.K == 1));
+}
+
+void smallp_setup(Shard& s) {  // once per shard, outside stream capture
+    if (!smallp_supported(s) || !ring_ok(s)) return;
+    const size_t smem = ring_smem(s);
+    if (s.p <= 32 && s.K == 1)
+        set_ring_smem<32, 1, true>(smem);
+    else if (s.p <= 32)
+        set_ring_smem<32, 2, true>(smem);
+    else
+        set_ring_smem<64, 1, true>(smem);
 }
 
 void smallp_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
@@ -229,14 +319,18 @@ void smallp_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard)
     a.blk = s.blk;
     a.guard = guard;
     const int64_t want = (s.n + kSpThreads - 1) / kSpThreads;
+    const bool ring = ring_ok(s);
+    // ring: one persistent block per SM (its ring is most of the SM's shared memory)
     const int grid = (int)std::max<int64_t>(
-        1, std::min<int64_t>({want, (int64_t)s.part_chunks, (int64_t)kBlockPartials, 2LL * s.ctx->num_sms}));
+        1, std::min<int64_t>({want, (int64_t)s.part_chunks, (int64_t)kBlockPartials,
+                              (ring ? 1LL : 2LL) * s.ctx->num_sms}));
+    const size_t smem = ring ? ring_smem(s) : 0;
     if (s.p <= 32 && s.K == 1)
-        launch_pt<32, 1>(s, mode, a, grid);
+        launch_pt<32, 1>(s, mode, a, grid, ring, smem);
     else if (s.p <= 32)
-        launch_pt<32, 2>(s, mode, a, grid);
+        launch_pt<32, 2>(s, mode, a, grid, ring, smem);
     else
-        launch_pt<64, 1>(s, mode, a, grid);
+        launch_pt<64, 1>(s, mode, a, grid, ring, smem);
     NADMM_LAUNCH_CHECK();
     s.rows_grid = grid;
     s.last_chunks = grid;

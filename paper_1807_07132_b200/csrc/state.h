@@ -224,6 +224,7 @@ int sparse_cols_pass(Shard& s, XtuKind kind, const double* vin, double* out, con
 
 // ---- small-p dense path (kernels_smallp.cu): p*(C-1) <= 64 ----
 bool smallp_supported(const Shard& s);
+void smallp_setup(Shard& s);
 void smallp_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
 // ---- GEMM path (kernels_gemm.cu): dense shards outside the fused passes' shapes ----
 void gemm_setup(Shard& s);
