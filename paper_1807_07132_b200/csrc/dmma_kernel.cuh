@@ -219,10 +219,14 @@ constexpr int kDmmaChains = NADMM_DMMA_CHAINS;  // phase-A accumulator chains pe
 #define NADMM_DMMA_BULK_PUSH 1
 #endif
 constexpr bool kDmmaBulkPush = NADMM_DMMA_BULK_PUSH;  // exchange by bulk smem->peer copies (else st.async)
-constexpr int kDmmaRecvBufs = NADMM_DMMA_RECV_BUFS;  // receive buffers per CTA, flow-controlled by remote credits
+constexpr int kDmmaRecvBufs = NADMM_DMMA_RECV_BUFS;
+// Up to 8 compute warps per CTA (2 per SM sub-partition). Measured: 16 narrow (MT = 4) warps per
+// CTA spill under the 102-register cap and run 30-50 % slower on the CIFAR shapes.
+__host__ __device__ constexpr int dmma_max_compute(int) { return 8; }  // receive buffers per CTA, flow-controlled by remote credits
 constexpr int kDmmaRedBufs = 2;   // compute-warp partial buffers (pusher frees them)
 constexpr int kDmmaEpiWarps = 2;  // epilogue warps
 constexpr int kDmmaAux = kDmmaEpiWarps + 2;  // + pusher + producer
+__host__ __device__ constexpr int dmma_max_threads(int mt) { return 32 * (dmma_max_compute(mt) + kDmmaAux); }
 
 template <int K>
 struct DmmaSmem {
@@ -338,7 +342,7 @@ __device__ __forceinline__ void dmma_cg_tail(const DmmaArgs& a, int K, int chunk
 // LAG: tiles of phase A in flight ahead of phase B; STAGES >= LAG + 2 ring slots (the LAG tiles
 // waiting for phase B, the one in phase A, and the ones loading).
 template <int MT, int KT, int R, int BM, int LAG, int STAGES, int MODE>
-__global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
+__global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_pass_kernel(DmmaArgs a) {
     using namespace dmma_detail;
     static_assert(STAGES >= LAG + 2, "ring depth");
     constexpr int K = 8 * KT + R;
@@ -468,25 +472,51 @@ __global__ void __launch_bounds__(384, 1) dmma_pass_kernel(DmmaArgs a) {
             DMMA_TRACE(i, 2);
             // every CTA of the cluster released receive buffer br (its previous tile's epilogue is done)
             if (i >= kDmmaRecvBufs) mbar_wait(&credit[br], (uint32_t)(((i / kDmmaRecvBufs) - 1) & 1));
+            DMMA_TRACE(i, 13);
             const double* rd = red + (size_t)b * nc * PART;
             const uint32_t dst_local = smem_u32(recv + ((size_t)br * csize + crank) * PART);
             const uint32_t bar_local = smem_u32(&rbar[br]);
-            for (int i2 = lane; i2 < PART / 2; i2 += 32) {
-                double v0[8], v1[8];
+            // all of this lane's pairs are loaded first and their trees summed together: independent
+            // chains hide the FP64 pipe's latency under the compute warps' DMMAs
+            constexpr int NPAIR = (PART / 2 + 31) / 32;
+            double s0[NPAIR], s1[NPAIR];
 #pragma unroll
-                for (int w = 0; w < 8; ++w) {
-                    double2 v = make_double2(0.0, 0.0);
-                    if (w < nc) v = *reinterpret_cast<const double2*>(rd + (size_t)w * PART + 2 * i2);
-                    v0[w] = v.x;
-                    v1[w] = v.y;
+            for (int j = 0; j < NPAIR; ++j) s0[j] = s1[j] = 0.0;
+            constexpr int NGRP = (dmma_max_compute(MT) + 7) / 8;
+#pragma unroll
+            for (int gw = 0; gw < NGRP; ++gw) {  // groups of 8 warps, each summed as a fixed tree
+                const int w0 = 8 * gw;
+                if (w0 >= nc) break;
+                double v0[NPAIR][8], v1[NPAIR][8];
+#pragma unroll
+                for (int j = 0; j < NPAIR; ++j) {
+                    const int i2 = lane + 32 * j;
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) {
+                        double2 v = make_double2(0.0, 0.0);
+                        if (w0 + w < nc && i2 < PART / 2)
+                            v = *reinterpret_cast<const double2*>(rd + (size_t)(w0 + w) * PART + 2 * i2);
+                        v0[j][w] = v.x;
+                        v1[j][w] = v.y;
+                    }
                 }
-                const double s0 = tree_sum(v0, nc), s1 = tree_sum(v1, nc);
+#pragma unroll
+                for (int j = 0; j < NPAIR; ++j) {
+                    s0[j] = s0[j] + tree_sum(v0[j], nc - w0);
+                    s1[j] = s1[j] + tree_sum(v1[j], nc - w0);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < NPAIR; ++j) {
+                const int i2 = lane + 32 * j;
+                if (i2 >= PART / 2) continue;
                 if (kDmmaBulkPush)
-                    *reinterpret_cast<double2*>(sendb + (size_t)br * PART + 2 * i2) = make_double2(s0, s1);
+                    *reinterpret_cast<double2*>(sendb + (size_t)br * PART + 2 * i2) = make_double2(s0[j], s1[j]);
                 else
                     for (uint32_t q = 0; q < csize; ++q)
-                        st_async_v2(mapa(dst_local + 16u * i2, q), s0, s1, mapa(bar_local, q));
+                        st_async_v2(mapa(dst_local + 16u * i2, q), s0[j], s1[j], mapa(bar_local, q));
             }
+            DMMA_TRACE(i, 14);
             if (kDmmaBulkPush) {
                 // the summed partial goes to every peer as one bulk copy each (lane q -> CTA q); the
                 // send buffer br is rewritten only after every peer returned its credit for br

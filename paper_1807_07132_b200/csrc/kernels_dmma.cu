@@ -76,7 +76,7 @@ std::vector<Layout> candidate_layouts(int64_t p, int K) {
             for (int cs = 1; cs <= 8; ++cs) {
                 const int W = 8 * mt;
                 const int nw = (int)((p + (int64_t)cs * W - 1) / ((int64_t)cs * W));
-                if (nw < 2 || nw > 8) continue;  // compute warps; + kDmmaAux exchange/producer warps
+                if (nw < 2 || nw > dmma_max_compute(mt)) continue;  // compute warps (+ kDmmaAux aux warps)
                 const int fs = nw * W;
                 const double waste = (double)cs * fs / (double)p - 1.0;
                 if (waste > 0.15) continue;

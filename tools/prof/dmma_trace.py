@@ -30,6 +30,6 @@ d = np.diff(t[4:40, 7])
 print("steady cycles per tile (B done to B done):", float(np.median(d)))
 for a, b, nm in [(1, 2, "A done -> pusher got"), (2, 3, "push time"), (3, 4, "push done -> rbar"), (4, 5, "epilogue"),
                  (5, 6, "epi done -> B start (same tile)"), (6, 7, "B time"), (0, 1, "A time"),
-                 (4, 8, "epi: full wait"), (8, 9, "epi: pass1"), (9, 10, "epi: bar1"), (10, 11, "epi: credits"),
-                 (11, 12, "epi: pass2"), (12, 13, "epi: bar2"), (13, 5, "epi: tail")]:
+                 (4, 8, "epi: full wait"), (8, 9, "epi: pass1"), (9, 11, "epi: credits"), (11, 12, "epi: pass2"),
+                 (2, 13, "push: credit wait"), (13, 14, "push: partial sums"), (14, 3, "push: bulk copies")]:
     print(f"{nm:32s} median {float(np.median(t[4:40, b] - t[4:40, a])):9.0f} cycles")
