@@ -81,6 +81,15 @@ def main(cfgs):
         report("cfg4", f"CSR {n}x{p} nnz/row={nnz_row} C={C1}", time_hv(ds, 5), sparse_bytes(n, p, C1 - 1, nnz),
                4 * nnz * (C1 - 1))
         ds.close()
+    if "5full" in cfgs:
+        n, p, C1 = 500000, 2048, 100  # the full per-GPU cfg5 shard (8.2 GB of X)
+        X = np.empty((n, p))
+        for r0 in range(0, n, 50000):
+            X[r0:r0 + 50000] = rng.normal(size=(min(50000, n - r0), p)) / 45
+        ds = nadmm.Dataset.dense(X, (np.arange(n) % C1 + 1).astype(np.int32), C1, ctx=ctx)
+        del X
+        report("cfg5", f"dense {n}x{p} C={C1}", time_hv(ds, 3), dense_bytes(n, p, C1 - 1), 4 * n * p * (C1 - 1))
+        ds.close()
     if "5" in cfgs:
         n, p, C1 = 125000, 2048, 100  # a quarter of the 500,000-row cfg5 shard (time scales with n)
         X = rng.normal(size=(n, p)) / 45
