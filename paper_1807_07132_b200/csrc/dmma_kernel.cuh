@@ -223,7 +223,10 @@ constexpr int kDmmaRecvBufs = NADMM_DMMA_RECV_BUFS;
 // Up to 8 compute warps per CTA (2 per SM sub-partition). Measured: 16 narrow (MT = 4) warps per
 // CTA spill under the 102-register cap and run 30-50 % slower on the CIFAR shapes.
 __host__ __device__ constexpr int dmma_max_compute(int) { return 8; }  // receive buffers per CTA, flow-controlled by remote credits
-constexpr int kDmmaRedBufs = 2;   // compute-warp partial buffers (pusher frees them)
+#ifndef NADMM_DMMA_RED_BUFS
+#define NADMM_DMMA_RED_BUFS 2
+#endif
+constexpr int kDmmaRedBufs = NADMM_DMMA_RED_BUFS;  // compute-warp partial buffers (pusher frees them)
 constexpr int kDmmaEpiWarps = 2;  // epilogue warps
 constexpr int kDmmaAux = kDmmaEpiWarps + 2;  // + pusher + producer
 __host__ __device__ constexpr int dmma_max_threads(int mt) { return 32 * (dmma_max_compute(mt) + kDmmaAux); }
