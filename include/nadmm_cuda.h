@@ -253,6 +253,23 @@ nadmm_status nadmm_generate_sparse(int64_t n, int64_t p, int32_t C, int32_t nnz_
 /* partition (src/data_io.cpp:300-328): owner[i] = worker of row i. */
 nadmm_status nadmm_partition(int64_t n, int32_t n_workers, int32_t strided, int32_t* owner);
 
+/* Real-data readers feeding nadmm_shard_csr / nadmm_shard_dense (host-only).
+ * load_libsvm (src/data_io.cpp:85-137): parse, then fetch into caller buffers of the reported
+ * sizes (indptr n+1, indices/vals nnz, labels n, label_values C), then free. Rows are canonical
+ * (columns ascending, duplicates summed); labels remapped to 1..C in ascending value order
+ * (src/data_io.cpp:51-66). Errors: unreadable file NADMM_ECONFIG, malformed content NADMM_EDATA. */
+typedef struct nadmm_libsvm_s* nadmm_libsvm;
+nadmm_status nadmm_libsvm_parse(const char* path, nadmm_libsvm* out, int64_t* n, int64_t* p, int64_t* nnz,
+                                int32_t* C);
+nadmm_status nadmm_libsvm_fetch(nadmm_libsvm h, int64_t* indptr, int32_t* indices, double* vals, int32_t* labels,
+                                double* label_values);
+void nadmm_libsvm_free(nadmm_libsvm h);
+/* load_idx (src/data_io.cpp:220-271): n images of p pixels; X (n x p) scaled to [0,1], labels
+ * digit+1, C = max digit + 1, label_values 0..C-1 (up to 256 entries). */
+nadmm_status nadmm_idx_info(const char* images, const char* labels, int64_t* n, int64_t* p);
+nadmm_status nadmm_idx_load(const char* images, const char* labels, double* X, int32_t* y, int32_t* C,
+                            double* label_values);
+
 #ifdef __cplusplus
 }
 #endif

@@ -106,13 +106,46 @@ class Dataset {
     int64_t cols() const { return p_; }
     int32_t num_classes() const { return C_; }
     int64_t weight_dim() const { return (int64_t)(C_ - 1) * p_; }  // d = (C-1) p, block-major
+    // original label values in class order (inc/dataset.hpp:46-50); set by the readers below
+    const Vector& label_values() const { return label_values_; }
+    void set_label_values(Vector v) { label_values_ = std::move(v); }
 
   private:
     Dataset(nadmm_shard h, int64_t n, int64_t p, int32_t C) : h_(h), n_(n), p_(p), C_(C) {}
     nadmm_shard h_ = nullptr;
     int64_t n_, p_;
     int32_t C_;
+    Vector label_values_;
 };
+
+// ---- readers (inc/nadmm/data_io.hpp:52-65): load_libsvm -> sparse shard, load_idx -> dense ----
+inline std::shared_ptr<Dataset> load_libsvm(const Context& ctx, const std::string& path) {
+    nadmm_libsvm h = nullptr;
+    int64_t n = 0, p = 0, nnz = 0;
+    int32_t C = 0;
+    check(nadmm_libsvm_parse(path.c_str(), &h, &n, &p, &nnz, &C));
+    std::unique_ptr<nadmm_libsvm_s, void (*)(nadmm_libsvm)> guard(h, nadmm_libsvm_free);
+    std::vector<int64_t> indptr((size_t)n + 1);
+    std::vector<int32_t> indices((size_t)nnz), labels((size_t)n);
+    Vector vals((size_t)nnz), values((size_t)C);
+    check(nadmm_libsvm_fetch(h, indptr.data(), indices.data(), vals.data(), labels.data(), values.data()));
+    auto ds = Dataset::sparse(ctx, indptr, indices, vals, p, labels, C);
+    ds->set_label_values(std::move(values));
+    return ds;
+}
+
+inline std::shared_ptr<Dataset> load_idx(const Context& ctx, const std::string& images, const std::string& labels) {
+    int64_t n = 0, p = 0;
+    check(nadmm_idx_info(images.c_str(), labels.c_str(), &n, &p));
+    Vector X((size_t)(n * p)), values(256);
+    std::vector<int32_t> y((size_t)n);
+    int32_t C = 0;
+    check(nadmm_idx_load(images.c_str(), labels.c_str(), X.data(), y.data(), &C, values.data()));
+    values.resize((size_t)C);
+    auto ds = Dataset::dense(ctx, X, n, p, y, C);
+    ds->set_label_values(std::move(values));
+    return ds;
+}
 
 // ---- model level (src/softmax.cpp:51-153), memoised on w like SoftmaxMemo ----
 inline double loss(const Dataset& ds, const Vector& w, double lambda) {

@@ -440,6 +440,38 @@ class Ref:
             _dp(Xtr), _ip(ytr), _dp(Xte), _ip(yte)))
         return Xtr, ytr, Xte, yte
 
+    def _loaded(self, h) -> dict:
+        """Copy a Dataset returned by the reference's readers out of the heap handle."""
+        try:
+            n, p, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+            c, sp = C.c_int(), C.c_int()
+            self._chk(self.lib.nadmm_ref_dataset_info(h, C.byref(n), C.byref(p), C.byref(nnz), C.byref(c), C.byref(sp)))
+            out = dict(n=n.value, p=p.value, C=c.value, labels=np.zeros(n.value, dtype=np.int32),
+                       label_values=np.zeros(c.value))
+            if sp.value:
+                out.update(indptr=np.zeros(n.value + 1, dtype=np.int64), indices=np.zeros(nnz.value, dtype=np.int32),
+                           vals=np.zeros(nnz.value))
+                self._chk(self.lib.nadmm_ref_dataset_fetch(h, _lp(out["indptr"]), _ip(out["indices"]),
+                                                           _dp(out["vals"]), _ip(out["labels"]),
+                                                           _dp(out["label_values"])))
+            else:
+                out["X"] = np.zeros((n.value, p.value))
+                self._chk(self.lib.nadmm_ref_dataset_fetch(h, None, None, _dp(out["X"]), _ip(out["labels"]),
+                                                           _dp(out["label_values"])))
+            return out
+        finally:
+            self.lib.nadmm_ref_dataset_free(h)
+
+    def load_libsvm(self, path) -> dict:
+        h = VP()
+        self._chk(self.lib.nadmm_ref_load_libsvm(str(path).encode(), C.byref(h)))
+        return self._loaded(h)
+
+    def load_idx(self, images, labels) -> dict:
+        h = VP()
+        self._chk(self.lib.nadmm_ref_load_idx(str(images).encode(), str(labels).encode(), C.byref(h)))
+        return self._loaded(h)
+
     def partition_owner(self, n, n_workers, strided=False):
         out = np.zeros(n, dtype=np.int32)
         self._chk(self.lib.nadmm_ref_partition(C.c_int64(n), C.c_int(n_workers), C.c_int(int(strided)), _ip(out)))

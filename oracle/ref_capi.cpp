@@ -382,4 +382,46 @@ int nadmm_ref_rng_stream(std::uint64_t seed, int kind, std::uint64_t bound, std:
     });
 }
 
+// ---- real-data readers (src/data_io.cpp:85-137 load_libsvm, 220-271 load_idx) ----
+// The loaded Dataset stays on the heap behind an opaque handle; info + fetch copy it out.
+int nadmm_ref_load_libsvm(const char* path, void** out) {
+    return guard([&] { *out = new Dataset(load_libsvm(path)); });
+}
+
+int nadmm_ref_load_idx(const char* images, const char* labels, void** out) {
+    return guard([&] { *out = new Dataset(load_idx(images, labels)); });
+}
+
+int nadmm_ref_dataset_info(void* h, std::int64_t* n, std::int64_t* p, std::int64_t* nnz, int* C, int* is_sparse) {
+    return guard([&] {
+        const Dataset& ds = *static_cast<Dataset*>(h);
+        *n = ds.n();
+        *p = ds.p();
+        *nnz = ds.is_sparse() ? static_cast<std::int64_t>(ds.sparse_features().nonZeros()) : ds.n() * ds.p();
+        *C = ds.num_classes();
+        *is_sparse = ds.is_sparse() ? 1 : 0;
+    });
+}
+
+// Sparse: indptr (n+1, widened to int64), indices (nnz), vals (nnz). Dense: vals = X (n x p).
+int nadmm_ref_dataset_fetch(void* h, std::int64_t* indptr, std::int32_t* indices, double* vals, std::int32_t* labels,
+                            double* label_values) {
+    return guard([&] {
+        const Dataset& ds = *static_cast<Dataset*>(h);
+        if (ds.is_sparse()) {
+            const auto& S = ds.sparse_features();
+            for (Index i = 0; i <= ds.n(); ++i) indptr[i] = S.outerIndexPtr()[i];
+            const auto nnz = static_cast<std::size_t>(S.nonZeros());
+            for (std::size_t k = 0; k < nnz; ++k) indices[k] = S.innerIndexPtr()[k];
+            std::memcpy(vals, S.valuePtr(), sizeof(double) * nnz);
+        } else {
+            std::memcpy(vals, ds.dense_features().data(), sizeof(double) * static_cast<std::size_t>(ds.n() * ds.p()));
+        }
+        std::memcpy(labels, ds.labels().data(), sizeof(std::int32_t) * static_cast<std::size_t>(ds.n()));
+        const auto& lv = ds.label_values();
+        if (!lv.empty()) std::memcpy(label_values, lv.data(), sizeof(double) * lv.size());
+    });
+}
+
 }  // extern "C"
+

@@ -29,7 +29,8 @@ __all__ = [
     "weight_blocks", "Objective", "make_softmax_objective", "make_augmented_objective", "NewtonConfig",
     "NewtonIterRecord", "NewtonResult", "newton_solve", "InnerStats", "Worker", "PenaltyPolicy", "StoppingConfig",
     "AdmmConfig", "EvalContext", "AdmmRunResult", "run_admm", "Communicator", "generate_synthetic",
-    "generate_sparse", "partition_owner", "partition", "mix_seed", "default_context",
+    "generate_sparse", "partition_owner", "partition", "mix_seed", "default_context", "LoadedData", "read_libsvm",
+    "read_idx", "load_libsvm", "load_idx",
 ]
 
 
@@ -146,6 +147,7 @@ class Dataset:
         self.handle, self.ctx = handle, ctx
         self._n, self._p, self._C, self._sparse = n, p, C_, sparse
         self._labels = labels
+        self._label_values = np.zeros(0)
 
     @staticmethod
     def dense(features, labels, num_classes: int, ctx: Optional[Context] = None) -> "Dataset":
@@ -194,6 +196,14 @@ class Dataset:
 
     def labels(self) -> np.ndarray:
         return self._labels
+
+    def label_values(self) -> np.ndarray:
+        """Original label values in class order: label_values()[c-1] is class c's (inc/dataset.hpp:46-50);
+        empty unless the dataset came from a reader."""
+        return self._label_values
+
+    def set_label_values(self, values) -> None:
+        self._label_values = np.asarray(values, dtype=np.float64).copy()
 
     def device_bytes(self) -> int:
         return int(L.lib().nadmm_shard_device_bytes(self.handle))
@@ -607,6 +617,78 @@ def generate_sparse(n: int, p: int, num_classes: int, nnz_per_row: int, seed: in
     _check(L.lib().nadmm_generate_sparse(n, p, num_classes, nnz_per_row, seed, _lp(indptr), _ip(indices), _dp(vals),
                                          _ip(labels)), data=True)
     return indptr, indices, vals, labels
+
+
+# ---- real-data readers (src/data_io.cpp:85-137, 220-271) -----------------------------------------
+@dataclass
+class LoadedData:
+    """A file read into host arrays, before it becomes a device shard. Sparse files fill the CSR
+    triple (canonical rows: columns ascending, duplicates summed); dense files fill X (n x p)."""
+    n: int
+    p: int
+    num_classes: int
+    labels: np.ndarray
+    label_values: np.ndarray
+    indptr: Optional[np.ndarray] = None
+    indices: Optional[np.ndarray] = None
+    vals: Optional[np.ndarray] = None
+    X: Optional[np.ndarray] = None
+
+    @property
+    def sparse(self) -> bool:
+        return self.X is None
+
+    def to_device(self, ctx: Optional[Context] = None) -> "Dataset":
+        if self.sparse:
+            ds = Dataset.sparse(self.indptr, self.indices, self.vals, self.labels, self.num_classes, self.p, ctx=ctx)
+        else:
+            ds = Dataset.dense(self.X, self.labels, self.num_classes, ctx=ctx)
+        ds.set_label_values(self.label_values)
+        return ds
+
+
+def read_libsvm(path) -> LoadedData:
+    """LIBSVM text ("label idx:val ...", 1-based) -> host CSR, labels remapped to 1..C ascending.
+    Same errors as the reference's load_libsvm: ConfigError (cannot open, < 2 classes, p = 0),
+    DataError (non-integer label, malformed token, 0-based index, no rows, non-finite value)."""
+    lib = L.lib()
+    h = C.c_void_p()
+    n, p, nnz, c = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
+    _check(lib.nadmm_libsvm_parse(str(path).encode(), C.byref(h), C.byref(n), C.byref(p), C.byref(nnz), C.byref(c)),
+           data=True)
+    try:
+        out = LoadedData(n.value, p.value, c.value, np.empty(n.value, dtype=np.int32), np.empty(c.value),
+                         indptr=np.empty(n.value + 1, dtype=np.int64), indices=np.empty(nnz.value, dtype=np.int32),
+                         vals=np.empty(nnz.value))
+        _check(lib.nadmm_libsvm_fetch(h, _lp(out.indptr), _ip(out.indices), _dp(out.vals), _ip(out.labels),
+                                      _dp(out.label_values)), data=True)
+        return out
+    finally:
+        lib.nadmm_libsvm_free(h)
+
+
+def read_idx(images, labels) -> LoadedData:
+    """IDX image (0x803) + label (0x801) files -> host dense X in [0, 1], labels digit + 1."""
+    lib = L.lib()
+    n, p = C.c_int64(), C.c_int64()
+    ib, lb = str(images).encode(), str(labels).encode()
+    _check(lib.nadmm_idx_info(ib, lb, C.byref(n), C.byref(p)), data=True)
+    X = np.empty((n.value, p.value))
+    y = np.empty(n.value, dtype=np.int32)
+    lv = np.empty(256)
+    c = C.c_int32()
+    _check(lib.nadmm_idx_load(ib, lb, _dp(X), _ip(y), C.byref(c), _dp(lv)), data=True)
+    return LoadedData(n.value, p.value, c.value, y, lv[:c.value].copy(), X=X)
+
+
+def load_libsvm(path, ctx: Optional[Context] = None) -> "Dataset":
+    """load_libsvm (inc/nadmm/data_io.hpp:52-57): the file as a device-resident sparse Dataset."""
+    return read_libsvm(path).to_device(ctx)
+
+
+def load_idx(images, labels, ctx: Optional[Context] = None) -> "Dataset":
+    """load_idx (inc/nadmm/data_io.hpp:63-65): MNIST-style IDX files as a device-resident dense Dataset."""
+    return read_idx(images, labels).to_device(ctx)
 
 
 def partition_owner(n: int, n_workers: int, strided: bool = False) -> np.ndarray:

@@ -109,6 +109,11 @@ SIGNATURES = {
                                      D, I32]),
     "nadmm_generate_sparse": (S, [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_uint64, I64, I32, D, I32]),
     "nadmm_partition": (S, [C.c_int64, C.c_int32, C.c_int32, I32]),
+    "nadmm_libsvm_parse": (S, [C.c_char_p, C.POINTER(VP), I64, I64, I64, I32]),
+    "nadmm_libsvm_fetch": (S, [VP, I64, I32, D, I32, D]),
+    "nadmm_libsvm_free": (None, [VP]),
+    "nadmm_idx_info": (S, [C.c_char_p, C.c_char_p, I64, I64]),
+    "nadmm_idx_load": (S, [C.c_char_p, C.c_char_p, D, I32, I32, D]),
 }
 
 _lib = None
