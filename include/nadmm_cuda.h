@@ -150,6 +150,34 @@ nadmm_status nadmm_newton_solve(nadmm_shard shard, const nadmm_newton_cfg* cfg, 
                                 double rho, const double* z, const double* y, double* x_inout,
                                 nadmm_newton_iter* trace, int32_t trace_cap, nadmm_newton_summary* out);
 
+/* L-BFGS inner solver: lbfgs_solve (src/lbfgs.cpp:94-181) with the strong-Wolfe
+ * bracket-and-zoom search (src/lbfgs.cpp:40-90), on the same objectives as nadmm_newton_solve. */
+typedef struct {                  /* LbfgsConfig (inc/lbfgs.hpp:9-18) */
+    int32_t history;              /* 25 (device limit 256) */
+    double wolfe_c1;              /* 1e-4 */
+    double wolfe_c2;              /* 0.9 */
+    int32_t max_iters;            /* 100 */
+    int32_t ls_max_iters;         /* 20 */
+    double grad_tol;              /* 1e-8 */
+} nadmm_lbfgs_cfg;
+
+typedef struct {                  /* LbfgsIterRecord (inc/lbfgs.hpp:20-27) */
+    int32_t iter;
+    double grad_norm;
+    double step;
+    double objective;
+    int32_t fn_evals;
+    int32_t ls_fallback;
+} nadmm_lbfgs_iter;
+
+void nadmm_lbfgs_cfg_default(nadmm_lbfgs_cfg* cfg);
+
+/* x_inout: x0 in, LbfgsResult::x out; `out` carries converged / final_grad_norm / trace length.
+ * Errors as the reference: invalid config NADMM_ECONFIG, non-finite objective NADMM_ESOLVER. */
+nadmm_status nadmm_lbfgs_solve(nadmm_shard shard, const nadmm_lbfgs_cfg* cfg, double lambda, int32_t augmented,
+                               double rho, const double* z, const double* y, double* x_inout,
+                               nadmm_lbfgs_iter* trace, int32_t trace_cap, nadmm_newton_summary* out);
+
 /* ------------------------------------------------------------------------------------------ */
 /* Worker level -- run_worker ADMM branch (src/worker.cpp:127-196)                              */
 /* ------------------------------------------------------------------------------------------ */

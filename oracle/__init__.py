@@ -539,6 +539,23 @@ class RefDataset:
             _dp(_cfg(cfg)), _dp(x), _dp(tr), C.c_int(trace_cap), C.byref(nt), C.byref(conv), C.byref(gn)))
         return dict(x=x, trace=_trace_rows(tr, nt.value), converged=bool(conv.value), final_grad_norm=gn.value)
 
+    def lbfgs_solve(self, lam, x0, cfg=(25, 1e-4, 0.9, 100, 20, 1e-8), rho=None, z=None, y=None, trace_cap=1024):
+        """The reference's lbfgs_solve (src/lbfgs.cpp:94-181); cfg = (history, c1, c2, max_iters,
+        ls_max_iters, grad_tol)."""
+        d = self.sh.d
+        x = np.zeros(d)
+        tr = np.zeros((trace_cap, 6))
+        nt, conv, gn = C.c_int(), C.c_int(), C.c_double()
+        aug = rho is not None
+        zz = _f64(z if aug else np.zeros(d))
+        yy = _f64(y if aug else np.zeros(d))
+        self.ref._chk(self.ref.lib.nadmm_ref_lbfgs_solve(
+            self.h, C.c_double(lam), C.c_int(int(aug)), C.c_double(rho or 0.0), _dp(zz), _dp(yy), _dp(_f64(x0)),
+            _dp(_f64(cfg)), _dp(x), _dp(tr), C.c_int(trace_cap), C.byref(nt), C.byref(conv), C.byref(gn)))
+        keys = ("iter", "grad_norm", "step", "objective", "fn_evals", "ls_fallback")
+        rows = [dict(zip(keys, r.tolist())) for r in tr[: min(nt.value, trace_cap)]]
+        return dict(x=x, trace=rows, converged=bool(conv.value), final_grad_norm=gn.value)
+
     def worker(self) -> "RefWorker":
         h = VP()
         self.ref._chk(self.ref.lib.nadmm_ref_worker_create(self.h, C.byref(h)))

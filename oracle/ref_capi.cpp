@@ -312,9 +312,10 @@ int nadmm_ref_newton_solve_cb(nadmm_ref_value_fn value, nadmm_ref_grad_fn grad, 
 }
 
 // L-BFGS inner solver (SURVEY §8f "next" #1): lcfg = history, c1, c2, max_iters, ls_max_iters, grad_tol.
+// trace rows (doubles): iter, grad_norm, step, objective, fn_evals, ls_fallback.
 int nadmm_ref_lbfgs_solve(void* ds, double lambda, int augmented, double rho, const double* z, const double* y,
-                          const double* x0, const double* lcfg, double* x_out, int* iters, int* converged,
-                          double* final_grad_norm, double* final_objective) {
+                          const double* x0, const double* lcfg, double* x_out, double* trace, int trace_cap,
+                          int* iters, int* converged, double* final_grad_norm) {
     return guard([&] {
         auto data = std::make_shared<const Dataset>(*static_cast<Dataset*>(ds));
         const Index d = data->weight_dim();
@@ -329,10 +330,20 @@ int nadmm_ref_lbfgs_solve(void* ds, double lambda, int augmented, double rho, co
         c.grad_tol = lcfg[5];
         LbfgsResult r = lbfgs_solve(obj, vec_from(x0, d), c);
         vec_to(r.x, x_out);
+        int k = 0;
+        for (const auto& t : r.trace) {
+            if (k >= trace_cap) break;
+            double* row = trace + 6 * k++;
+            row[0] = t.iter;
+            row[1] = t.grad_norm;
+            row[2] = t.step;
+            row[3] = t.objective;
+            row[4] = t.fn_evals;
+            row[5] = t.ls_fallback ? 1.0 : 0.0;
+        }
         *iters = static_cast<int>(r.trace.size());
         *converged = r.converged ? 1 : 0;
         *final_grad_norm = r.final_grad_norm;
-        *final_objective = r.trace.empty() ? obj.value(r.x) : r.trace.back().objective;
     });
 }
 

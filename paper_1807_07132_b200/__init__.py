@@ -30,7 +30,7 @@ __all__ = [
     "NewtonIterRecord", "NewtonResult", "newton_solve", "InnerStats", "Worker", "PenaltyPolicy", "StoppingConfig",
     "AdmmConfig", "EvalContext", "AdmmRunResult", "run_admm", "Communicator", "generate_synthetic",
     "generate_sparse", "partition_owner", "partition", "mix_seed", "default_context", "LoadedData", "read_libsvm",
-    "read_idx", "load_libsvm", "load_idx",
+    "read_idx", "load_libsvm", "load_idx", "LbfgsConfig", "LbfgsIterRecord", "LbfgsResult", "lbfgs_solve",
 ]
 
 
@@ -393,6 +393,59 @@ def newton_solve(obj: Objective, x0, cfg: Optional[NewtonConfig] = None) -> Newt
     recs = [NewtonIterRecord(r.iter, r.grad_norm, r.step, r.cg_iters, r.cg_residual, r.objective, bool(r.ls_capped),
                              bool(r.cg_fallback), r.fn_evals) for r in tr[: min(summ.iterations, cap)]]
     return NewtonResult(x, recs, bool(summ.converged), summ.final_grad_norm)
+
+
+# ---- L-BFGS (inc/lbfgs.hpp; src/lbfgs.cpp) ---------------------------------------------------------
+@dataclass
+class LbfgsConfig:  # inc/lbfgs.hpp:9-18
+    history: int = 25
+    wolfe_c1: float = 1e-4
+    wolfe_c2: float = 0.9
+    max_iters: int = 100
+    ls_max_iters: int = 20
+    grad_tol: float = 1e-8
+
+    def to_c(self) -> L.LbfgsCfg:
+        return L.LbfgsCfg(self.history, self.wolfe_c1, self.wolfe_c2, self.max_iters, self.ls_max_iters,
+                          self.grad_tol)
+
+
+@dataclass
+class LbfgsIterRecord:  # inc/lbfgs.hpp:20-27
+    iter: int = 0
+    grad_norm: float = 0.0
+    step: float = 0.0
+    objective: float = 0.0
+    fn_evals: int = 0
+    ls_fallback: bool = False
+
+
+@dataclass
+class LbfgsResult:  # inc/lbfgs.hpp:29-34
+    x: np.ndarray
+    trace: list
+    converged: bool = False
+    final_grad_norm: float = 0.0
+
+
+def lbfgs_solve(obj: Objective, x0, cfg: Optional[LbfgsConfig] = None) -> LbfgsResult:
+    """Limited-memory BFGS with the strong-Wolfe search (src/lbfgs.cpp:94-181) on the device."""
+    cfg = cfg or LbfgsConfig()
+    if not isinstance(obj, Objective):
+        raise ConfigError("the device lbfgs_solve takes a softmax Objective (make_softmax_objective)")
+    data = obj.data
+    x = _wvec(data, x0, "x0").copy()
+    cap = max(1, min(cfg.max_iters, 1 << 16))
+    tr = (L.LbfgsIter * cap)()
+    summ = L.NewtonSummary()
+    c = cfg.to_c()
+    z = obj.z if obj.augmented else np.zeros(0)
+    y = obj.y if obj.augmented else np.zeros(0)
+    _check(L.lib().nadmm_lbfgs_solve(data.handle, C.byref(c), obj.lam, int(obj.augmented), float(obj.rho or 0.0),
+                                     _dp(z), _dp(y), _dp(x), tr, cap, C.byref(summ)))
+    recs = [LbfgsIterRecord(r.iter, r.grad_norm, r.step, r.objective, r.fn_evals, bool(r.ls_fallback))
+            for r in tr[: min(summ.iterations, cap)]]
+    return LbfgsResult(x, recs, bool(summ.converged), summ.final_grad_norm)
 
 
 # ---- worker (inc/worker.hpp; src/worker.cpp:127-196) ----------------------------------------------

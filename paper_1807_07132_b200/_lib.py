@@ -34,6 +34,16 @@ class NewtonSummary(C.Structure):
     _fields_ = [("converged", C.c_int32), ("final_grad_norm", C.c_double), ("iterations", C.c_int32)]
 
 
+class LbfgsCfg(C.Structure):  # nadmm_lbfgs_cfg == LbfgsConfig (inc/lbfgs.hpp:9-18)
+    _fields_ = [("history", C.c_int32), ("wolfe_c1", C.c_double), ("wolfe_c2", C.c_double),
+                ("max_iters", C.c_int32), ("ls_max_iters", C.c_int32), ("grad_tol", C.c_double)]
+
+
+class LbfgsIter(C.Structure):  # LbfgsIterRecord (inc/lbfgs.hpp:20-27)
+    _fields_ = [("iter", C.c_int32), ("grad_norm", C.c_double), ("step", C.c_double), ("objective", C.c_double),
+                ("fn_evals", C.c_int32), ("ls_fallback", C.c_int32)]
+
+
 class InnerStats(C.Structure):  # InnerStats (inc/comm.hpp:67-73)
     _fields_ = [("grad_norm", C.c_double), ("inner_iters", C.c_uint32), ("cg_iters", C.c_uint32),
                 ("fn_evals", C.c_uint32), ("flags", C.c_uint32)]
@@ -87,6 +97,9 @@ SIGNATURES = {
     "nadmm_set_point_dev": (S, [VP, VP]),
     "nadmm_hessian_vec_dev": (S, [VP, VP, C.c_double, VP]),
     "nadmm_newton_cfg_default": (None, [C.POINTER(NewtonCfg)]),
+    "nadmm_lbfgs_cfg_default": (None, [C.POINTER(LbfgsCfg)]),
+    "nadmm_lbfgs_solve": (S, [VP, C.POINTER(LbfgsCfg), C.c_double, C.c_int32, C.c_double, D, D, D,
+                              C.POINTER(LbfgsIter), C.c_int32, C.POINTER(NewtonSummary)]),
     "nadmm_newton_solve": (S, [VP, C.POINTER(NewtonCfg), C.c_double, C.c_int32, C.c_double, D, D, D,
                                C.POINTER(NewtonIter), C.c_int32, C.POINTER(NewtonSummary)]),
     "nadmm_worker_create": (S, [VP, C.POINTER(VP)]),

@@ -549,6 +549,34 @@ nadmm_status nadmm_newton_solve(nadmm_shard s, const nadmm_newton_cfg* cfg, doub
     });
 }
 
+void nadmm_lbfgs_cfg_default(nadmm_lbfgs_cfg* c) {
+    if (c) *c = nadmm_lbfgs_cfg{25, 1e-4, 0.9, 100, 20, 1e-8};  // inc/lbfgs.hpp:10-15
+}
+
+nadmm_status nadmm_lbfgs_solve(nadmm_shard s, const nadmm_lbfgs_cfg* cfg, double lambda, int32_t augmented,
+                               double rho, const double* z, const double* y, double* x_inout,
+                               nadmm_lbfgs_iter* trace, int32_t trace_cap, nadmm_newton_summary* out) {
+    return guard([&] {
+        nadmm_lbfgs_cfg c;
+        nadmm_lbfgs_cfg_default(&c);
+        if (cfg) c = *cfg;
+        validate_lbfgs_cfg(c);
+        check_shard(s);
+        if (!x_inout) raise(NADMM_ECONFIG, "x_inout required");
+        if (augmented) {
+            if (rho <= 0.0) raise(NADMM_ECONFIG, "augmented objective requires rho > 0");
+            if (!z || !y) raise(NADMM_ECONFIG, "augmented objective requires z and y");
+            upload(s->z, z, sizeof(double) * s->d, s->ctx->stream);
+            upload(s->y, y, sizeof(double) * s->d, s->ctx->stream);
+        }
+        upload(s->x, x_inout, sizeof(double) * s->d, s->ctx->stream);
+        const LbfgsResult r = device_lbfgs_solve(*s, c, lambda, augmented != 0, rho);
+        download(x_inout, s->x, sizeof(double) * s->d, s->ctx->stream);
+        for (int k = 0; trace && k < std::min<int>(trace_cap, (int)r.trace.size()); ++k) trace[k] = r.trace[k];
+        if (out) *out = nadmm_newton_summary{r.converged ? 1 : 0, r.final_grad_norm, (int32_t)r.trace.size()};
+    });
+}
+
 }  // extern "C"
 
 // ---- worker level ----

@@ -33,4 +33,15 @@ SolveResult solve_result(Shard& s, const nadmm_newton_cfg& cfg);
 SolveResult device_newton_solve(Shard& s, const nadmm_newton_cfg& cfg, double lambda, bool aug, double rho,
                                 int newton_max);
 
+// lbfgs_solve (src/lbfgs.cpp:94-181) from s.x (z / y in s.z / s.y when augmented); x left in s.x.
+constexpr int kLbMaxHist = 256;
+using LbfgsCfg = nadmm_lbfgs_cfg;
+struct LbfgsResult {
+    std::vector<nadmm_lbfgs_iter> trace;
+    bool converged = false;
+    double final_grad_norm = 0.0;
+};
+void validate_lbfgs_cfg(const LbfgsCfg& c);
+LbfgsResult device_lbfgs_solve(Shard& s, const LbfgsCfg& cfg, double lambda, bool aug, double rho);
+
 }  // namespace nadmm
