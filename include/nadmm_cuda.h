@@ -197,6 +197,11 @@ nadmm_status nadmm_worker_free(nadmm_worker w);
 nadmm_status nadmm_worker_solve(nadmm_worker w, double rho, const double* z, const double* y,
                                 const nadmm_newton_cfg* cfg, int32_t inner_iters, double* x_out,
                                 nadmm_inner_stats* stats);
+/* The same round with the L-BFGS inner solver (src/worker.cpp:183-195): cfg->max_iters is replaced
+ * by inner_iters; stats.inner_iters = trace length, fn_evals summed, flags bit0 = a Wolfe fallback. */
+nadmm_status nadmm_worker_solve_lbfgs(nadmm_worker w, double rho, const double* z, const double* y,
+                                      const nadmm_lbfgs_cfg* cfg, int32_t inner_iters, double* x_out,
+                                      nadmm_inner_stats* stats);
 
 /* ------------------------------------------------------------------------------------------ */
 /* Consensus level -- run_admm (inc/admm.hpp:17-140)                          */
@@ -225,6 +230,9 @@ typedef struct {                  /* AdmmConfig + PenaltyPolicy + StoppingConfig
     double f_star;                /* > 0: theta = (F - F*)/F* recorded per row */
     double theta_stop;            /* > 0 (needs f_star): stop at the first k with theta <= theta_stop */
     int32_t ignore_convergence;   /* throughput runs: report convergence in the rows but keep iterating */
+    /* inner solver of the workers (InnerSolverKind, inc/admm.hpp:105-114; src/worker.cpp:170-195) */
+    int32_t inner_solver;         /* 0 newton, 1 lbfgs (its max_iters is set to inner_iters) */
+    nadmm_lbfgs_cfg lbfgs;
 } nadmm_admm_cfg;
 
 void nadmm_admm_cfg_default(nadmm_admm_cfg* cfg);

@@ -472,19 +472,33 @@ class Worker:
         cfg = cfg or NewtonConfig()
         z = _wvec(self.shard, z, "z")
         y = _wvec(self.shard, y, "y")
-        d = self.shard.weight_dim()
-        if out is not None:
-            if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.shape == (d,)
-                    and out.flags.c_contiguous):
-                raise ConfigError(f"out must be a contiguous float64 array of length {d}")
-            x = out
-        else:
-            x = np.zeros(d)
+        x = self._out(out)
         st = L.InnerStats()
         c = cfg.to_c()
         _check(L.lib().nadmm_worker_solve(self.handle, float(rho), _dp(z), _dp(y), C.byref(c), int(inner_iters),
                                           _dp(x), C.byref(st)))
         return x, InnerStats(st.grad_norm, st.inner_iters, st.cg_iters, st.fn_evals, st.flags)
+
+    def solve_lbfgs(self, rho: float, z, y, cfg: Optional[LbfgsConfig] = None, inner_iters: int = 1, out=None):
+        """The same round with the L-BFGS inner solver (src/worker.cpp:183-195)."""
+        cfg = cfg or LbfgsConfig()
+        z = _wvec(self.shard, z, "z")
+        y = _wvec(self.shard, y, "y")
+        x = self._out(out)
+        st = L.InnerStats()
+        c = cfg.to_c()
+        _check(L.lib().nadmm_worker_solve_lbfgs(self.handle, float(rho), _dp(z), _dp(y), C.byref(c),
+                                                int(inner_iters), _dp(x), C.byref(st)))
+        return x, InnerStats(st.grad_norm, st.inner_iters, st.cg_iters, st.fn_evals, st.flags)
+
+    def _out(self, out):
+        d = self.shard.weight_dim()
+        if out is None:
+            return np.zeros(d)
+        if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.shape == (d,)
+                and out.flags.c_contiguous):
+            raise ConfigError(f"out must be a contiguous float64 array of length {d}")
+        return out
 
     def __del__(self):
         try:
@@ -520,6 +534,8 @@ class AdmmConfig:  # inc/admm.hpp:107-117
     stopping: StoppingConfig = field(default_factory=StoppingConfig)
     newton: NewtonConfig = field(default_factory=NewtonConfig)
     inner_iters: int = 1
+    inner_solver: str = "newton"  # InnerSolverKind (inc/admm.hpp:105-114): "newton" | "lbfgs"
+    lbfgs: LbfgsConfig = field(default_factory=LbfgsConfig)
 
     def to_c(self) -> L.AdmmCfg:
         c = L.AdmmCfg()
@@ -532,6 +548,10 @@ class AdmmConfig:  # inc/admm.hpp:107-117
         c.max_outer_iters, c.standard_norms = self.stopping.max_outer_iters, int(self.stopping.standard_norms)
         c.inner_iters = self.inner_iters
         c.newton = self.newton.to_c()
+        if self.inner_solver not in ("newton", "lbfgs"):
+            raise ConfigError(f"unknown inner solver {self.inner_solver!r}")
+        c.inner_solver = 1 if self.inner_solver == "lbfgs" else 0
+        c.lbfgs = self.lbfgs.to_c()
         return c
 
 

@@ -60,7 +60,7 @@ class AdmmCfg(C.Structure):  # AdmmConfig + PenaltyPolicy + StoppingConfig (inc/
                 ("eps_abs", C.c_double), ("eps_rel", C.c_double), ("max_outer_iters", C.c_int32),
                 ("standard_norms", C.c_int32), ("inner_iters", C.c_int32), ("newton", NewtonCfg),
                 ("eval_objective", C.c_int32), ("f_star", C.c_double), ("theta_stop", C.c_double),
-                ("ignore_convergence", C.c_int32)]
+                ("ignore_convergence", C.c_int32), ("inner_solver", C.c_int32), ("lbfgs", LbfgsCfg)]
 
 
 class MetricsRow(C.Structure):  # MetricsRow (inc/metrics.hpp:15-27)
@@ -103,6 +103,8 @@ SIGNATURES = {
     "nadmm_newton_solve": (S, [VP, C.POINTER(NewtonCfg), C.c_double, C.c_int32, C.c_double, D, D, D,
                                C.POINTER(NewtonIter), C.c_int32, C.POINTER(NewtonSummary)]),
     "nadmm_worker_create": (S, [VP, C.POINTER(VP)]),
+    "nadmm_worker_solve_lbfgs": (S, [VP, C.c_double, D, D, C.POINTER(LbfgsCfg), C.c_int32, D,
+                                     C.POINTER(InnerStats)]),
     "nadmm_worker_free": (S, [VP]),
     "nadmm_worker_solve": (S, [VP, C.c_double, D, D, C.POINTER(NewtonCfg), C.c_int32, D, C.POINTER(InnerStats)]),
     "nadmm_comm_unique_id": (S, [C.POINTER(C.c_uint8)]),

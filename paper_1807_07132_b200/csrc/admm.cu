@@ -189,6 +189,8 @@ void nadmm_admm_cfg_default(nadmm_admm_cfg* c) {  // inc/admm.hpp:37-56, 107-117
     c->standard_norms = 0;
     c->inner_iters = 1;
     nadmm_newton_cfg_default(&c->newton);
+    c->inner_solver = 0;
+    nadmm_lbfgs_cfg_default(&c->lbfgs);
     c->eval_objective = 0;
     c->f_star = 0.0;
     c->theta_stop = 0.0;
@@ -249,6 +251,7 @@ struct AdmmRun {
     nadmm_comm comm = nullptr;
     nadmm_admm_cfg cfg{};
     nadmm_newton_cfg ncfg{};
+    nadmm_lbfgs_cfg lcfg{};
     Ctx* ctx = nullptr;
     cudaStream_t st = nullptr;
     int64_t d = 0;
@@ -280,6 +283,10 @@ struct AdmmRun {
         ncfg = cfg.newton;
         ncfg.newton_max_iters = cfg.inner_iters;
         validate_newton_cfg(ncfg);
+        if (cfg.inner_solver != 0 && cfg.inner_solver != 1) raise(NADMM_ECONFIG, "inner_solver must be 0 or 1");
+        lcfg = cfg.lbfgs;
+        lcfg.max_iters = cfg.inner_iters;  // src/worker.cpp:184
+        if (cfg.inner_solver == 1) validate_lbfgs_cfg(lcfg);
         for (int i = 0; i < nl; ++i) {
             if (!sh[i]) raise(NADMM_ECONFIG, "null shard");
             shards.push_back(sh[i]);
@@ -355,11 +362,19 @@ struct AdmmRun {
         for (int i = 0; i < n_local; ++i) {  // (1) scatter z / solve (all workers enqueued back to back)
             Shard& s = *shards[i];
             NADMM_CUDA(cudaMemcpyAsync(s.z, z, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+            if (cfg.inner_solver == 1) {  // L-BFGS: host-driven line search, synchronous per worker
+                const nadmm_inner_stats lst = lbfgs_inner_stats(device_lbfgs_solve(s, lcfg, 0.0, true, rho[i]));
+                inner += (int)lst.inner_iters;
+                fe_sum += (int)lst.fn_evals;
+                flags |= (int)lst.flags;
+                pending[i] = 2;
+                continue;
+            }
             pending[i] = !solve_launch(s, ncfg, 0.0, true, rho[i], cfg.inner_iters);
         }
         // the workers' inner stats come back with the iteration's single synchronisation below
         for (int i = 0; i < n_local; ++i)
-            if (pending[i]) solve_readback_async(*shards[i]);
+            if (pending[i] == 1) solve_readback_async(*shards[i]);
         LocalPtrs lp{};  // (2) consensus sum + one allreduce
         lp.n = n_local;
         double rho_sum = 0.0;
@@ -401,6 +416,7 @@ struct AdmmRun {
         NADMM_CUDA(cudaStreamSynchronize(st));
         for (int i = 0; i < n_local; ++i) {  // gather the workers' inner stats
             Shard& s = *shards[i];
+            if (pending[i] == 2) continue;  // L-BFGS stats already gathered
             SolveResult r = pending[i] ? solve_result(s, ncfg) : solve_collect(s, ncfg, false);
             if (r.error) raise((nadmm_status)r.error, "worker inner solve failed");
             inner += r.iterations;

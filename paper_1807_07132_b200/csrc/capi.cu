@@ -626,6 +626,28 @@ nadmm_status nadmm_worker_solve(nadmm_worker w, double rho, const double* z, con
     });
 }
 
+nadmm_status nadmm_worker_solve_lbfgs(nadmm_worker w, double rho, const double* z, const double* y,
+                                      const nadmm_lbfgs_cfg* cfg, int32_t inner_iters, double* x_out,
+                                      nadmm_inner_stats* stats) {
+    return guard([&] {
+        if (!w) raise(NADMM_ECONFIG, "null worker");
+        Shard& s = *w->shard;
+        nadmm_lbfgs_cfg c;
+        nadmm_lbfgs_cfg_default(&c);
+        if (cfg) c = *cfg;
+        c.max_iters = inner_iters;  // src/worker.cpp:184
+        validate_lbfgs_cfg(c);
+        check_shard(w->shard);
+        if (rho <= 0.0) raise(NADMM_ECONFIG, "augmented objective requires rho > 0");
+        if (!z || !y) raise(NADMM_ECONFIG, "z and y required");
+        upload(s.z, z, sizeof(double) * s.d, s.ctx->stream);
+        upload(s.y, y, sizeof(double) * s.d, s.ctx->stream);
+        const LbfgsResult r = device_lbfgs_solve(s, c, 0.0, true, rho);  // x_local warm start in s.x
+        if (x_out) download(x_out, s.x, sizeof(double) * s.d, s.ctx->stream);
+        if (stats) *stats = lbfgs_inner_stats(r);
+    });
+}
+
 }  // extern "C"
 
 namespace nadmm {

@@ -43,5 +43,14 @@ struct LbfgsResult {
 };
 void validate_lbfgs_cfg(const LbfgsCfg& c);
 LbfgsResult device_lbfgs_solve(Shard& s, const LbfgsCfg& cfg, double lambda, bool aug, double rho);
+// InnerStats of an L-BFGS worker round (src/worker.cpp:186-194).
+inline nadmm_inner_stats lbfgs_inner_stats(const LbfgsResult& r) {
+    nadmm_inner_stats st{r.final_grad_norm, (uint32_t)r.trace.size(), 0u, 0u, 0u};
+    for (const auto& t : r.trace) {
+        st.fn_evals += (uint32_t)t.fn_evals;
+        if (t.ls_fallback) st.flags |= 1u;
+    }
+    return st;
+}
 
 }  // namespace nadmm

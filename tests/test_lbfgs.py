@@ -143,3 +143,59 @@ def test_lbfgs_default_config():
     d = nadmm.LbfgsConfig()
     assert (c.history, c.wolfe_c1, c.wolfe_c2, c.max_iters, c.ls_max_iters, c.grad_tol) == \
         (d.history, d.wolfe_c1, d.wolfe_c2, d.max_iters, d.ls_max_iters, d.grad_tol) == CFG
+
+
+@pytest.mark.gpu
+def test_worker_lbfgs_rounds_match_reference(nadmm, ref):
+    """run_worker's L-BFGS branch (src/worker.cpp:183-195): warm-started rounds, InnerStats packing."""
+    rng = np.random.default_rng(12)
+    X, y = random_dense(rng, 300, 14, 4, scale=0.5)
+    ds = nadmm.Dataset.dense(X, y, 4)
+    rd = ref.dataset(oracle.Shard(X, y, 4))
+    w = nadmm.Worker(ds)
+    d = ds.weight_dim()
+    x_ref = np.zeros(d)
+    cfg = nadmm.LbfgsConfig(grad_tol=1e-6)
+    for k in range(4):
+        z, yy = rng.normal(size=d) * 0.1, rng.normal(size=d) * 0.1
+        rho, inner = [1.0, 2.0, 0.5, 1.0][k], [3, 5, 2, 8][k]
+        xg, st = w.solve_lbfgs(rho, z, yy, cfg, inner_iters=inner)
+        o = rd.lbfgs_solve(0.0, x_ref, (25, 1e-4, 0.9, inner, 20, 1e-6), rho=rho, z=z, y=yy)
+        x_ref = o["x"]
+        assert rel(xg, x_ref) <= TOL_X
+        assert st.inner_iters == len(o["trace"])
+        assert st.fn_evals == sum(int(t["fn_evals"]) for t in o["trace"])
+        assert st.flags == (1 if any(t["ls_fallback"] for t in o["trace"]) else 0)
+        assert st.cg_iters == 0
+        assert st.grad_norm == pytest.approx(o["final_grad_norm"], rel=1e-6)
+
+
+@pytest.mark.gpu
+def test_admm_lbfgs_inner_solver_matches_composed_reference(nadmm, port, ref):
+    """run_admm with inner_solver = lbfgs against the reference's lbfgs_solve per worker composed with
+    the SPEC z / y updates (fixed penalty), outer iteration by outer iteration."""
+    N, C_, p, K, inner = 3, 4, 10, 5, 4
+    Xtr, ytr, _, _ = port.generate_synthetic(900, p, C_, separation=3.0, noise=1.0, seed=2)
+    owner = port.partition_owner(len(ytr), N)
+    parts = [(Xtr[owner == i], ytr[owner == i]) for i in range(N)]
+    lam = 1e-3
+    cfg = nadmm.AdmmConfig(n_workers=N, lam=lam, stopping=nadmm.StoppingConfig(max_outer_iters=K),
+                           inner_iters=inner, inner_solver="lbfgs", lbfgs=nadmm.LbfgsConfig(grad_tol=1e-6))
+    rg = nadmm.run_admm([nadmm.Dataset.dense(X, y, C_) for X, y in parts], cfg,
+                        nadmm.EvalContext(eval_objective=False, ignore_convergence=True))
+    assert rg.iterations == K
+    rds = [ref.dataset(oracle.Shard(X, y, C_)) for X, y in parts]
+    d = (C_ - 1) * p
+    x, yv, z = np.zeros((N, d)), np.zeros((N, d)), np.zeros(d)
+    rho = np.ones(N)
+    for k in range(K):
+        fe = 0
+        for i in range(N):
+            o = rds[i].lbfgs_solve(0.0, x[i], (25, 1e-4, 0.9, inner, 20, 1e-6), rho=1.0, z=z, y=yv[i])
+            x[i] = o["x"]
+            fe += sum(int(t["fn_evals"]) for t in o["trace"])
+        z = port.z_update(x, yv, rho, lam)
+        yv = port.y_update(yv, x, z, rho)
+        assert rg.metrics[k]["fn_evals"] == fe
+        assert rg.metrics[k]["cg_iters"] == 0
+    assert rel(rg.z, z) <= TOL_X
