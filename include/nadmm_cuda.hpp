@@ -231,6 +231,52 @@ inline NewtonResult newton_solve(const Dataset& ds, double lambda, Vector x0, co
     return r;
 }
 
+// ---- lbfgs_solve (inc/lbfgs.hpp:9-39) ----
+struct LbfgsConfig {
+    int history = 25;
+    double wolfe_c1 = 1e-4;
+    double wolfe_c2 = 0.9;
+    int max_iters = 100;
+    int ls_max_iters = 20;
+    double grad_tol = 1e-8;
+    nadmm_lbfgs_cfg to_c() const {
+        return nadmm_lbfgs_cfg{history, wolfe_c1, wolfe_c2, max_iters, ls_max_iters, grad_tol};
+    }
+};
+
+struct LbfgsIterRecord {
+    int iter;
+    double grad_norm, step, objective;
+    int fn_evals;
+    bool ls_fallback;
+};
+
+struct LbfgsResult {
+    Vector x;
+    std::vector<LbfgsIterRecord> trace;
+    bool converged = false;
+    double final_grad_norm = 0.0;
+};
+
+inline LbfgsResult lbfgs_solve(const Dataset& ds, double lambda, Vector x0, const LbfgsConfig& cfg = {},
+                               const Augmentation* aug = nullptr) {
+    const nadmm_lbfgs_cfg c = cfg.to_c();
+    std::vector<nadmm_lbfgs_iter> tr((size_t)std::max(1, cfg.max_iters));
+    nadmm_newton_summary sum{};
+    check(nadmm_lbfgs_solve(ds.handle(), &c, lambda, aug ? 1 : 0, aug ? aug->rho : 0.0,
+                            aug ? aug->z.data() : nullptr, aug ? aug->y.data() : nullptr, x0.data(), tr.data(),
+                            (int32_t)tr.size(), &sum));
+    LbfgsResult r;
+    r.x = std::move(x0);
+    r.converged = sum.converged != 0;
+    r.final_grad_norm = sum.final_grad_norm;
+    for (int i = 0; i < sum.iterations && i < (int)tr.size(); ++i) {
+        const nadmm_lbfgs_iter& t = tr[(size_t)i];
+        r.trace.push_back({t.iter, t.grad_norm, t.step, t.objective, t.fn_evals, t.ls_fallback != 0});
+    }
+    return r;
+}
+
 // ---- the worker's ADMM branch (src/worker.cpp:127-196) ----
 struct InnerStats {
     double grad_norm;
@@ -252,6 +298,16 @@ class Worker {
         x_out.resize((size_t)ds_->weight_dim());
         nadmm_inner_stats st{};
         check(nadmm_worker_solve(h_, rho, z.data(), y.data(), &c, inner_iters, x_out.data(), &st));
+        return InnerStats{st.grad_norm, st.inner_iters, st.cg_iters, st.fn_evals, st.flags};
+    }
+
+    // the same round with the L-BFGS inner solver (src/worker.cpp:183-195)
+    InnerStats solve_lbfgs(double rho, const Vector& z, const Vector& y, Vector& x_out, const LbfgsConfig& cfg = {},
+                           int inner_iters = 1) {
+        const nadmm_lbfgs_cfg c = cfg.to_c();
+        x_out.resize((size_t)ds_->weight_dim());
+        nadmm_inner_stats st{};
+        check(nadmm_worker_solve_lbfgs(h_, rho, z.data(), y.data(), &c, inner_iters, x_out.data(), &st));
         return InnerStats{st.grad_norm, st.inner_iters, st.cg_iters, st.fn_evals, st.flags};
     }
 
