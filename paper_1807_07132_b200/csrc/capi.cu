@@ -161,7 +161,7 @@ Shard::~Shard() {
     }
     for (cudaEvent_t e : tl_events) cudaEventDestroy(e);
     for (double** v : {&X, &wt, &vals, &cval, &L0, &P, &U, &Lp, &rowM, &rowA, &part, &blk, &cache_x, &gbase, &scal, &x, &g,
-                       &pd, &r, &dv, &hd, &z, &y, &t, &tmp})
+                       &pd, &r, &dv, &hd, &z, &y, &t, &tmp, &lb_ws})
         dev_free(*v);
     dev_free(indptr);
     dev_free(indices);

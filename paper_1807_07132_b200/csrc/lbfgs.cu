@@ -203,17 +203,6 @@ __global__ void __launch_bounds__(kLbClThreads, 1) k_lb_direction(int64_t d, con
     cl.sync();  // no CTA exits while peers may still read its slots
 }
 
-template <typename T>
-struct DevBuf {
-    T* p = nullptr;
-    explicit DevBuf(size_t n) { NADMM_CUDA(cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1))); }
-    ~DevBuf() {
-        if (p) cudaFree(p);
-    }
-    DevBuf(const DevBuf&) = delete;
-    DevBuf& operator=(const DevBuf&) = delete;
-};
-
 struct Lbfgs {
     Shard& s;
     const LbfgsCfg& cfg;
@@ -222,7 +211,12 @@ struct Lbfgs {
     cudaStream_t st;
     int64_t d;
     int nb;
-    DevBuf<double> S, Y, vx, vg, vxa, vga, vp, vq, part, out;
+    double* S;  // (history + 1) x d curvature pairs s_i, then the same for y_i
+    double* Y;
+    double* vp;  // direction
+    double* vq;  // two-loop working vector
+    double* part;
+    double* out;
     double* x;
     double* g;
     double* xa;
@@ -231,26 +225,46 @@ struct Lbfgs {
 
     Lbfgs(Shard& sh, const LbfgsCfg& c, bool a, double r)
         : s(sh), cfg(c), aug(a), rho(r), st(sh.ctx->stream), d(sh.d),
-          nb((int)std::min<int64_t>(kLbMaxBlocks, std::max<int64_t>(1, (sh.d + kLbThreads - 1) / kLbThreads))),
-          S((size_t)(c.history + 1) * sh.d), Y((size_t)(c.history + 1) * sh.d), vx(sh.d), vg(sh.d), vxa(sh.d),
-          vga(sh.d), vp(sh.d), vq(sh.d), part(3 * (size_t)nb), out(4) {
-        x = vx.p;
-        g = vg.p;
-        xa = vxa.p;
-        ga = vga.p;
+          nb((int)std::min<int64_t>(kLbMaxBlocks, std::max<int64_t>(1, (sh.d + kLbThreads - 1) / kLbThreads))) {
+        // one workspace per shard, grown on demand and reused by later solves (no per-solve allocation)
+        const int64_t hist = (int64_t)(c.history + 1) * d;
+        const int64_t need = 2 * hist + 6 * d + 3 * (int64_t)kLbMaxBlocks + 4;
+        if (sh.lb_ws_len < need) {
+            if (sh.lb_ws) {
+                NADMM_CUDA(cudaStreamSynchronize(st));
+                cudaFree(sh.lb_ws);
+                sh.bytes -= 8 * sh.lb_ws_len;
+                sh.lb_ws = nullptr;
+                sh.lb_ws_len = 0;
+            }
+            NADMM_CUDA(cudaMalloc(&sh.lb_ws, sizeof(double) * (size_t)need));
+            sh.lb_ws_len = need;
+            sh.bytes += 8 * need;
+        }
+        double* w = sh.lb_ws;
+        S = w;
+        Y = S + hist;
+        x = Y + hist;
+        g = x + d;
+        xa = g + d;
+        ga = xa + d;
+        vp = ga + d;
+        vq = vp + d;
+        part = vq + d;
+        out = part + 3 * kLbMaxBlocks;
     }
 
     void fetch(int n) {
-        NADMM_CUDA(cudaMemcpyAsync(host, out.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        NADMM_CUDA(cudaMemcpyAsync(host, out, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
         NADMM_CUDA(cudaStreamSynchronize(st));
     }
 
     // f(w), |g(w)|^2 and g(w)'p (p may be null); the gradient lands in gout.
     void eval(const double* w, double* gout, const double* p, double& f, double& gsq, double& gp) {
         op_cache_grad(s, w, nullptr);  // base loss (ridge included) -> scal[0], base gradient -> gbase
-        k_lb_grad<<<nb, kLbThreads, 0, st>>>(d, w, s.gbase, s.z, s.y, rho, aug ? 1 : 0, p, gout, part.p);
+        k_lb_grad<<<nb, kLbThreads, 0, st>>>(d, w, s.gbase, s.z, s.y, rho, aug ? 1 : 0, p, gout, part);
         NADMM_LAUNCH_CHECK();
-        k_lb_sum<<<1, 32, 0, st>>>(part.p, nb, 3, s.scal, out.p);
+        k_lb_sum<<<1, 32, 0, st>>>(part, nb, 3, s.scal, out);
         NADMM_LAUNCH_CHECK();
         s.ctx->stats.kernel_launches += 2;
         fetch(4);
@@ -269,10 +283,10 @@ struct Lbfgs {
     // Phi (src/lbfgs.cpp:19-31): f(x + a p) and the directional derivative, into xa / ga.
     int evals = 0;
     std::pair<double, double> phi(double a) {
-        point(x, a, vp.p, xa);
+        point(x, a, vp, xa);
         ++evals;
         double f, gsq, gp;
-        eval(xa, ga, vp.p, f, gsq, gp);
+        eval(xa, ga, vp, f, gsq, gp);
         last_f = f;
         last_gsq = gsq;
         return {f, gp};
@@ -375,10 +389,10 @@ struct Lbfgs {
             // curvature pair into a free ring slot (src/lbfgs.cpp:153-166)
             int free_slot = 0;
             while (std::find(hist.begin(), hist.end(), free_slot) != hist.end()) ++free_slot;
-            k_lb_pair<<<nb, kLbThreads, 0, st>>>(d, xa, x, ga, g, S.p + (int64_t)free_slot * d,
-                                                 Y.p + (int64_t)free_slot * d, part.p);
+            k_lb_pair<<<nb, kLbThreads, 0, st>>>(d, xa, x, ga, g, S + (int64_t)free_slot * d,
+                                                 Y + (int64_t)free_slot * d, part);
             NADMM_LAUNCH_CHECK();
-            k_lb_sum<<<1, 32, 0, st>>>(part.p, nb, 3, nullptr, out.p);
+            k_lb_sum<<<1, 32, 0, st>>>(part, nb, 3, nullptr, out);
             NADMM_LAUNCH_CHECK();
             s.ctx->stats.kernel_launches += 2;
             fetch(3);
@@ -421,8 +435,8 @@ struct Lbfgs {
         attr[0].val.clusterDim.z = 1;
         lc.attrs = attr;
         lc.numAttrs = 1;
-        NADMM_CUDA(cudaLaunchKernelEx(&lc, k_lb_direction, d, (const double*)g, (const double*)S.p,
-                                      (const double*)Y.p, h, gamma, vq.p, vp.p, out.p));
+        NADMM_CUDA(cudaLaunchKernelEx(&lc, k_lb_direction, d, (const double*)g, (const double*)S,
+                                      (const double*)Y, h, gamma, vq, vp, out));
         s.ctx->stats.kernel_launches++;
     }
 };

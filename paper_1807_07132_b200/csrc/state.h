@@ -177,6 +177,9 @@ struct Shard {
     bool tl_capture = false;
     std::vector<const char*> tl_names;
     std::vector<cudaEvent_t> tl_events;
+    // L-BFGS workspace (lbfgs.cu), kept across solves: curvature history + work vectors
+    double* lb_ws = nullptr;
+    int64_t lb_ws_len = 0;
     void ensure_timers(int n);
     ~Shard();
 };
