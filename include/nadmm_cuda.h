@@ -178,6 +178,16 @@ nadmm_status nadmm_lbfgs_solve(nadmm_shard shard, const nadmm_lbfgs_cfg* cfg, do
                                double rho, const double* z, const double* y, double* x_inout,
                                nadmm_lbfgs_iter* trace, int32_t trace_cap, nadmm_newton_summary* out);
 
+/* Synchronous mini-batch SGD: SgdConfig + the worker session's
+ * sgd_batch / steps_per_epoch / seed (inc/worker.hpp:20-28). */
+typedef struct {
+    double eta;                   /* step size (> 0) */
+    int32_t batch;                /* mini-batch rows per worker, 1 <= batch <= local n */
+    int32_t epochs;               /* data passes (nadmm_sgd_run) */
+    int32_t steps_per_epoch;      /* worker: >= 1; nadmm_sgd_run: <= 0 -> ceil(n / (batch N)) */
+    uint64_t seed;                /* epoch permutation seed: Rng(mix_seed(seed, epoch)).shuffle */
+} nadmm_sgd_cfg;
+
 /* ------------------------------------------------------------------------------------------ */
 /* Worker level -- run_worker ADMM branch (src/worker.cpp:127-196)                              */
 /* ------------------------------------------------------------------------------------------ */
@@ -202,6 +212,14 @@ nadmm_status nadmm_worker_solve(nadmm_worker w, double rho, const double* z, con
 nadmm_status nadmm_worker_solve_lbfgs(nadmm_worker w, double rho, const double* z, const double* y,
                                       const nadmm_lbfgs_cfg* cfg, int32_t inner_iters, double* x_out,
                                       nadmm_inner_stats* stats);
+
+/* run_worker's SGD branch (src/worker.cpp:197-218) for scatter `iteration`: g_out = the mini-batch
+ * gradient at z (lambda 0) divided by the batch size. Stats: inner_iters = fn_evals = 1.
+ * Batch outside [1, local n] -> NADMM_ECONFIG "sgd batch size must lie in [1, local n]". */
+nadmm_status nadmm_worker_sgd_grad(nadmm_worker w, const nadmm_sgd_cfg* cfg, uint32_t iteration, const double* z,
+                                   double* g_out, nadmm_inner_stats* stats);
+/* The worker's epoch permutation: Rng(mix_seed(seed, epoch)).shuffle of 0..n-1 (src/worker.cpp:199-205). */
+nadmm_status nadmm_sgd_permutation(uint64_t seed, uint32_t epoch, int64_t n, int32_t* perm);
 
 /* ------------------------------------------------------------------------------------------ */
 /* Consensus level -- run_admm (inc/admm.hpp:17-140)                          */
@@ -261,6 +279,14 @@ typedef struct {                  /* MetricsRow subset (inc/metrics.hpp:15-27) *
 nadmm_status nadmm_admm_run(const nadmm_shard* shards, int32_t n_local, nadmm_comm comm, const nadmm_admm_cfg* cfg,
                             double* z_out, double* rho_out, nadmm_metrics_row* rows, int32_t row_cap,
                             int32_t* iterations, int32_t* converged);
+
+/* sync_sgd over this rank's shards (comm may be NULL): per step every worker's
+ * mini-batch gradient at x, g_bar = sum / N in worker (then rank) order, x <- x - eta g_bar; one
+ * metrics row per epoch (train_objective = F(x) with lambda; messages = 2N per step). x_inout: x0
+ * in, x out. F > 1e3 F(x0) aborts with NADMM_ESOLVER (unstable step size). */
+nadmm_status nadmm_sgd_run(const nadmm_shard* shards, int32_t n_local, nadmm_comm comm, const nadmm_sgd_cfg* cfg,
+                           double lambda, double* x_inout, nadmm_metrics_row* rows, int32_t row_cap,
+                           int32_t* epochs_done);
 
 /* Stepping form of the same loop: create (AdmmState::initial), step up to n_iters outer iterations
  * (stops early on convergence / theta_stop / max_outer_iters), read the result, free. rows gets

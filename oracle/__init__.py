@@ -462,6 +462,11 @@ class Ref:
         finally:
             self.lib.nadmm_ref_dataset_free(h)
 
+    def shuffle(self, seed, n):
+        out = np.zeros(n, dtype=np.int64)
+        self._chk(self.lib.nadmm_ref_shuffle(C.c_uint64(seed), C.c_int64(n), _lp(out)))
+        return out
+
     def load_libsvm(self, path) -> dict:
         h = VP()
         self._chk(self.lib.nadmm_ref_load_libsvm(str(path).encode(), C.byref(h)))
@@ -555,6 +560,18 @@ class RefDataset:
         keys = ("iter", "grad_norm", "step", "objective", "fn_evals", "ls_fallback")
         rows = [dict(zip(keys, r.tolist())) for r in tr[: min(nt.value, trace_cap)]]
         return dict(x=x, trace=rows, converged=bool(conv.value), final_grad_norm=gn.value)
+
+    def gradient_subset(self, rows, w, lam=0.0):
+        """gradient(data.subset(rows), w, lam) (src/softmax.cpp:80-95; src/dataset.cpp:87-115)."""
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        h = VP()
+        self.ref._chk(self.ref.lib.nadmm_ref_subset(self.h, _lp(rows), C.c_int64(len(rows)), C.byref(h)))
+        try:
+            g = np.zeros(self.sh.d)
+            self.ref._chk(self.ref.lib.nadmm_ref_gradient(h, _dp(_f64(w)), C.c_double(lam), _dp(g)))
+            return g
+        finally:
+            self.ref.lib.nadmm_ref_dataset_free(h)
 
     def worker(self) -> "RefWorker":
         h = VP()

@@ -434,5 +434,24 @@ int nadmm_ref_dataset_fetch(void* h, std::int64_t* indptr, std::int32_t* indices
     });
 }
 
+// detail::Rng(seed).shuffle of 0..n-1 (inc/data_io.hpp:23-28): the SGD worker's permutation.
+int nadmm_ref_shuffle(std::uint64_t seed, std::int64_t n, std::int64_t* out) {
+    return guard([&] {
+        std::vector<Index> perm(static_cast<std::size_t>(n));
+        for (Index i = 0; i < n; ++i) perm[static_cast<std::size_t>(i)] = i;
+        detail::Rng rng(seed);
+        rng.shuffle(perm);
+        for (Index i = 0; i < n; ++i) out[i] = perm[static_cast<std::size_t>(i)];
+    });
+}
+
+// Dataset::subset (src/dataset.cpp:87-115), the SGD mini-batch.
+int nadmm_ref_subset(void* ds, const std::int64_t* rows, std::int64_t m, void** out) {
+    return guard([&] {
+        std::vector<Index> r(rows, rows + m);
+        *out = new Dataset(static_cast<Dataset*>(ds)->subset(r));
+    });
+}
+
 }  // extern "C"
 

@@ -31,6 +31,7 @@ __all__ = [
     "AdmmConfig", "EvalContext", "AdmmRunResult", "run_admm", "Communicator", "generate_synthetic",
     "generate_sparse", "partition_owner", "partition", "mix_seed", "default_context", "LoadedData", "read_libsvm",
     "read_idx", "load_libsvm", "load_idx", "LbfgsConfig", "LbfgsIterRecord", "LbfgsResult", "lbfgs_solve",
+    "SgdConfig", "SgdResult", "sgd_permutation", "sync_sgd",
 ]
 
 
@@ -448,6 +449,51 @@ def lbfgs_solve(obj: Objective, x0, cfg: Optional[LbfgsConfig] = None) -> LbfgsR
     return LbfgsResult(x, recs, bool(summ.converged), summ.final_grad_norm)
 
 
+# ---- synchronous SGD (src/worker.cpp:197-218) -----------------------------------
+@dataclass
+class SgdConfig:  # SgdConfig + WorkerSessionConfig sgd_batch / steps_per_epoch / seed
+    eta: float = 1.0
+    batch: int = 100
+    epochs: int = 1
+    steps_per_epoch: int = 0  # worker: >= 1; sync_sgd: 0 -> ceil(n / (batch N))
+    seed: int = 0
+
+    def to_c(self) -> L.SgdCfg:
+        return L.SgdCfg(self.eta, self.batch, self.epochs, self.steps_per_epoch, self.seed)
+
+
+@dataclass
+class SgdResult:
+    x: np.ndarray
+    metrics: list
+    epochs: int
+
+
+def sgd_permutation(seed: int, epoch: int, n: int) -> np.ndarray:
+    """The SGD worker's epoch permutation Rng(mix_seed(seed, epoch)).shuffle(0..n-1)."""
+    out = np.empty(n, dtype=np.int32)
+    _check(L.lib().nadmm_sgd_permutation(seed, epoch, n, _ip(out)))
+    return out
+
+
+def sync_sgd(parts: Sequence[Dataset], cfg: SgdConfig, lam: float = 0.0, x0=None,
+             comm: Optional[Communicator] = None) -> SgdResult:
+    """Synchronous mini-batch SGD over device shards: one metrics row per epoch."""
+    if not parts:
+        raise ConfigError("sync_sgd needs at least one shard")
+    d = parts[0].weight_dim()
+    x = np.zeros(d) if x0 is None else _wvec(parts[0], x0, "x0").copy()
+    hs = (C.c_void_p * len(parts))(*[p.handle for p in parts])
+    cap = max(1, cfg.epochs)
+    rows = (L.MetricsRow * cap)()
+    done = C.c_int32()
+    c = cfg.to_c()
+    _check(L.lib().nadmm_sgd_run(hs, len(parts), comm.handle if comm else None, C.byref(c), float(lam), _dp(x), rows,
+                                 cap, C.byref(done)))
+    metrics = [{f: getattr(r, f) for f, _ in L.MetricsRow._fields_} for r in rows[: min(done.value, cap)]]
+    return SgdResult(x, metrics, done.value)
+
+
 # ---- worker (inc/worker.hpp; src/worker.cpp:127-196) ----------------------------------------------
 @dataclass
 class InnerStats:  # inc/comm.hpp:67-73
@@ -490,6 +536,15 @@ class Worker:
         _check(L.lib().nadmm_worker_solve_lbfgs(self.handle, float(rho), _dp(z), _dp(y), C.byref(c),
                                                 int(inner_iters), _dp(x), C.byref(st)))
         return x, InnerStats(st.grad_norm, st.inner_iters, st.cg_iters, st.fn_evals, st.flags)
+
+    def sgd_grad(self, cfg: SgdConfig, iteration: int, z):
+        """The SGD branch of run_worker for scatter `iteration`: the mini-batch gradient at z / batch."""
+        z = _wvec(self.shard, z, "z")
+        g = np.zeros(self.shard.weight_dim())
+        st = L.InnerStats()
+        c = cfg.to_c()
+        _check(L.lib().nadmm_worker_sgd_grad(self.handle, C.byref(c), int(iteration), _dp(z), _dp(g), C.byref(st)))
+        return g, InnerStats(st.grad_norm, st.inner_iters, st.cg_iters, st.fn_evals, st.flags)
 
     def _out(self, out):
         d = self.shard.weight_dim()

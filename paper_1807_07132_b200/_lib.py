@@ -44,6 +44,11 @@ class LbfgsIter(C.Structure):  # LbfgsIterRecord (inc/lbfgs.hpp:20-27)
                 ("fn_evals", C.c_int32), ("ls_fallback", C.c_int32)]
 
 
+class SgdCfg(C.Structure):  # nadmm_sgd_cfg: SgdConfig + the worker session's SGD keys
+    _fields_ = [("eta", C.c_double), ("batch", C.c_int32), ("epochs", C.c_int32), ("steps_per_epoch", C.c_int32),
+                ("seed", C.c_uint64)]
+
+
 class InnerStats(C.Structure):  # InnerStats (inc/comm.hpp:67-73)
     _fields_ = [("grad_norm", C.c_double), ("inner_iters", C.c_uint32), ("cg_iters", C.c_uint32),
                 ("fn_evals", C.c_uint32), ("flags", C.c_uint32)]
@@ -103,6 +108,10 @@ SIGNATURES = {
     "nadmm_newton_solve": (S, [VP, C.POINTER(NewtonCfg), C.c_double, C.c_int32, C.c_double, D, D, D,
                                C.POINTER(NewtonIter), C.c_int32, C.POINTER(NewtonSummary)]),
     "nadmm_worker_create": (S, [VP, C.POINTER(VP)]),
+    "nadmm_worker_sgd_grad": (S, [VP, C.POINTER(SgdCfg), C.c_uint32, D, D, C.POINTER(InnerStats)]),
+    "nadmm_sgd_permutation": (S, [C.c_uint64, C.c_uint32, C.c_int64, I32]),
+    "nadmm_sgd_run": (S, [C.POINTER(VP), C.c_int32, VP, C.POINTER(SgdCfg), C.c_double, D, C.POINTER(MetricsRow),
+                          C.c_int32, C.POINTER(C.c_int32)]),
     "nadmm_worker_solve_lbfgs": (S, [VP, C.c_double, D, D, C.POINTER(LbfgsCfg), C.c_int32, D,
                                      C.POINTER(InnerStats)]),
     "nadmm_worker_free": (S, [VP]),

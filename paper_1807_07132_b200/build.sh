@@ -6,7 +6,7 @@ NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
 mkdir -p build lib
 FLAGS=(-std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC
        -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr -Xptxas -v)
-SRCS=(kernels_pass kernels_vec kernels_dmma kernels_smallp kernels_gemm kernels_sparse newton lbfgs capi admm data_io)
+SRCS=(kernels_pass kernels_vec kernels_dmma kernels_smallp kernels_gemm kernels_sparse newton lbfgs sgd capi admm data_io)
 pids=()
 for s in "${SRCS[@]}"; do
   "$NVCC" "${FLAGS[@]}" -c "csrc/$s.cu" -o "build/$s.o" > "build/$s.ptxas.log" 2>&1 &

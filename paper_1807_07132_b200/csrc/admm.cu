@@ -608,6 +608,62 @@ nadmm_status nadmm_admm_free(nadmm_admm run) {
     return NADMM_OK;
 }
 
+nadmm_status nadmm_sgd_run(const nadmm_shard* shards, int32_t n_local, nadmm_comm comm, const nadmm_sgd_cfg* cfg,
+                           double lambda, double* x_inout, nadmm_metrics_row* rows, int32_t row_cap,
+                           int32_t* epochs_done) {
+    try {
+        if (!shards || n_local < 1) raise(NADMM_ECONFIG, "sync_sgd needs at least one shard");
+        if (!cfg || !x_inout) raise(NADMM_ECONFIG, "cfg and x_inout required");
+        if (!(cfg->eta > 0.0)) raise(NADMM_ECONFIG, "sgd step size must be > 0");
+        if (cfg->epochs < 0) raise(NADMM_ECONFIG, "sgd epochs must be >= 0");
+        std::vector<Shard*> sh;
+        for (int i = 0; i < n_local; ++i) {
+            if (!shards[i]) raise(NADMM_ECONFIG, "null shard");
+            sh.push_back(shards[i]);
+        }
+        Ctx* ctx = sh[0]->ctx;
+        for (Shard* s : sh)
+            if (s->ctx != ctx) raise(NADMM_ECONFIG, "all local shards must share one context");
+        (void)cudaGetLastError();
+        NADMM_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t st = ctx->stream;
+        const int64_t d = sh[0]->d;
+        double* x = nullptr;
+        double* hb = nullptr;
+        NADMM_CUDA(cudaMalloc(&x, sizeof(double) * (size_t)d));
+        NADMM_CUDA(cudaMalloc(&hb, sizeof(double) * 8));
+        struct Free {
+            double* a;
+            double* b;
+            ~Free() {
+                cudaFree(a);
+                cudaFree(b);
+            }
+        } fr{x, hb};
+        NADMM_CUDA(cudaMemcpyAsync(x, x_inout, sizeof(double) * (size_t)d, cudaMemcpyHostToDevice, st));
+        SgdReduce red;
+        if (comm) {
+            red.dev = [&](double* v, int64_t n) {
+                NADMM_NCCL(ncclAllReduce(v, v, (size_t)n, ncclDouble, ncclSum, comm->comm, st));
+            };
+            red.host = [&](double* v, int n) {
+                NADMM_CUDA(cudaMemcpyAsync(hb, v, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+                NADMM_NCCL(ncclAllReduce(hb, hb, (size_t)n, ncclDouble, ncclSum, comm->comm, st));
+                NADMM_CUDA(cudaMemcpyAsync(v, hb, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+                NADMM_CUDA(cudaStreamSynchronize(st));
+            };
+        }
+        const SgdOutcome o = sgd_run(sh, comm ? &red : nullptr, *cfg, lambda, x, rows, row_cap);
+        NADMM_CUDA(cudaMemcpyAsync(x_inout, x, sizeof(double) * (size_t)d, cudaMemcpyDeviceToHost, st));
+        NADMM_CUDA(cudaStreamSynchronize(st));
+        if (epochs_done) *epochs_done = o.epochs;
+        return NADMM_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    }
+}
+
 nadmm_status nadmm_admm_run(const nadmm_shard* shards, int32_t n_local, nadmm_comm comm, const nadmm_admm_cfg* cfg,
                             double* z_out, double* rho_out, nadmm_metrics_row* rows, int32_t row_cap,
                             int32_t* iterations, int32_t* converged) {

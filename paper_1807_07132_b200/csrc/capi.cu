@@ -161,7 +161,7 @@ Shard::~Shard() {
     }
     for (cudaEvent_t e : tl_events) cudaEventDestroy(e);
     for (double** v : {&X, &wt, &vals, &cval, &L0, &P, &U, &Lp, &rowM, &rowA, &part, &blk, &cache_x, &gbase, &scal, &x, &g,
-                       &pd, &r, &dv, &hd, &z, &y, &t, &tmp, &lb_ws})
+                       &pd, &r, &dv, &hd, &z, &y, &t, &tmp, &lb_ws, &sgd_u})
         dev_free(*v);
     dev_free(indptr);
     dev_free(indices);
@@ -169,6 +169,7 @@ Shard::~Shard() {
     dev_free(crow);
     dev_free(labels);
     dev_free(pred);
+    dev_free(sgd_perm);
     dev_free(gbar);
     dev_free(prm);
     dev_free(st);
@@ -645,6 +646,29 @@ nadmm_status nadmm_worker_solve_lbfgs(nadmm_worker w, double rho, const double* 
         const LbfgsResult r = device_lbfgs_solve(s, c, 0.0, true, rho);  // x_local warm start in s.x
         if (x_out) download(x_out, s.x, sizeof(double) * s.d, s.ctx->stream);
         if (stats) *stats = lbfgs_inner_stats(r);
+    });
+}
+
+nadmm_status nadmm_sgd_permutation(uint64_t seed, uint32_t epoch, int64_t n, int32_t* perm) {
+    return guard([&] {
+        if (n < 0 || (n > 0 && !perm)) raise(NADMM_ECONFIG, "bad permutation request");
+        epoch_permutation(nadmm_mix_seed(seed, epoch), n, perm);
+    });
+}
+
+nadmm_status nadmm_worker_sgd_grad(nadmm_worker w, const nadmm_sgd_cfg* cfg, uint32_t iteration, const double* z,
+                                   double* g_out, nadmm_inner_stats* stats) {
+    return guard([&] {
+        if (!w) raise(NADMM_ECONFIG, "null worker");
+        if (!cfg) raise(NADMM_ECONFIG, "sgd session config required");
+        Shard& s = *w->shard;
+        validate_sgd(s, *cfg);
+        check_shard(w->shard);
+        if (!z || !g_out) raise(NADMM_ECONFIG, "z and g_out required");
+        upload(s.z, z, sizeof(double) * s.d, s.ctx->stream);
+        sgd_worker_grad(s, *cfg, iteration, s.z, s.tmp);
+        download(g_out, s.tmp, sizeof(double) * s.d, s.ctx->stream);
+        if (stats) *stats = nadmm_inner_stats{0.0, 1u, 0u, 1u, 0u};  // src/worker.cpp:216-217
     });
 }
 

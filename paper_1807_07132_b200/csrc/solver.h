@@ -1,6 +1,7 @@
 // Host-side solver entry points shared by the C ABI, the worker and the ADMM driver.
 #pragma once
 
+#include <functional>
 #include <vector>
 
 #include "state.h"
@@ -43,6 +44,22 @@ struct LbfgsResult {
 };
 void validate_lbfgs_cfg(const LbfgsCfg& c);
 LbfgsResult device_lbfgs_solve(Shard& s, const LbfgsCfg& cfg, double lambda, bool aug, double rho);
+// Synchronous mini-batch SGD (sgd.cu; src/worker.cpp:197-218).
+void epoch_permutation(uint64_t seed, int64_t n, int32_t* perm);
+void validate_sgd(const Shard& s, const nadmm_sgd_cfg& c);
+void sgd_worker_grad(Shard& s, const nadmm_sgd_cfg& c, uint32_t iteration, const double* z, double* g);
+struct SgdReduce {  // cross-rank sums (NCCL), absent on a single rank
+    std::function<void(double*, int)> host;
+    std::function<void(double*, int64_t)> dev;
+};
+struct SgdOutcome {
+    int epochs = 0;
+    int steps_per_epoch = 0;
+    double f0 = 0.0, final_objective = 0.0;
+};
+SgdOutcome sgd_run(std::vector<Shard*>& shards, const SgdReduce* red, const nadmm_sgd_cfg& cfg, double lambda,
+                   double* x_dev, nadmm_metrics_row* rows, int row_cap);
+
 // InnerStats of an L-BFGS worker round (src/worker.cpp:186-194).
 inline nadmm_inner_stats lbfgs_inner_stats(const LbfgsResult& r) {
     nadmm_inner_stats st{r.final_grad_norm, (uint32_t)r.trace.size(), 0u, 0u, 0u};

@@ -180,6 +180,12 @@ struct Shard {
     // L-BFGS workspace (lbfgs.cu), kept across solves: curvature history + work vectors
     double* lb_ws = nullptr;
     int64_t lb_ws_len = 0;
+    // SGD worker state (sgd.cu): the epoch permutation on the device and the batch coefficients
+    int32_t* sgd_perm = nullptr;
+    int sgd_epoch = -1;
+    uint64_t sgd_seed = 0;
+    double* sgd_u = nullptr;
+    int64_t sgd_u_len = 0;
     void ensure_timers(int n);
     ~Shard();
 };
