@@ -55,7 +55,7 @@ def test_worker_sgd_batch_errors(nadmm, batch):
     X, y = random_dense(rng, 230, 5, 3)
     w = nadmm.Worker(nadmm.Dataset.dense(X, y, 3))
     with pytest.raises(nadmm.ConfigError, match=r"sgd batch size must lie in \[1, local n\]"):
-        w.sgd_grad(nadmm.SgdConfig(batch=batch, steps_per_epoch=1), 0, np.zeros(8))
+        w.sgd_grad(nadmm.SgdConfig(batch=batch, steps_per_epoch=1), 0, np.zeros(10))
 
 
 @pytest.mark.gpu
