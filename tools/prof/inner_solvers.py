@@ -1,5 +1,6 @@
 """Newton-CG vs L-BFGS as the ADMM workers' inner solver (the paper's Fig. 1-style
-comparison) on the bench workload: CIFAR-shaped 50,000 x 3,072, C = 10, 8 ADMM nodes on one GPU,
+comparison) and synchronous mini-batch SGD with the Appendix's step-size sweep (§8f #4; Fig. 2-style)
+on the bench workload: CIFAR-shaped 50,000 x 3,072, C = 10, 8 ADMM nodes on one GPU,
 SPS penalty, lambda = 1e-3. Reports time-to-target theta = (F - F*)/F* <= 0.05 and time per outer
 iteration. usage: python tools/prof/inner_solvers.py [max_outer_iters]"""
 import json
@@ -42,6 +43,23 @@ def main(max_outer: int):
                 "ms_per_outer_iter": 1e3 * rows[-1]["wall_seconds"] / len(rows) if rows else None,
                 "fn_evals_total": int(sum(m["fn_evals"] for m in rows)),
                 "cg_iters_total": int(sum(m["cg_iters"] for m in rows))}
+        print(json.dumps(line), flush=True)
+        out.append(line)
+    # sync-SGD: batch 100 per worker, ceil(n / (m N)) steps per epoch, eta swept by decades
+    n_total = sum(s.n() for s in shards)
+    for eta in [1e-4, 1e-3, 1e-2, 1e-1, 1.0, 10.0]:
+        cfg = nadmm.SgdConfig(eta=eta, batch=100, epochs=5, seed=0)
+        try:
+            r = nadmm.sync_sgd(shards, cfg, lam)
+        except nadmm.SolverError as e:
+            print(json.dumps({"solver": "sync_sgd", "eta": eta, "diverged": str(e)}), flush=True)
+            continue
+        thetas = [(m["train_objective"] - fstar) / fstar for m in r.metrics]
+        line = {"solver": "sync_sgd", "eta": eta, "batch": 100, "epochs": r.epochs,
+                "steps_per_epoch": r.metrics[0]["inner_iterations"] if r.metrics else None,
+                "messages_per_epoch": r.metrics[0]["messages"] if r.metrics else None,
+                "theta_per_epoch": thetas, "seconds": r.metrics[-1]["wall_seconds"] if r.metrics else None,
+                "n_total": n_total}
         print(json.dumps(line), flush=True)
         out.append(line)
     return out
