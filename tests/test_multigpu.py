@@ -31,8 +31,14 @@ def _data():
 
 
 def _cfg(nadmm, penalty):
+    if penalty == "lbfgs":  # L-BFGS inner solver (fixed penalty)
+        return nadmm.AdmmConfig(n_workers=NODES, lam=LAM, stopping=nadmm.StoppingConfig(max_outer_iters=10),
+                                inner_iters=3, inner_solver="lbfgs", lbfgs=nadmm.LbfgsConfig(grad_tol=1e-6))
     return nadmm.AdmmConfig(n_workers=NODES, lam=LAM, penalty=nadmm.PenaltyPolicy(kind=penalty),
                             stopping=nadmm.StoppingConfig(max_outer_iters=25))
+
+
+SGD = dict(eta=0.05, batch=40, epochs=3, seed=4)
 
 
 def _rank(rank, world, port, penalty, out):
@@ -49,15 +55,20 @@ def _rank(rank, world, port, penalty, out):
         shards = [nadmm.Dataset.dense(Xtr[owner == i], ytr[owner == i], C, ctx=ctx) for i in mine]
         uid = nd.share_unique_id(dist, rank, nadmm.Communicator.unique_id)
         comm = nadmm.Communicator(ctx, uid, world, rank)
-        res = nadmm.run_admm(shards, _cfg(nadmm, penalty), nadmm.EvalContext(eval_objective=True), comm)
-        out[rank] = {"z": res.z, "it": res.iterations, "conv": res.converged,
-                     "F": [r["train_objective"] for r in res.metrics]}
+        if penalty == "sgd":
+            res = nadmm.sync_sgd(shards, nadmm.SgdConfig(**SGD), LAM, comm=comm)
+            out[rank] = {"z": res.x, "it": res.epochs, "conv": False,
+                         "F": [r["train_objective"] for r in res.metrics]}
+        else:
+            res = nadmm.run_admm(shards, _cfg(nadmm, penalty), nadmm.EvalContext(eval_objective=True), comm)
+            out[rank] = {"z": res.z, "it": res.iterations, "conv": res.converged,
+                         "F": [r["train_objective"] for r in res.metrics]}
         comm.close()
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("penalty", ["fixed", "spectral"])
+@pytest.mark.parametrize("penalty", ["fixed", "spectral", "lbfgs", "sgd"])
 def test_two_ranks_match_single_process(nadmm, penalty):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs two GPUs")
@@ -66,6 +77,14 @@ def test_two_ranks_match_single_process(nadmm, penalty):
     Xtr, ytr, owner = _data()
     ctx = nadmm.Context(0)
     shards = [nadmm.Dataset.dense(Xtr[owner == i], ytr[owner == i], C, ctx=ctx) for i in range(NODES)]
+    if penalty == "sgd":  # cross-rank sums regroup the worker order: equal to rounding, not bitwise
+        res = nadmm.sync_sgd(shards, nadmm.SgdConfig(**SGD), LAM)
+        for r in range(2):
+            assert out[r]["it"] == res.epochs
+            np.testing.assert_allclose(out[r]["z"], res.x, rtol=1e-9, atol=1e-12)
+            np.testing.assert_allclose(out[r]["F"], [m["train_objective"] for m in res.metrics], rtol=1e-9)
+        np.testing.assert_array_equal(out[0]["z"], out[1]["z"])
+        return
     ref = nadmm.run_admm(shards, _cfg(nadmm, penalty), nadmm.EvalContext(eval_objective=True))
     for r in range(2):
         assert out[r]["it"] == ref.iterations and out[r]["conv"] == ref.converged
