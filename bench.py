@@ -318,10 +318,10 @@ def main():
     rho = 1.0
 
     def e2e_step():
-        hv = 0
-        for i, w in enumerate(workers):
-            _, s = w.solve(rho, zbuf, ybufs[i], cfg.newton, 1, out=xbufs[i])  # x lands in pinned memory
-            hv += s.cg_iters + s.inner_iters
+        # one WorkerPool round through the worker ABI (nadmm_workers_solve): z, y_i host -> device,
+        # the workers' solves (concurrent on the GPU), x_i device -> pinned host memory
+        _, sts = nadmm.workers_solve(workers, rho, zbuf, ybufs, cfg.newton, 1, outs=xbufs)
+        hv = sum(s.cg_iters + s.inner_iters for s in sts)
         S = np.zeros(d + 1)
         for i in range(len(workers)):  # reference coordinator: z_update / y_update
             S[:d] += rho * xbufs[i] - ybufs[i]
@@ -344,7 +344,7 @@ def main():
     hv_e2e = sum_over_ranks(hv_e2e)
     e2e = {"value": hv_e2e / t_e2e, "unit": "Hv/s", "h2d_bytes_per_step": per * 2 * d * 8 * world,
            "d2h_bytes_per_step": per * d * 8 * world,
-           "path": "nadmm_worker_solve per node (scatter z,y_i / gather x_i) + host coordinator"}
+           "path": "nadmm_workers_solve per round (scatter z,y_i / gather x_i for all local nodes) + host coordinator"}
 
     # ---------------- time to target: theta = (F - F*)/F* <= 0.05 ----------------
     ttt = {}

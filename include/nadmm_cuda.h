@@ -209,6 +209,14 @@ nadmm_status nadmm_worker_solve(nadmm_worker w, double rho, const double* z, con
                                 nadmm_inner_stats* stats);
 /* The same round with the L-BFGS inner solver (src/worker.cpp:183-195): cfg->max_iters is replaced
  * by inner_iters; stats.inner_iters = trace length, fn_evals summed, flags bit0 = a Wolfe fallback. */
+/* One scatter -> gather round for several workers of this process (the reference's WorkerPool,
+ * src/worker.cpp:222-240): worker i gets (rho[i], z, y[i]) from host memory and returns x_out[i]
+ * and stats[i], exactly as n calls of nadmm_worker_solve, but the workers run concurrently on the
+ * GPU (NADMM_NODE_STREAMS streams, default 2) with a single synchronisation for the round. */
+nadmm_status nadmm_workers_solve(const nadmm_worker* workers, int32_t n, const double* rho, const double* z,
+                                 const double* const* y, const nadmm_newton_cfg* cfg, int32_t inner_iters,
+                                 double* const* x_out, nadmm_inner_stats* stats);
+
 nadmm_status nadmm_worker_solve_lbfgs(nadmm_worker w, double rho, const double* z, const double* y,
                                       const nadmm_lbfgs_cfg* cfg, int32_t inner_iters, double* x_out,
                                       nadmm_inner_stats* stats);

@@ -31,7 +31,7 @@ __all__ = [
     "AdmmConfig", "EvalContext", "AdmmRunResult", "run_admm", "Communicator", "generate_synthetic",
     "generate_sparse", "partition_owner", "partition", "mix_seed", "default_context", "LoadedData", "read_libsvm",
     "read_idx", "load_libsvm", "load_idx", "LbfgsConfig", "LbfgsIterRecord", "LbfgsResult", "lbfgs_solve",
-    "SgdConfig", "SgdResult", "sgd_permutation", "sync_sgd",
+    "SgdConfig", "SgdResult", "sgd_permutation", "sync_sgd", "workers_solve",
 ]
 
 
@@ -447,6 +447,27 @@ def lbfgs_solve(obj: Objective, x0, cfg: Optional[LbfgsConfig] = None) -> LbfgsR
     recs = [LbfgsIterRecord(r.iter, r.grad_norm, r.step, r.objective, r.fn_evals, bool(r.ls_fallback))
             for r in tr[: min(summ.iterations, cap)]]
     return LbfgsResult(x, recs, bool(summ.converged), summ.final_grad_norm)
+
+
+def workers_solve(workers: Sequence["Worker"], rho, z, ys, cfg: Optional[NewtonConfig] = None, inner_iters: int = 1,
+                  outs=None):
+    """One scatter -> gather round over several workers (the reference's WorkerPool): the workers
+    run concurrently on the GPU; x_i land in `outs[i]` (e.g. pinned float64 buffers) if given."""
+    cfg = cfg or NewtonConfig()
+    n = len(workers)
+    if n == 0:
+        raise ConfigError("at least one worker required")
+    rho = np.ascontiguousarray(np.broadcast_to(np.asarray(rho, dtype=np.float64), (n,)))
+    z = _wvec(workers[0].shard, z, "z")
+    ys = [_wvec(w.shard, y, "y") for w, y in zip(workers, ys)]
+    xs = [w._out(None if outs is None else outs[i]) for i, w in enumerate(workers)]
+    hs = (C.c_void_p * n)(*[w.handle for w in workers])
+    yp = (L.D * n)(*[_dp(y) for y in ys])
+    xp = (L.D * n)(*[_dp(x) for x in xs])
+    st = (L.InnerStats * n)()
+    c = cfg.to_c()
+    _check(L.lib().nadmm_workers_solve(hs, n, _dp(rho), _dp(z), yp, C.byref(c), int(inner_iters), xp, st))
+    return xs, [InnerStats(s.grad_norm, s.inner_iters, s.cg_iters, s.fn_evals, s.flags) for s in st]
 
 
 # ---- synchronous SGD (SPEC.md:446-468; src/worker.cpp:197-218) -----------------------------------

@@ -108,6 +108,8 @@ SIGNATURES = {
     "nadmm_newton_solve": (S, [VP, C.POINTER(NewtonCfg), C.c_double, C.c_int32, C.c_double, D, D, D,
                                C.POINTER(NewtonIter), C.c_int32, C.POINTER(NewtonSummary)]),
     "nadmm_worker_create": (S, [VP, C.POINTER(VP)]),
+    "nadmm_workers_solve": (S, [C.POINTER(VP), C.c_int32, D, D, C.POINTER(D), C.POINTER(NewtonCfg), C.c_int32,
+                                C.POINTER(D), C.POINTER(InnerStats)]),
     "nadmm_worker_sgd_grad": (S, [VP, C.POINTER(SgdCfg), C.c_uint32, D, D, C.POINTER(InnerStats)]),
     "nadmm_sgd_permutation": (S, [C.c_uint64, C.c_uint32, C.c_int64, I32]),
     "nadmm_sgd_run": (S, [C.POINTER(VP), C.c_int32, VP, C.POINTER(SgdCfg), C.c_double, D, C.POINTER(MetricsRow),

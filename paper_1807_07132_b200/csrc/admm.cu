@@ -359,8 +359,33 @@ struct AdmmRun {
     void iterate(nadmm_metrics_row* row) {
         int inner = 0, cg_sum = 0, fe_sum = 0, flags = 0;
         std::vector<char> pending(n_local, 0);
+        // concurrent nodes: node i's solve on node_stream[i % k] (forked from / joined back to st)
+        bool conc = ctx->node_streams > 1 && cfg.inner_solver == 0 && n_local > 1;
+        for (int i = 0; conc && i < n_local; ++i) conc = dmma_supported(*shards[i]);
+        const int ks = conc ? std::min(ctx->node_streams, n_local) : 1;
+        for (int i = 0; i < n_local; ++i) use_layout_split(*shards[i], ks);
+        if (conc) {
+            NADMM_CUDA(cudaEventRecord(ctx->node_fork, st));
+            for (int k2 = 0; k2 < ks; ++k2) NADMM_CUDA(cudaStreamWaitEvent(ctx->node_stream[k2], ctx->node_fork, 0));
+        }
         for (int i = 0; i < n_local; ++i) {  // (1) scatter z / solve (all workers enqueued back to back)
             Shard& s = *shards[i];
+            if (conc) {
+                ctx->stream = ctx->node_stream[i % ks];
+                NADMM_CUDA(cudaMemcpyAsync(s.z, z, sizeof(double) * d, cudaMemcpyDeviceToDevice, ctx->stream));
+                try {
+                    pending[i] = !solve_launch(s, ncfg, 0.0, true, rho[i], cfg.inner_iters);
+                    if (pending[i]) {
+                        solve_readback_async(s);
+                        pending[i] = 3;  // readback enqueued on the node stream
+                    }
+                } catch (...) {
+                    ctx->stream = st;
+                    throw;
+                }
+                ctx->stream = st;
+                continue;
+            }
             NADMM_CUDA(cudaMemcpyAsync(s.z, z, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
             if (cfg.inner_solver == 1) {  // L-BFGS: host-driven line search, synchronous per worker
                 const nadmm_inner_stats lst = lbfgs_inner_stats(device_lbfgs_solve(s, lcfg, 0.0, true, rho[i]));
@@ -375,6 +400,11 @@ struct AdmmRun {
         // the workers' inner stats come back with the iteration's single synchronisation below
         for (int i = 0; i < n_local; ++i)
             if (pending[i] == 1) solve_readback_async(*shards[i]);
+        if (conc)
+            for (int k2 = 0; k2 < ks; ++k2) {
+                NADMM_CUDA(cudaEventRecord(ctx->node_join[k2], ctx->node_stream[k2]));
+                NADMM_CUDA(cudaStreamWaitEvent(st, ctx->node_join[k2], 0));
+            }
         LocalPtrs lp{};  // (2) consensus sum + one allreduce
         lp.n = n_local;
         double rho_sum = 0.0;
@@ -417,7 +447,7 @@ struct AdmmRun {
         for (int i = 0; i < n_local; ++i) {  // gather the workers' inner stats
             Shard& s = *shards[i];
             if (pending[i] == 2) continue;  // L-BFGS stats already gathered
-            SolveResult r = pending[i] ? solve_result(s, ncfg) : solve_collect(s, ncfg, false);
+            SolveResult r = pending[i] ? solve_result(s, ncfg) : solve_collect(s, ncfg, false);  // 1 and 3
             if (r.error) raise((nadmm_status)r.error, "worker inner solve failed");
             inner += r.iterations;
             cg_sum += r.cg_sum;

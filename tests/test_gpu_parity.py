@@ -197,3 +197,24 @@ def test_admm_run_matches_oracle(nadmm, port, penalty):
     yall = np.concatenate([s.labels for s in parts_o])
     full_g = nadmm.Dataset.dense(Xall, yall, C)
     np.testing.assert_array_equal(nadmm.predict(full_g, rg.z), port.predict(oracle.Shard(Xall, yall, C), ro["z"]))
+
+
+def test_workers_round_matches_reference(nadmm, ref):
+    """nadmm_workers_solve (the WorkerPool round, workers concurrent on the GPU) against the
+    reference's run_worker ADMM branch, worker by worker, over several warm-started rounds."""
+    rng = np.random.default_rng(15)
+    parts = [random_dense(rng, 300 + 50 * i, 3072, 10, scale=0.02) for i in range(4)]  # DMMA shards
+    dss = [nadmm.Dataset.dense(X, y, 10) for X, y in parts]
+    rws = [ref.dataset(oracle.Shard(X, y, 10)).worker() for X, y in parts]
+    ws = [nadmm.Worker(ds) for ds in dss]
+    d = dss[0].weight_dim()
+    for k in range(3):
+        z = rng.normal(size=d) * 0.01
+        ys = [rng.normal(size=d) * 0.01 for _ in ws]
+        rho = [1.0, 0.5, 2.0, 1.5]
+        xs, sts = nadmm.workers_solve(ws, rho, z, ys)
+        for i in range(len(ws)):
+            xr, sr = rws[i].solve(rho[i], z, ys[i])
+            assert rel(xs[i], xr) <= TOL_NEWTON
+            assert (sts[i].inner_iters, sts[i].cg_iters, sts[i].fn_evals, sts[i].flags) == \
+                (sr["inner_iters"], sr["cg_iters"], sr["fn_evals"], sr["flags"])
