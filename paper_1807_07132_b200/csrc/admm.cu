@@ -429,8 +429,28 @@ struct AdmmRun {
             ctx->stats.kernel_launches++;
         }
         ++k;
-        if (cfg.eval_objective)  // F_i(z) of the global objective (Eq. (5)) for the metrics stream
-            for (int i = 0; i < n_local; ++i) op_value(*shards[i], z, fz + i, 0, nullptr);
+        if (cfg.eval_objective) {  // F_i(z) of the global objective (Eq. (5)) for the metrics stream
+            if (conc) {  // the value passes of the nodes run concurrently like their solves
+                NADMM_CUDA(cudaEventRecord(ctx->node_fork, st));
+                for (int k2 = 0; k2 < ks; ++k2)
+                    NADMM_CUDA(cudaStreamWaitEvent(ctx->node_stream[k2], ctx->node_fork, 0));
+            }
+            for (int i = 0; i < n_local; ++i) {
+                ctx->stream = conc ? ctx->node_stream[i % ks] : st;
+                try {
+                    op_value(*shards[i], z, fz + i, 0, nullptr);
+                } catch (...) {
+                    ctx->stream = st;
+                    throw;
+                }
+                ctx->stream = st;
+            }
+            if (conc)
+                for (int k2 = 0; k2 < ks; ++k2) {
+                    NADMM_CUDA(cudaEventRecord(ctx->node_join[k2], ctx->node_stream[k2]));
+                    NADMM_CUDA(cudaStreamWaitEvent(st, ctx->node_join[k2], 0));
+                }
+        }
         for (int i = 0; i < n_local; ++i) {
             k_reduce_groups<<<4, 32, 0, st>>>(wpart + (int64_t)i * 6 * kBlockPartials, vg, 4, wred + (int64_t)i * 6);
             ctx->stats.kernel_launches++;

@@ -226,7 +226,7 @@ nadmm_status nadmm_ctx_create(int32_t device, nadmm_ctx* out) {
         c->num_sms = prop.multiProcessorCount;
         NADMM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->node_streams = 2;  // measured: two concurrent ADMM nodes per GPU (+19% on the bench workload)
-        if (const char* ns = getenv("NADMM_NODE_STREAMS")) c->node_streams = std::max(1, std::min(4, atoi(ns)));
+        if (const char* ns = getenv("NADMM_NODE_STREAMS")) c->node_streams = std::max(1, std::min(Ctx::kMaxNodeStreams, atoi(ns)));
         if (c->node_streams > 1) {
             for (int i = 0; i < c->node_streams; ++i) {
                 NADMM_CUDA(cudaStreamCreateWithFlags(&c->node_stream[i], cudaStreamNonBlocking));
@@ -247,7 +247,7 @@ nadmm_status nadmm_ctx_destroy(nadmm_ctx ctx) {
         cudaStreamSynchronize(ctx->stream);
         if (ctx->dctr) cudaFree(ctx->dctr);
         gemm_teardown(*ctx);
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < Ctx::kMaxNodeStreams; ++i) {
             if (ctx->node_stream[i]) cudaStreamDestroy(ctx->node_stream[i]);
             if (ctx->node_join[i]) cudaEventDestroy(ctx->node_join[i]);
         }

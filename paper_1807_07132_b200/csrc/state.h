@@ -72,11 +72,12 @@ struct Ctx {
     nadmm_stats stats{};
     bool timing = false;
     unsigned long long* dctr = nullptr;  // device counters: [0] Hv products applied
-    // concurrent ADMM nodes (NADMM_NODE_STREAMS = 2..4): node i's Newton graph runs on node_stream[i % k],
+    // concurrent ADMM nodes (NADMM_NODE_STREAMS = 2..8): node i's Newton graph runs on node_stream[i % k],
     // each DMMA shard's persistent grid sized to 1/k of the co-resident clusters so all k fit at once
     int node_streams = 1;
-    cudaStream_t node_stream[4] = {nullptr, nullptr, nullptr, nullptr};
-    cudaEvent_t node_fork = nullptr, node_join[4] = {nullptr, nullptr, nullptr, nullptr};
+    static constexpr int kMaxNodeStreams = 8;
+    cudaStream_t node_stream[kMaxNodeStreams] = {};
+    cudaEvent_t node_fork = nullptr, node_join[kMaxNodeStreams] = {};
     void* blas = nullptr;     // cublasHandle_t of the GEMM path (created with the first dense shard)
     void* blas_ws = nullptr;  // its fixed workspace
 };
