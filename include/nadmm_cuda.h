@@ -58,6 +58,9 @@ int32_t nadmm_abi_version(void);
 /* ------------------------------------------------------------------------------------------ */
 nadmm_status nadmm_ctx_create(int32_t device, nadmm_ctx* out);
 nadmm_status nadmm_ctx_destroy(nadmm_ctx ctx);
+/* Concurrent ADMM nodes per GPU (NADMM_NODE_STREAMS, default 4): run_admm / nadmm_workers_solve run
+ * up to this many local nodes' solves at once, each DMMA shard on a 1/k-GPU persistent grid. */
+int32_t nadmm_ctx_node_streams(nadmm_ctx ctx);
 nadmm_status nadmm_ctx_synchronize(nadmm_ctx ctx);
 /* Raw cudaStream_t of the context, for callers that order their own work against it. */
 void* nadmm_ctx_stream(nadmm_ctx ctx);

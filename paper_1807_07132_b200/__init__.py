@@ -111,6 +111,10 @@ class Context:
         except Exception:
             pass
 
+    def node_streams(self) -> int:
+        """Concurrent ADMM nodes per GPU (nadmm_ctx_node_streams)."""
+        return int(L.lib().nadmm_ctx_node_streams(self.handle))
+
     def synchronize(self) -> None:
         _check(L.lib().nadmm_ctx_synchronize(self.handle))
 

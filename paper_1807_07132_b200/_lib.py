@@ -107,6 +107,7 @@ SIGNATURES = {
                               C.POINTER(LbfgsIter), C.c_int32, C.POINTER(NewtonSummary)]),
     "nadmm_newton_solve": (S, [VP, C.POINTER(NewtonCfg), C.c_double, C.c_int32, C.c_double, D, D, D,
                                C.POINTER(NewtonIter), C.c_int32, C.POINTER(NewtonSummary)]),
+    "nadmm_ctx_node_streams": (C.c_int32, [VP]),
     "nadmm_worker_create": (S, [VP, C.POINTER(VP)]),
     "nadmm_workers_solve": (S, [C.POINTER(VP), C.c_int32, D, D, C.POINTER(D), C.POINTER(NewtonCfg), C.c_int32,
                                 C.POINTER(D), C.POINTER(InnerStats)]),
