@@ -197,7 +197,22 @@ __device__ long long g_dmma_trace[64][16];  // per-tile clock64 stamps of CTA 0 
     do { \
         if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (i) < 64) g_dmma_trace[(i)][(k)] = clock64(); \
     } while (0)
+// kernel-level globaltimer stamps of every CTA (ns): 0 entry, 1 setup done, 2 first TMA issued,
+// 3 tile 0 landed (compute warp 0), 4 last phase B done, 5 partial written, 6 final cluster sync, 7 exit
+__device__ long long g_dmma_kst[256][8];
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define DMMA_KST(k) \
+    do { \
+        if (blockIdx.x < 256) g_dmma_kst[blockIdx.x][(k)] = gtimer(); \
+    } while (0)
 #else
+#define DMMA_KST(k) \
+    do { \
+    } while (0)
 #define DMMA_TRACE(i, k) \
     do { \
     } while (0)
@@ -390,6 +405,7 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_pass_kernel(Dmma
     uint64_t* credit = rbar + kDmmaRecvBufs;       // kDmmaRecvBufs: every CTA consumed its copy (CS)
     uint64_t* u_full = credit + kDmmaRecvBufs;     // STAGES: U tile ready (epilogue warps)
 
+    if (threadIdx.x == 0) DMMA_KST(0);
     const int64_t ntiles = (n + BM - 1) / BM;
     int T = cid < ntiles ? (int)((ntiles - 1 - cid) / ncl + 1) : 0;  // this cluster's tiles
     const int64_t rem_f = p - f_cta;
@@ -434,6 +450,7 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_pass_kernel(Dmma
     // CG did not fail (src/newton.cpp:52)
     if (MODE == kModeHv && a.tail == kTailCert && !a.st->cert_act) T = 0;
     if (csize > 1) cluster_sync_all();  // peers' barriers are initialised before any remote traffic
+    if (threadIdx.x == 0) DMMA_KST(1);
 
     auto tile_of = [&](int i) -> int64_t { return (int64_t)cid + (int64_t)i * ncl; };
     const int role_pusher = nc, role_producer = nc + 1, role_epi0 = nc + 2;
@@ -443,6 +460,7 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_pass_kernel(Dmma
         if (lane == 0) {
             for (int i = 0; i < T; ++i) {
                 const int stage = i % STAGES;
+                if (i == 1) DMMA_KST(2);
                 // tile i + kDmmaPrefetch: HBM -> L2 now, so the ring refill after the empty wait hits L2
                 // (the ring alone keeps too few bytes in flight: most stages wait for phase B)
                 if (kDmmaPrefetch > 0 && i + kDmmaPrefetch < T && row_bytes) {
@@ -734,6 +752,7 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_pass_kernel(Dmma
             const int stage = i % STAGES, b = i % kDmmaRedBufs;
             mbar_wait(&full[stage], (uint32_t)((i / STAGES) & 1));
             if (warp == 0) DMMA_TRACE(i, 0);
+            if (i == 0 && warp == 0 && lane == 0) DMMA_KST(3);
             const double* xt = xs + (size_t)stage * BM * S;
             // NCH independent DMMA accumulator chains over the k-steps: a dependent DMMA waits behind the
             // other warps' DMMAs in the shared FP64 pipe, so short chains keep phase A throughput-bound
@@ -854,6 +873,7 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_pass_kernel(Dmma
             if (lane == 0) mbar_arrive(&empty[stage]);
         }
 
+        if (warp == 0 && lane == 0) DMMA_KST(4);
         // ---------------- this cluster's split-K partial of X^T U ----------------
         if (PHASE_B) {
             const int64_t d = (int64_t)K * p;
@@ -881,8 +901,10 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_pass_kernel(Dmma
             }
         }
     }
+    if (threadIdx.x == 0) DMMA_KST(5);
     __syncthreads();
     if (csize > 1) cluster_sync_all();  // no CTA leaves while peers may still target its shared memory
+    if (threadIdx.x == 0) DMMA_KST(6);
     if (PHASE_B && a.tail != kTailNone) {
         // all clusters' partials (and loss slots) written -> the whole (co-resident) grid runs the tail
         grid_barrier(a.done_ctr);
@@ -901,6 +923,7 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_pass_kernel(Dmma
             newton_tail_body(d, a.st, a.prm, a.part, (int)ncl, a.x, a.z, a.y, a.gbase, a.g, a.t, a.blk, (int)ncl,
                              a.scal, a.trace, a.trace_cap, a.done_ctr, misc);
     }
+    if (threadIdx.x == 0) DMMA_KST(7);
 }
 
 }  // namespace nadmm

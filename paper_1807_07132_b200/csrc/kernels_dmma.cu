@@ -367,4 +367,7 @@ void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
 extern "C" __attribute__((visibility("default"))) int nadmm_debug_dmma_trace(long long* out) {
     return (int)cudaMemcpyFromSymbol(out, nadmm::g_dmma_trace, sizeof(nadmm::g_dmma_trace));
 }
+extern "C" __attribute__((visibility("default"))) int nadmm_debug_dmma_kstamps(long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, nadmm::g_dmma_kst, sizeof(nadmm::g_dmma_kst));
+}
 #endif
