@@ -49,7 +49,11 @@ constexpr int kBM = 8;
 struct Pipe {
     int lag, stages;
 };
+#ifdef NADMM_DMMA_PIPE6  // profiling: six-stage rings (needs fewer exchange buffers to fit)
+constexpr Pipe kPipes[] = {{4, 6}, {3, 5}, {2, 5}, {2, 6}, {3, 6}};
+#else
 constexpr Pipe kPipes[] = {{4, 6}, {3, 5}, {2, 5}};
+#endif
 constexpr int kNumPipes = sizeof(kPipes) / sizeof(kPipes[0]);
 
 struct Layout {
@@ -59,7 +63,10 @@ struct Layout {
     double waste = 0.0;
 };
 
-constexpr size_t kSmemLimit = 220 * 1024;
+#ifndef NADMM_DMMA_SMEM_KB
+#define NADMM_DMMA_SMEM_KB 220
+#endif
+constexpr size_t kSmemLimit = NADMM_DMMA_SMEM_KB * 1024;
 
 size_t smem_bytes(int pipe, int nw, int S, int K, int cs) {
     return dmma_smem_bytes(kPipes[pipe].stages, kBM, nw, S, K, cs) + 64;
@@ -149,6 +156,10 @@ int setup_layout(Shard& s, const Layout& L) {
         case 0: return setup_pipe<0>(s, L);
         case 1: return setup_pipe<1>(s, L);
         case 2: return setup_pipe<2>(s, L);
+#ifdef NADMM_DMMA_PIPE6
+        case 3: return setup_pipe<3>(s, L);
+        case 4: return setup_pipe<4>(s, L);
+#endif
         default: return 0;
     }
 }
@@ -178,6 +189,10 @@ void launch_mode(Shard& s, const Layout& L, const DmmaArgs& a, int clusters) {
         case 0: launch_pipe<0, MODE>(s, L, a, clusters); break;
         case 1: launch_pipe<1, MODE>(s, L, a, clusters); break;
         case 2: launch_pipe<2, MODE>(s, L, a, clusters); break;
+#ifdef NADMM_DMMA_PIPE6
+        case 3: launch_pipe<3, MODE>(s, L, a, clusters); break;
+        case 4: launch_pipe<4, MODE>(s, L, a, clusters); break;
+#endif
         default: raise(NADMM_ECONFIG, "dmma: unsupported pipeline");
     }
 }
