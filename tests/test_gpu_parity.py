@@ -218,3 +218,24 @@ def test_workers_round_matches_reference(nadmm, ref):
             assert rel(xs[i], xr) <= TOL_NEWTON
             assert (sts[i].inner_iters, sts[i].cg_iters, sts[i].fn_evals, sts[i].flags) == \
                 (sr["inner_iters"], sr["cg_iters"], sr["fn_evals"], sr["flags"])
+
+
+def test_admm_concurrent_dmma_nodes_match_oracle(nadmm, port):
+    """run_admm over DMMA shards (C - 1 = 9): the nodes' solves run on the context's node streams
+    with quarter-GPU layouts; the loop must still match the oracle's sequential one."""
+    N, C, p = 4, 10, 784
+    Xtr, ytr, _, _ = port.generate_synthetic(2400, p, C, separation=3.0, noise=1.0, seed=4)
+    owner = port.partition_owner(len(ytr), N)
+    parts_o = [oracle.Shard(Xtr[owner == i], ytr[owner == i], C) for i in range(N)]
+    parts_g = [nadmm.Dataset.dense(Xtr[owner == i], ytr[owner == i], C) for i in range(N)]
+    assert parts_g[0].ctx.node_streams() >= 2
+    cfg_o = oracle.admm_cfg(n_workers=N, lam=1e-3, penalty="spectral", max_outer_iters=6)
+    ro = port.admm_run(parts_o, cfg_o)
+    cfg = nadmm.AdmmConfig(n_workers=N, lam=1e-3, penalty=nadmm.PenaltyPolicy(kind="spectral"),
+                           stopping=nadmm.StoppingConfig(max_outer_iters=6))
+    rg = nadmm.run_admm(parts_g, cfg, nadmm.EvalContext(eval_objective=True))
+    assert rg.iterations == ro["iterations"]
+    assert rel(rg.z, ro["z"]) <= TOL_ADMM
+    for mg, mo in zip(rg.metrics, ro["metrics"]):
+        assert abs(mg["train_objective"] - mo["train_objective"]) <= TOL_ADMM * abs(mo["train_objective"])
+        assert mg["cg_iters"] == mo["cg_iters"] and mg["fn_evals"] == mo["fn_evals"]
