@@ -162,11 +162,12 @@ Shard::~Shard() {
     }
     for (cudaEvent_t e : tl_events) cudaEventDestroy(e);
     for (double** v : {&X, &wt, &vals, &cval, &L0, &P, &U, &Lp, &rowM, &rowA, &part, &blk, &cache_x, &gbase, &scal, &x, &g,
-                       &pd, &r, &dv, &hd, &z, &y, &t, &tmp, &lb_ws, &sgd_u})
+                       &pd, &r, &dv, &hd, &z, &y, &t, &tmp, &lb_ws, &sgd_u, &lsum})
         dev_free(*v);
     dev_free(indptr);
     dev_free(indices);
     dev_free(cptr);
+    dev_free(rblk);
     dev_free(crow);
     dev_free(labels);
     dev_free(pred);
@@ -415,6 +416,29 @@ nadmm_status nadmm_shard_csr(nadmm_ctx ctx, const int64_t* indptr, const int32_t
         s->labels = dev_alloc<int32_t>(*s, n + kRowPad);
         NADMM_CUDA(cudaMemsetAsync(s->labels, 0, sizeof(int32_t) * (n + kRowPad), ctx->stream));
         upload(s->labels, labels, sizeof(int32_t) * n, ctx->stream);
+        // column blocks for the rows pass: transposed weights of one block within ~48 MB of L2
+        const int64_t wbytes = 8 * (int64_t)(C - 1) * p;
+        int64_t kBlockBudget = int64_t(48) << 20;
+        if (const char* e = getenv("NADMM_SPARSE_BLOCK_KB")) kBlockBudget = std::max<int64_t>(1, atoll(e)) << 10;
+        std::vector<int64_t> rblk;
+        if (C - 1 <= 32 && wbytes > kBlockBudget) {
+            const int nb = (int)std::min<int64_t>(64, (wbytes + kBlockBudget - 1) / kBlockBudget);
+            const int64_t width = (p + nb - 1) / nb;
+            rblk.resize((size_t)n * (nb + 1));
+            for (int64_t i = 0; i < n; ++i) {  // rows are canonical: columns ascending
+                int64_t q = rp[i];
+                for (int b = 0; b < nb; ++b) {
+                    const int64_t lo = (int64_t)b * width;
+                    while (q < rp[i + 1] && ri[q] < lo) ++q;
+                    rblk[(size_t)i * (nb + 1) + b] = q;
+                }
+                rblk[(size_t)i * (nb + 1) + nb] = rp[i + 1];
+            }
+            s->nblk = nb;
+            s->rblk = dev_alloc<int64_t>(*s, (int64_t)rblk.size());
+            upload(s->rblk, rblk.data(), sizeof(int64_t) * rblk.size(), ctx->stream);
+            s->lsum = dev_alloc<double>(*s, n * (C - 1));
+        }
         alloc_work(*s);
         NADMM_CUDA(cudaStreamSynchronize(ctx->stream));
         *out = s.release();

@@ -51,6 +51,10 @@ struct SpArgs {
     int32_t* pred;
     double* blk;
     const int32_t* guard;
+    // column blocks: this launch covers block `b` of `nb`, row segments from rblk; running logits in lsum
+    int nb, b;
+    const int64_t* rblk;
+    double* lsum;
 };
 
 // Ascending-order sum over classes of a per-lane value (every lane gets the same result).
@@ -69,8 +73,10 @@ __global__ void __launch_bounds__(kSpRowsThreads) sparse_rows_kernel(SpArgs a) {
     const int K = a.K;
     const bool on = lane < K;
     double acc_loss = 0.0;
+    const bool blocked = a.nb > 1;
     for (int64_t i = (int64_t)blockIdx.x * (kSpRowsThreads / 32) + wib; i < a.n; i += warps_total) {
-        const int64_t q0 = a.indptr[i], q1 = a.indptr[i + 1];
+        const int64_t q0 = blocked ? a.rblk[i * (a.nb + 1) + a.b] : a.indptr[i];
+        const int64_t q1 = blocked ? a.rblk[i * (a.nb + 1) + a.b + 1] : a.indptr[i + 1];
         double lg = 0.0;
         int64_t q = q0;
         for (; q + kGather <= q1; q += kGather) {  // kGather gathers in flight, accumulated in CSR order
@@ -89,6 +95,13 @@ __global__ void __launch_bounds__(kSpRowsThreads) sparse_rows_kernel(SpArgs a) {
         for (; q < q1; ++q) {
             const double w = on ? __ldg(a.wt + (int64_t)__ldg(a.indices + q) * K + lane) : 0.0;
             lg += __ldg(a.vals + q) * w;
+        }
+        if (blocked) {  // logits = ((block 0 + block 1) + ...) + last block, in block order
+            if (a.b > 0 && on) lg = a.lsum[i * K + lane] + lg;
+            if (a.b < a.nb - 1) {
+                if (on) a.lsum[i * K + lane] = lg;
+                continue;
+            }
         }
         const int b = a.labels[i];
         if (MODE == kModeLp) {
@@ -132,7 +145,7 @@ __global__ void __launch_bounds__(kSpRowsThreads) sparse_rows_kernel(SpArgs a) {
             }
         }
     }
-    if (MODE == kModeCache || MODE == kModeValue || MODE == kModePredict) {
+    if ((MODE == kModeCache || MODE == kModeValue || MODE == kModePredict) && (!blocked || a.b == a.nb - 1)) {
         if (lane == 0) red[wib] = acc_loss;
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -226,15 +239,21 @@ void sparse_rows_pass(Shard& s, PassMode mode, const double* W, const int32_t* g
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((s.n + 7) / 8, std::min<int64_t>(kBlockPartials, 8LL * s.ctx->num_sms)));
     s.rows_grid = grid;
-    switch (mode) {
-        case kModeCache: sparse_rows_kernel<kModeCache><<<grid, kSpRowsThreads, 0, st>>>(a); break;
-        case kModeHv: sparse_rows_kernel<kModeHv><<<grid, kSpRowsThreads, 0, st>>>(a); break;
-        case kModeLp: sparse_rows_kernel<kModeLp><<<grid, kSpRowsThreads, 0, st>>>(a); break;
-        case kModeValue: sparse_rows_kernel<kModeValue><<<grid, kSpRowsThreads, 0, st>>>(a); break;
-        case kModePredict: sparse_rows_kernel<kModePredict><<<grid, kSpRowsThreads, 0, st>>>(a); break;
+    a.nb = s.nblk;
+    a.rblk = s.rblk;
+    a.lsum = s.lsum;
+    for (int b = 0; b < s.nblk; ++b) {  // one launch per column block (its weights stay L2-resident)
+        a.b = b;
+        switch (mode) {
+            case kModeCache: sparse_rows_kernel<kModeCache><<<grid, kSpRowsThreads, 0, st>>>(a); break;
+            case kModeHv: sparse_rows_kernel<kModeHv><<<grid, kSpRowsThreads, 0, st>>>(a); break;
+            case kModeLp: sparse_rows_kernel<kModeLp><<<grid, kSpRowsThreads, 0, st>>>(a); break;
+            case kModeValue: sparse_rows_kernel<kModeValue><<<grid, kSpRowsThreads, 0, st>>>(a); break;
+            case kModePredict: sparse_rows_kernel<kModePredict><<<grid, kSpRowsThreads, 0, st>>>(a); break;
+        }
+        NADMM_LAUNCH_CHECK();
     }
-    NADMM_LAUNCH_CHECK();
-    s.ctx->stats.kernel_launches += 2;
+    s.ctx->stats.kernel_launches += 1 + s.nblk;
     s.ctx->stats.data_passes++;
 }
 

@@ -185,6 +185,12 @@ struct Shard {
     std::vector<cudaEvent_t> tl_events;
     // L-BFGS workspace (lbfgs.cu), kept across solves: curvature history + work vectors
     int layout_split = 1;  // concurrent shards the DMMA layout was tuned for
+    // column-blocked CSR rows pass (kernels_sparse.cu): when the transposed weights exceed an L2-sized
+    // budget, the rows pass runs once per column block so each block's weights stay L2-resident.
+    // rblk[i * (nblk + 1) + b] = first nonzero of row i in column block b; lsum = running logits
+    int nblk = 1;
+    int64_t* rblk = nullptr;
+    double* lsum = nullptr;
     double* lb_ws = nullptr;
     int64_t lb_ws_len = 0;
     // SGD worker state (sgd.cu): the epoch permutation on the device and the batch coefficients

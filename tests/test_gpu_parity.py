@@ -239,3 +239,25 @@ def test_admm_concurrent_dmma_nodes_match_oracle(nadmm, port):
     for mg, mo in zip(rg.metrics, ro["metrics"]):
         assert abs(mg["train_objective"] - mo["train_objective"]) <= TOL_ADMM * abs(mo["train_objective"])
         assert mg["cg_iters"] == mo["cg_iters"] and mg["fn_evals"] == mo["fn_evals"]
+
+
+@pytest.mark.parametrize("block_kb", [64, 16])
+def test_sparse_column_blocked_rows_pass(nadmm, port, monkeypatch, block_kb):
+    """Shards whose transposed weights exceed the L2 budget run the CSR rows pass once per column
+    block (running logits between blocks); forced here with a small budget: same results."""
+    monkeypatch.setenv("NADMM_SPARSE_BLOCK_KB", str(block_kb))
+    rng = np.random.default_rng(31)
+    n, p, C = 257, 3000, 12  # weights 3000 x 11 doubles = 258 KB -> 5 / 17 column blocks
+    ip, ix, vv, y = random_csr(rng, n, p, C, 0.02)
+    ds = nadmm.Dataset.sparse(ip, ix, vv, y, C, p)
+    sh = oracle.Shard(labels=y, C_=C, csr=(ip, ix, vv), p=p)
+    w = rng.normal(size=sh.d) * 0.5
+    v = rng.normal(size=sh.d)
+    assert abs(nadmm.loss(ds, w, 1e-3) - port.loss(sh, w, 1e-3)) <= TOL_KERNEL * abs(port.loss(sh, w, 1e-3))
+    assert rel(nadmm.gradient(ds, w, 0.0), port.gradient(sh, w, 0.0)) <= TOL_KERNEL
+    assert rel(nadmm.hessian_vec(ds, w, v, 1e-3), port.hessian_vec(sh, w, v, 1e-3)) <= TOL_KERNEL
+    np.testing.assert_array_equal(nadmm.predict(ds, w), port.predict(sh, w))
+    r = nadmm.newton_solve(nadmm.make_softmax_objective(ds, 1e-3), np.zeros(sh.d), nadmm.NewtonConfig(newton_max_iters=3))
+    o = port.newton_solve(sh, 1e-3, np.zeros(sh.d), cfg=list(nadmm.NewtonConfig(newton_max_iters=3).__dict__.values()))
+    _cmp_trace(r.trace, o["trace"])
+    assert rel(r.x, o["x"]) <= TOL_NEWTON
