@@ -80,10 +80,7 @@ void alloc_work(Shard& s) {
     const int64_t nk = (s.n + kRowPad) * s.K;
     s.L0 = dev_alloc<double>(s, nk);
     s.P = dev_alloc<double>(s, nk);
-    // class-per-lane CSR path: U and the transposed weights use a row stride of K rounded up to 4
-    // doubles, so every row gather is whole 32-byte sectors (5 instead of 5.5 on average at K = 19)
-    s.kpad = (s.sparse && s.K <= 32) ? (s.K + 3) & ~3 : s.K;
-    s.U = dev_alloc<double>(s, std::max<int64_t>(nk, (s.n + kRowPad) * (int64_t)s.kpad));
+    s.U = dev_alloc<double>(s, nk);
     s.Lp = dev_alloc<double>(s, nk);
     s.rowM = dev_alloc<double>(s, s.n);
     s.rowA = dev_alloc<double>(s, s.n);
@@ -93,7 +90,7 @@ void alloc_work(Shard& s) {
         s.part_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(2LL * s.ctx->num_sms, cap));
         s.part = dev_alloc<double>(s, s.part_chunks * s.d);
     }
-    if (s.sparse && s.K <= 32) s.wt = dev_alloc<double>(s, (int64_t)s.kpad * s.p);
+    if (s.sparse && s.K <= 32) s.wt = dev_alloc<double>(s, s.d);
     s.blk = dev_alloc<double>(s, (int64_t)kSlotCount * kBlockPartials);
     NADMM_CUDA(cudaMemsetAsync(s.blk, 0, sizeof(double) * kSlotCount * kBlockPartials, s.ctx->stream));
     for (double** v : {&s.x, &s.g, &s.pd, &s.r, &s.dv, &s.hd, &s.z, &s.y, &s.t, &s.tmp, &s.gbase, &s.cache_x}) {

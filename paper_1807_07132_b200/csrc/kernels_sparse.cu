@@ -23,7 +23,7 @@ constexpr int kGather = 8;  // independent gathers in flight per warp
 
 // wt (p x K) = transpose of the block-major W (K x p): 32-column tiles through shared memory so both
 // the reads (along p) and the writes (32*K contiguous doubles) are coalesced.
-__global__ void __launch_bounds__(256) transpose_w_kernel(const double* __restrict__ W, int64_t p, int K, int KW,
+__global__ void __launch_bounds__(256) transpose_w_kernel(const double* __restrict__ W, int64_t p, int K,
                                                           double* __restrict__ wt, const int32_t* guard) {
     if (guard && !*guard) return;
     __shared__ double tile[32][33];
@@ -31,12 +31,9 @@ __global__ void __launch_bounds__(256) transpose_w_kernel(const double* __restri
     for (int64_t j0 = (int64_t)blockIdx.x * 32; j0 < p; j0 += (int64_t)gridDim.x * 32) {
         for (int c = ty; c < K; c += 8) tile[c][tx] = (j0 + tx < p) ? W[(int64_t)c * p + j0 + tx] : 0.0;
         __syncthreads();
-        const int64_t base = j0 * KW;
-        const int64_t total = (p - j0 < 32 ? p - j0 : 32) * KW;
-        for (int q = threadIdx.x; q < total; q += 256) {
-            const int c = q % KW;
-            wt[base + q] = c < K ? tile[c][q / KW] : 0.0;
-        }
+        const int64_t base = j0 * K;
+        const int64_t total = (p - j0 < 32 ? p - j0 : 32) * K;
+        for (int q = threadIdx.x; q < total; q += 256) wt[base + q] = tile[q % K][q / K];
         __syncthreads();
     }
 }
@@ -47,8 +44,8 @@ struct SpArgs {
     const double* vals;
     const int32_t* labels;
     int64_t n, p;
-    int K, KW;          // classes, padded row stride of wt and U
-    const double* wt;  // p x KW interleaved weights
+    int K;
+    const double* wt;  // p x K interleaved weights
     const double* Pin;
     double *L0, *P, *U, *Lp, *rowM, *rowA;
     int32_t* pred;
@@ -91,12 +88,12 @@ __global__ void __launch_bounds__(kSpRowsThreads) sparse_rows_kernel(SpArgs a) {
                 v[k] = __ldg(a.vals + q + k);
             }
 #pragma unroll
-            for (int k = 0; k < kGather; ++k) w[k] = on ? __ldg(a.wt + (int64_t)j[k] * a.KW + lane) : 0.0;
+            for (int k = 0; k < kGather; ++k) w[k] = on ? __ldg(a.wt + (int64_t)j[k] * K + lane) : 0.0;
 #pragma unroll
             for (int k = 0; k < kGather; ++k) lg += v[k] * w[k];
         }
         for (; q < q1; ++q) {
-            const double w = on ? __ldg(a.wt + (int64_t)__ldg(a.indices + q) * a.KW + lane) : 0.0;
+            const double w = on ? __ldg(a.wt + (int64_t)__ldg(a.indices + q) * K + lane) : 0.0;
             lg += __ldg(a.vals + q) * w;
         }
         if (blocked) {  // logits = ((block 0 + block 1) + ...) + last block, in block order
@@ -113,7 +110,7 @@ __global__ void __launch_bounds__(kSpRowsThreads) sparse_rows_kernel(SpArgs a) {
             const double pv = on ? a.Pin[i * K + lane] : 0.0;
             const double e = lg * pv;
             const double rs = class_sum(e, K);  // row_sum(V o P), ascending classes
-            if (on) a.U[i * a.KW + lane] = e - pv * rs;
+            if (on) a.U[i * K + lane] = e - pv * rs;
         } else {
             double m = on ? lg : -INFINITY;
             m = warp_max(m);
@@ -132,7 +129,7 @@ __global__ void __launch_bounds__(kSpRowsThreads) sparse_rows_kernel(SpArgs a) {
                         const double pc = e / alpha;
                         a.L0[i * K + lane] = lg;
                         a.P[i * K + lane] = pc;
-                        a.U[i * a.KW + lane] = (lane == b - 1) ? pc - 1.0 : pc;  // coeff (src/softmax.cpp:86-90)
+                        a.U[i * K + lane] = (lane == b - 1) ? pc - 1.0 : pc;  // coeff (src/softmax.cpp:86-90)
                     }
                 }
             } else {  // kModePredict: first class with P == max; class C only if strictly greater
@@ -163,7 +160,7 @@ __global__ void __launch_bounds__(kSpRowsThreads) sparse_rows_kernel(SpArgs a) {
 // X^T U through the CSC copy, one warp per column, lane = class; fused shifts and dot partials.
 __global__ void __launch_bounds__(256) csc_cols_kernel(const int64_t* __restrict__ cptr,
                                                        const int32_t* __restrict__ crow,
-                                                       const double* __restrict__ cval, int64_t p, int K, int KU,
+                                                       const double* __restrict__ cval, int64_t p, int K,
                                                        const double* __restrict__ U, const double* __restrict__ vin,
                                                        const DevParams* prm, int kind, double* __restrict__ out,
                                                        const double* __restrict__ dotvec, double* blk_slot,
@@ -191,11 +188,11 @@ __global__ void __launch_bounds__(256) csc_cols_kernel(const int64_t* __restrict
                 v[k] = __ldg(cval + q + k);
             }
 #pragma unroll
-            for (int k = 0; k < kGather; ++k) u[k] = on ? U[(int64_t)r[k] * KU + lane] : 0.0;
+            for (int k = 0; k < kGather; ++k) u[k] = on ? U[(int64_t)r[k] * K + lane] : 0.0;
 #pragma unroll
             for (int k = 0; k < kGather; ++k) acc += v[k] * u[k];
         }
-        for (; q < q1; ++q) acc += __ldg(cval + q) * (on ? U[(int64_t)__ldg(crow + q) * KU + lane] : 0.0);
+        for (; q < q1; ++q) acc += __ldg(cval + q) * (on ? U[(int64_t)__ldg(crow + q) * K + lane] : 0.0);
         if (on) {
             const int64_t o = (int64_t)lane * p + j;
             double s = acc;
@@ -218,7 +215,7 @@ bool sparse_lanes_supported(const Shard& s) { return s.sparse && s.K <= 32 && s.
 void sparse_rows_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
     cudaStream_t st = s.ctx->stream;
     const int tg = (int)std::max<int64_t>(1, std::min<int64_t>((s.p + 31) / 32, 8LL * s.ctx->num_sms));
-    transpose_w_kernel<<<tg, 256, 0, st>>>(W, s.p, s.K, s.kpad, s.wt, guard);
+    transpose_w_kernel<<<tg, 256, 0, st>>>(W, s.p, s.K, s.wt, guard);
     NADMM_LAUNCH_CHECK();
     SpArgs a{};
     a.indptr = s.indptr;
@@ -228,7 +225,6 @@ void sparse_rows_pass(Shard& s, PassMode mode, const double* W, const int32_t* g
     a.n = s.n;
     a.p = s.p;
     a.K = s.K;
-    a.KW = s.kpad;
     a.wt = s.wt;
     a.Pin = s.P;
     a.L0 = s.L0;
@@ -265,7 +261,7 @@ int sparse_cols_pass(Shard& s, XtuKind kind, const double* vin, double* out, con
                      const int32_t* guard) {
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((s.p + 7) / 8, std::min<int64_t>(kBlockPartials, 8LL * s.ctx->num_sms)));
-    csc_cols_kernel<<<grid, 256, 0, s.ctx->stream>>>(s.cptr, s.crow, s.cval, s.p, s.K, s.kpad, s.U, vin, s.prm, kind, out,
+    csc_cols_kernel<<<grid, 256, 0, s.ctx->stream>>>(s.cptr, s.crow, s.cval, s.p, s.K, s.U, vin, s.prm, kind, out,
                                                      dotvec, s.blk + (int64_t)dot_slot * kBlockPartials,
                                                      kind == kXtuHv ? s.ctx->dctr : nullptr, guard);
     NADMM_LAUNCH_CHECK();

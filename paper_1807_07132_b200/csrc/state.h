@@ -189,7 +189,6 @@ struct Shard {
     // budget, the rows pass runs once per column block so each block's weights stay L2-resident.
     // rblk[i * (nblk + 1) + b] = first nonzero of row i in column block b; lsum = running logits
     int nblk = 1;
-    int kpad = 0;  // row stride of U and of the transposed weights on the class-per-lane CSR path
     int64_t* rblk = nullptr;
     double* lsum = nullptr;
     double* lb_ws = nullptr;
