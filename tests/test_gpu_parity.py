@@ -218,6 +218,14 @@ def test_workers_round_matches_reference(nadmm, ref):
             assert rel(xs[i], xr) <= TOL_NEWTON
             assert (sts[i].inner_iters, sts[i].cg_iters, sts[i].fn_evals, sts[i].flags) == \
                 (sr["inner_iters"], sr["cg_iters"], sr["fn_evals"], sr["flags"])
+    # inner_iters > 1 needs a host decision per Newton iteration: the round runs the workers in turn
+    z = rng.normal(size=d) * 0.01
+    ys = [rng.normal(size=d) * 0.01 for _ in ws]
+    xs, sts = nadmm.workers_solve(ws, 1.0, z, ys, inner_iters=2)
+    for i in range(len(ws)):
+        xr, sr = rws[i].solve(1.0, z, ys[i], inner_iters=2)
+        assert rel(xs[i], xr) <= TOL_NEWTON
+        assert sts[i].inner_iters == sr["inner_iters"] and sts[i].cg_iters == sr["cg_iters"]
 
 
 def test_admm_concurrent_dmma_nodes_match_oracle(nadmm, port):
