@@ -256,6 +256,9 @@ void use_layout_split(Shard& s, int split) {
     if (split < 1) split = 1;
     if (s.layout_split == split || !dmma_supported(s)) return;
     invalidate_graphs(s);
+    // the grid-barrier counters are multiples of the grid size that last used them: a new grid size
+    // needs them restarted (stream-ordered after all earlier work on the shard)
+    NADMM_CUDA(cudaMemsetAsync(s.gbar, 0, 8 * sizeof(unsigned long long), s.ctx->stream));
     dmma_setup(s, split);
 }
 
