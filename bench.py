@@ -321,23 +321,30 @@ def main():
     ybufs = [_t.zeros(d, dtype=_t.float64).pin_memory().numpy() for _ in mine]
     xbufs = [_t.zeros(d, dtype=_t.float64).pin_memory().numpy() for _ in mine]
     rho = 1.0
+    coord_S = np.zeros(d + 1)  # coordinator scratch, allocated once
+    coord_t = np.empty(d)
 
     def e2e_step():
         # one WorkerPool round through the worker ABI (nadmm_workers_solve): z, y_i host -> device,
         # the workers' solves (concurrent on the GPU), x_i device -> pinned host memory
         _, sts = nadmm.workers_solve(workers, rho, zbuf, ybufs, cfg.newton, 1, outs=xbufs)
         hv = sum(s.cg_iters + s.inner_iters for s in sts)
-        S = np.zeros(d + 1)
+        S = coord_S
+        S.fill(0.0)
         for i in range(len(workers)):  # reference coordinator: z_update / y_update
-            S[:d] += rho * xbufs[i] - ybufs[i]
+            np.multiply(xbufs[i], rho, out=coord_t)
+            np.subtract(coord_t, ybufs[i], out=coord_t)
+            np.add(S[:d], coord_t, out=S[:d])
         S[d] = rho * len(workers)
         if dist:
             tS = _t.from_numpy(S)
             dist.all_reduce(tS)
             S = tS.numpy()
-        zbuf[:] = S[:d] / (LAM + S[d])
+        np.divide(S[:d], LAM + S[d], out=zbuf)
         for i in range(len(workers)):
-            ybufs[i][:] = ybufs[i] + rho * (zbuf - xbufs[i])
+            np.subtract(zbuf, xbufs[i], out=coord_t)
+            np.multiply(coord_t, rho, out=coord_t)
+            np.add(ybufs[i], coord_t, out=ybufs[i])
         return hv
 
     for _ in range(args.warmup):
