@@ -317,40 +317,42 @@ def main():
 
     d = (C - 1) * P
     workers = [nadmm.Worker(s) for s in shards]
-    zbuf = _t.zeros(d, dtype=_t.float64).pin_memory().numpy()
-    ybufs = [_t.zeros(d, dtype=_t.float64).pin_memory().numpy() for _ in mine]
-    xbufs = [_t.zeros(d, dtype=_t.float64).pin_memory().numpy() for _ in mine]
+    # host state of the coordinator in pinned memory: z, and one row per local worker of y_i / x_i
+    z_h = _t.zeros(d, dtype=_t.float64).pin_memory()
+    Y_h = _t.zeros(len(mine), d, dtype=_t.float64).pin_memory()
+    X_h = _t.zeros(len(mine), d, dtype=_t.float64).pin_memory()
+    zbuf = z_h.numpy()
+    ybufs = [row.numpy() for row in Y_h]
+    xbufs = [row.numpy() for row in X_h]
     rho = 1.0
     # coordinator scratch, allocated once; with N > 1 the z_update sum is reduced over NCCL through
     # a device staging copy (the K8 collective) instead of over gloo on host memory
     pin_S = _t.zeros(d + 1, dtype=_t.float64).pin_memory()
-    coord_S = pin_S.numpy()
-    coord_t = np.empty(d)
+    T_h = _t.empty(len(mine), d, dtype=_t.float64)
     nccl_grp = dist.new_group(backend="nccl") if dist else None
     dev_S = _t.empty(d + 1, dtype=_t.float64, device=f"cuda:{local}") if dist else None
+    # the coordinator's vector updates use up to 8 of this rank's host cores (torchrun sets
+    # OMP_NUM_THREADS=1 per rank; more threads than that measured slower on 221 KB vectors)
+    _t.set_num_threads(max(1, min(8, (os.cpu_count() or 1) // world)))
 
     def e2e_step():
         # one WorkerPool round through the worker ABI (nadmm_workers_solve): z, y_i host -> device,
         # the workers' solves (concurrent on the GPU), x_i device -> pinned host memory
         _, sts = nadmm.workers_solve(workers, rho, zbuf, ybufs, cfg.newton, 1, outs=xbufs)
         hv = sum(s.cg_iters + s.inner_iters for s in sts)
-        S = coord_S
-        S.fill(0.0)
-        for i in range(len(workers)):  # reference coordinator: z_update / y_update
-            np.multiply(xbufs[i], rho, out=coord_t)
-            np.subtract(coord_t, ybufs[i], out=coord_t)
-            np.add(S[:d], coord_t, out=S[:d])
-        S[d] = rho * len(workers)
+        # reference coordinator: z_update / y_update
+        _t.mul(X_h, rho, out=T_h)
+        T_h.sub_(Y_h)
+        _t.sum(T_h, 0, out=pin_S[:d])
+        pin_S[d] = rho * len(workers)
         if dist:
             dev_S.copy_(pin_S, non_blocking=True)
             dist.all_reduce(dev_S, group=nccl_grp)
             pin_S.copy_(dev_S, non_blocking=True)
             _t.cuda.current_stream().synchronize()
-        np.divide(S[:d], LAM + S[d], out=zbuf)
-        for i in range(len(workers)):
-            np.subtract(zbuf, xbufs[i], out=coord_t)
-            np.multiply(coord_t, rho, out=coord_t)
-            np.add(ybufs[i], coord_t, out=ybufs[i])
+        _t.div(pin_S[:d], LAM + pin_S[d], out=z_h)
+        _t.sub(z_h, X_h, out=T_h)
+        Y_h.add_(T_h, alpha=rho)
         return hv
 
     for _ in range(args.warmup):
