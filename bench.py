@@ -331,9 +331,10 @@ def main():
     T_h = _t.empty(len(mine), d, dtype=_t.float64)
     nccl_grp = dist.new_group(backend="nccl") if dist else None
     dev_S = _t.empty(d + 1, dtype=_t.float64, device=f"cuda:{local}") if dist else None
-    # the coordinator's vector updates use up to 8 of this rank's host cores (torchrun sets
-    # OMP_NUM_THREADS=1 per rank; more threads than that measured slower on 221 KB vectors)
-    _t.set_num_threads(max(1, min(8, (os.cpu_count() or 1) // world)))
+    # the coordinator's vector updates use up to 8 host threads, at most half of this rank's share
+    # of the cores (torchrun sets OMP_NUM_THREADS=1 per rank; more threads, or all cores busy next
+    # to the CUDA / NCCL host threads, measured slower on these 221 KB vectors)
+    _t.set_num_threads(max(1, min(8, (os.cpu_count() or 1) // (2 * world))))
 
     def e2e_step():
         # one WorkerPool round through the worker ABI (nadmm_workers_solve): z, y_i host -> device,
