@@ -400,6 +400,9 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
+        # torch and the reference share one libgomp: undo the e2e coordinator's thread cap so the
+        # reference's OpenMP regions get the `cores` this line reports
+        torch.set_num_threads(threads)
         kind, hv, dt = reference_worker_bench(Xtr[owner == 0], ytr[owner == 0], args.cpu_steps, 1, threads)
         cpu = {"value": hv / dt, "unit": "Hv/s", "cores": threads, "kind": kind,
                "sample": f"{args.cpu_steps} run_worker ADMM solves of node 0 (6250x3072) after 1 warm-up"}
