@@ -16,8 +16,11 @@ SPS; the F(z) monitoring pass is left to the time-to-target leg). `value` = shar
 Hessian-vector products applied per second on device-resident data (whole job, max-over-ranks
 device time); `e2e` = the same metric
 through the reference-facing worker ABI (nadmm_worker_solve: z, y_i host->device, x_i device->host
-every step, reference-style host coordinator). `--impl reference` times the reference's own CPU
-worker solve (oracle/_ref: the reference sources built against the Eigen stand-in) on this host.
+every step, host coordinator with SPS). `--impl reference` times the reference's own CPU implementation
+of the same step (oracle/_ref: the reference's worker solves, built from its sources against the Eigen
+stand-in, on a WorkerPool of host threads, plus the port's coordinator -- the reference ships none) on
+this host, without loading the product library. At N = 1 the bench also runs that CPU reference on the
+same time-to-target run and reports a `parity` block (iteration trace, F(z^k), z, test predictions).
 """
 from __future__ import annotations
 
@@ -110,61 +113,200 @@ def hv_bytes(n_loc: int) -> int:
     return 8 * n_loc * P + 8 * n_loc * K + 16 * P * K
 
 
-def reference_worker_bench(Xs, ys, steps: int, warmup: int, threads: int):
-    """The reference's own worker solve (run_worker ADMM branch) on host cores, per shard."""
+def lscpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def ref_admm_cfg(oracle, max_outer=100000):
+    return oracle.admm_cfg(n_workers=NODES, lam=LAM, penalty="spectral", max_outer_iters=max_outer)
+
+
+def ref_shards(oracle, r):
+    """The bench workload's 8 ADMM node shards from the REFERENCE's own generator / partition
+    (oracle/_ref: src/data_io.cpp:300-370) -- the reference arm never loads the product library."""
+    Xtr, ytr, Xte, yte = r.generate_synthetic(N_TOTAL, P, C, SEP, NOISE, SEED)
+    owner = r.partition_owner(len(ytr), NODES)
+    return [oracle.Shard(Xtr[owner == i], ytr[owner == i], C) for i in range(NODES)], (Xtr, ytr, Xte, yte)
+
+
+def ref_time_to_target(oracle, r, shards, f_star, max_outer=60, budget_s=120.0):
+    """The CPU reference's Newton-ADMM run (reference worker solves on a WorkerPool of host threads +
+    the port coordinator) until theta = (F(z^k) - F*)/F* <= THETA_TARGET; the clock covers solves,
+    coordinator and the F(z) evaluation, like the GPU's time-to-target leg."""
+    run = oracle.RefAdmm(r, shards, ref_admm_cfg(oracle, max_outer), workers_parallel=True, eval_objective=True)
+    t0 = time.perf_counter()
+    hit_t = hit_k = None
+    try:
+        while run.k < max_outer:
+            row = run.step()
+            row["wall_seconds"] = time.perf_counter() - t0
+            row["theta"] = (row["train_objective"] - f_star) / f_star
+            if row["theta"] <= THETA_TARGET:
+                hit_t, hit_k = row["wall_seconds"], row["iteration"]
+                break
+            if row["wall_seconds"] > budget_s:
+                break
+    finally:
+        run.close()
+    return run, hit_t, hit_k, time.perf_counter() - t0
+
+
+def load_f_star():
+    """F* of the bench workload (compute_reference semantics) as recorded by this
+    bench's own time-to-target leg in profiles/r2_fstar.json (GPU Newton solve at cg_tol 1e-10,
+    certified by the CPU reference's gradient at x*); the reference arm uses it as the target."""
+    try:
+        return float(json.loads((ROOT / "profiles" / "r2_fstar.json").read_text())["f_star"])
+    except Exception:
+        return None
+
+
+F_STAR = load_f_star()
+
+
+def compute_f_star(nadmm, ctx, Xtr, ytr, d):
+    """compute_reference: single-node Newton at cg_tol 1e-10, cg_max 200,
+    grad_tol 1e-10 on the full training set (GPU), then a certificate from the CPU REFERENCE:
+    its loss and gradient at x* (oracle/_ref). The objective is lambda-strongly convex, so
+    F(x*) - min F <= |grad F(x*)|^2 / (2 lambda): a small reference gradient norm proves x* optimal."""
+    full = nadmm.Dataset.dense(Xtr, ytr, C, ctx=ctx)
+    res = nadmm.newton_solve(nadmm.make_softmax_objective(full, LAM), np.zeros(d),
+                             nadmm.NewtonConfig(cg_tol=1e-10, cg_max_iters=200, grad_tol=1e-10,
+                                                newton_max_iters=100))
+    f_gpu = res.trace[-1].objective if res.trace else nadmm.loss(full, res.x, LAM)
+    full.close()
+    info = {"gpu_newton_iters": len(res.trace), "gpu_converged": bool(res.converged),
+            "gpu_final_grad_norm": float(res.final_grad_norm)}
+    if not res.converged:
+        print(f"[bench] WARNING: compute_reference did not converge (|g| = {res.final_grad_norm:.3e})",
+              file=sys.stderr)
+    try:
+        import oracle
+
+        r = oracle.ref()
+        if r is not None:
+            rd = r.dataset(oracle.Shard(Xtr, ytr, C))
+            f_cpu = rd.loss(res.x, LAM)
+            g = rd.gradient(res.x, LAM)
+            gn = float(np.linalg.norm(g))
+            info.update({"cpu_reference_f": f_cpu, "rel_diff_gpu_vs_cpu_f": abs(f_gpu - f_cpu) / abs(f_cpu),
+                         "cpu_reference_grad_norm": gn, "optimality_gap_bound": gn * gn / (2 * LAM)})
+            del rd
+    except Exception as e:  # the certificate is a check, never a dependency of the GPU number
+        info["cpu_check_error"] = str(e)
+    return f_gpu, info
+
+
+def cpu_reference_leg(Xtr, ytr, Xte, yte, owner, f_star, rows_gpu, z_gpu, pred_gpu, args):
+    """Rank 0 at N = 1: the CPU reference runs the same Newton-ADMM (reference worker solves +
+    the port coordinator) to the same target; the GPU run's per-iteration trace, z and test
+    predictions are compared with it (the bench's parity block), and its solve rate is the
+    cpu_baseline (host cores, same workload)."""
     import oracle
+    import torch
 
-    os.environ["OMP_NUM_THREADS"] = str(threads)
     r = oracle.ref()
-    kind = "reference"
-    if r is None:  # reference build unavailable -> C restatement
-        kind = "port"
-    sh = oracle.Shard(Xs, ys, C)
-    d = sh.d
-    rng = np.random.default_rng(0)
-    if kind == "reference":
-        w = r.dataset(sh).worker()
-        solve = lambda z, y: w.solve(1.0, z, y)
-    else:
-        P_ = oracle.Port()
-        state = {"x": np.zeros(d)}
-
-        def solve(z, y):
-            o = P_.newton_solve(sh, 0.0, state["x"], cfg=list(oracle.DEFAULT_NEWTON[:6]) + [1], rho=1.0, z=z, y=y)
-            state["x"] = o["x"]
-            tr = o["trace"]
-            return o["x"], {"cg_iters": sum(t["cg_iters"] for t in tr), "inner_iters": len(tr)}
-    z = np.zeros(d)
-    for _ in range(warmup):
-        solve(z, np.zeros(d))
-    hv, t0 = 0, time.perf_counter()
-    for k in range(steps):
-        z = rng.normal(size=d) * 1e-3
-        x, st = solve(z, np.zeros(d))
-        hv += int(st["cg_iters"]) + int(st["inner_iters"])  # CG Hv + certificate Hv per Newton step
-    dt = time.perf_counter() - t0
-    return kind, hv, dt
+    if r is None:
+        return {"skipped": "oracle/_ref not built"}, None
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)  # torch and the reference share one libgomp
+    shards = [oracle.Shard(Xtr[owner == i], ytr[owner == i], C) for i in range(NODES)]
+    k_gpu = len(rows_gpu)
+    run, hit_t, hit_k, spent = ref_time_to_target(oracle, r, shards, f_star, max_outer=max(k_gpu, 1) + 5,
+                                                  budget_s=float(os.environ.get("NADMM_CPU_BUDGET_S", 150)))
+    n = min(k_gpu, len(run.metrics))
+    same_trace = all((a["cg_iters"], a["fn_evals"], a["flags"]) == (b["cg_iters"], b["fn_evals"], b["flags"])
+                     for a, b in zip(rows_gpu[:n], run.metrics[:n]))
+    obj_diff = max((abs(a["train_objective"] - b["train_objective"]) / abs(b["train_objective"])
+                    for a, b in zip(rows_gpu[:n], run.metrics[:n])), default=None)
+    rho_diff = max((abs(a["rho_mean"] - b["rho_mean"]) / abs(b["rho_mean"])
+                    for a, b in zip(rows_gpu[:n], run.metrics[:n])), default=None)
+    z_diff = None
+    pred_same = None
+    if run.k == k_gpu:
+        z_diff = float(np.abs(z_gpu - run.z).max() / max(np.abs(run.z).max(), 1e-300))
+        pred_cpu = r.dataset(oracle.Shard(Xte, yte, C)).predict(run.z)
+        pred_same = bool(np.array_equal(pred_cpu, pred_gpu))
+    tol = 1e-9
+    parity = {"reference": "oracle/_ref worker solves (reference sources) + port coordinator, same data/config",
+              "outer_iters_to_target": {"gpu": k_gpu, "cpu_reference": hit_k},
+              "iterations_compared": n, "identical_inner_trace": same_trace,
+              "max_rel_diff_F_zk": obj_diff, "max_rel_diff_rho_mean": rho_diff, "rel_diff_z_final": z_diff,
+              "test_predictions_identical": pred_same, "tolerance": tol,
+              "pass": bool(hit_k == k_gpu and same_trace and obj_diff is not None and obj_diff <= tol
+                           and z_diff is not None and z_diff <= tol and pred_same)}
+    cpu = {"value": run.hv / max(run.solve_seconds, 1e-9), "unit": "Hv/s", "cores": cores, "kind": "reference",
+           "cpu_model": lscpu_model(), "time_to_target_s": hit_t, "ttt_outer_iters": hit_k,
+           "sample": f"{len(run.metrics)} outer iterations of the same 8-node SPS run to theta <= {THETA_TARGET} "
+                     f"({spent:.1f} s); Hv/s over the worker solves (8 worker threads x "
+                     f"{max(1, cores // NODES)} OpenMP threads)"}
+    return parity, cpu
 
 
 def run_reference_arm(args):
+    """`--impl reference`: the reference's own CPU implementation of the path (oracle/_ref: the
+    reference sources built against the Eigen stand-in, plus the port's coordinator since the
+    reference ships none) on the same config: one step = one outer Newton-ADMM iteration of the
+    8-node SPS consensus loop, the 8 workers' solves on a WorkerPool of host threads
+    (src/worker.cpp:225-242) with cores/8 OpenMP threads each."""
     rank = env_int("RANK", 0)
     if rank != 0:
         return
-    import paper_1807_07132_b200 as nadmm
+    import oracle
 
-    Xtr, ytr, _, _ = nadmm.generate_synthetic(N_TOTAL, P, C, SEP, NOISE, SEED)
-    owner = nadmm.partition_owner(len(ytr), NODES)
-    Xs, ys = Xtr[owner == 0], ytr[owner == 0]
-    threads = os.cpu_count() or 1
-    kind, hv, dt = reference_worker_bench(Xs, ys, args.steps, args.warmup, threads)
+    r = oracle.ref()
+    if r is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libnadmm_ref.so not built"}), flush=True)
+        return
+    cores = os.cpu_count() or 1
+    shards, _ = ref_shards(oracle, r)
+    run = oracle.RefAdmm(r, shards, ref_admm_cfg(oracle), workers_parallel=True)
+    for _ in range(args.warmup):
+        run.step()
+    hv0, t0 = run.hv, time.perf_counter()
+    for _ in range(args.steps):
+        run.step()
+    dt = time.perf_counter() - t0
+    hv = run.hv - hv0
+    run.close()
     v = hv / dt
+    # "as designed": one thread per worker (the reference's WorkerPool with single-threaded Eigen,
+    # no OpenMP in proj/CMakeLists.txt:1-6) -- one step, fresh state
+    one = oracle.RefAdmm(r, shards, ref_admm_cfg(oracle), workers_parallel=True, threads_per_worker=1)
+    ta = time.perf_counter()
+    one.step()
+    ta = time.perf_counter() - ta
+    as_designed = {"value": one.hv / ta, "unit": "Hv/s", "cores": NODES, "sample": "1 outer iteration, 8 worker "
+                   "threads x 1 OpenMP thread (WorkerPool + single-threaded Eigen)"}
+    one.close()
+    ttt = {}
+    if not args.no_ttt and F_STAR is not None:
+        run2, hit_t, hit_k, spent = ref_time_to_target(oracle, r, shards, F_STAR)
+        ttt = {"time_to_target_s": hit_t, "ttt_outer_iters": hit_k, "theta_target": THETA_TARGET, "f_star": F_STAR,
+               "f_star_source": "profiles/r2_fstar.json (GPU compute_reference, certified by the CPU reference "
+                                "gradient at x*)", "ttt_cpu_seconds_spent": spent}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Hv/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "sample": "one ADMM node (6250x3072) worker solve per step"},
-            "cpu_baseline": {"value": v, "unit": "Hv/s", "cores": threads, "kind": kind,
-                             "sample": f"{args.steps} run_worker ADMM solves of node 0 (6250x3072, 10 CG + cert Hv each)"},
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generate_synthetic: separation 1, noise 1, seed 0)",
+            "config": {"workload": WORKLOAD, "n_train": int(sum(s.n for s in shards)), "p": P, "classes": C,
+                       "lambda": LAM, "admm_nodes": NODES, "inner_iters": 1, "cg_max_iters": 10, "ls_max_iters": 10,
+                       "penalty": "spectral (SPS, rho0=1, T_f=2)"},
+            "cpu_baseline": {"value": v, "unit": "Hv/s", "cores": cores, "kind": "reference",
+                             "cpu_model": lscpu_model(),
+                             "sample": f"{args.steps} outer iterations of the 8-node SPS consensus loop after "
+                                       f"{args.warmup} warm-up; 8 worker threads x {max(1, cores // NODES)} OpenMP "
+                                       "threads (oracle/_ref reference worker solves + port coordinator)"},
+            "as_designed": as_designed,
             "e2e": {"value": v, "unit": "Hv/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    line.update(ttt)
     print(json.dumps(line), flush=True)
 
 
@@ -176,7 +318,6 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-target run")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
-    ap.add_argument("--cpu-steps", type=int, default=12)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: W >= 3
@@ -314,47 +455,44 @@ def main():
 
     # ---------------- e2e: reference-facing worker ABI with host buffers ----------------
     import torch as _t
+    from paper_1807_07132_b200 import dist as ndist
 
     d = (C - 1) * P
     workers = [nadmm.Worker(s) for s in shards]
-    # host state of the coordinator in pinned memory: z, and one row per local worker of y_i / x_i
-    z_h = _t.zeros(d, dtype=_t.float64).pin_memory()
+    # the coordinator's state in pinned host memory: y_i rows are scattered, x_i rows gathered
+    # (device -> pinned host) by nadmm_workers_solve every round
     Y_h = _t.zeros(len(mine), d, dtype=_t.float64).pin_memory()
     X_h = _t.zeros(len(mine), d, dtype=_t.float64).pin_memory()
-    zbuf = z_h.numpy()
-    ybufs = [row.numpy() for row in Y_h]
+    z_h = _t.zeros(d, dtype=_t.float64).pin_memory()
     xbufs = [row.numpy() for row in X_h]
-    rho = 1.0
-    # coordinator scratch, allocated once; with N > 1 the z_update sum is reduced over NCCL through
-    # a device staging copy (the K8 collective) instead of over gloo on host memory
-    pin_S = _t.zeros(d + 1, dtype=_t.float64).pin_memory()
-    T_h = _t.empty(len(mine), d, dtype=_t.float64)
+    Xn, zbuf = X_h.numpy(), z_h.numpy()
+    # with N > 1 the coordinator's [sum(rho x - y) | sum rho] is reduced over NCCL through a device
+    # staging copy (the one consensus collective) instead of over gloo on host memory
     nccl_grp = dist.new_group(backend="nccl") if dist else None
     dev_S = _t.empty(d + 1, dtype=_t.float64, device=f"cuda:{local}") if dist else None
-    # the coordinator's vector updates use up to 8 host threads, at most half of this rank's share
-    # of the cores (torchrun sets OMP_NUM_THREADS=1 per rank; more threads, or all cores busy next
-    # to the CUDA / NCCL host threads, measured slower on these 221 KB vectors)
+    pin_S = _t.zeros(d + 1, dtype=_t.float64).pin_memory() if dist else None
+
+    def nccl_sum(buf):
+        pin_S.numpy()[:] = buf
+        dev_S.copy_(pin_S, non_blocking=True)
+        dist.all_reduce(dev_S, group=nccl_grp)
+        pin_S.copy_(dev_S, non_blocking=True)
+        _t.cuda.current_stream().synchronize()
+        buf[:] = pin_S.numpy()
+
+    coord = ndist.HostCoordinator(d, LAM, len(mine), penalty="spectral", allreduce=nccl_sum if dist else None,
+                                  y=Y_h.numpy())
+    ybufs = [row for row in coord.y]
     _t.set_num_threads(max(1, min(8, (os.cpu_count() or 1) // (2 * world))))
 
     def e2e_step():
-        # one WorkerPool round through the worker ABI (nadmm_workers_solve): z, y_i host -> device,
-        # the workers' solves (concurrent on the GPU), x_i device -> pinned host memory
-        _, sts = nadmm.workers_solve(workers, rho, zbuf, ybufs, cfg.newton, 1, outs=xbufs)
-        hv = sum(s.cg_iters + s.inner_iters for s in sts)
-        # reference coordinator: z_update / y_update
-        _t.mul(X_h, rho, out=T_h)
-        T_h.sub_(Y_h)
-        _t.sum(T_h, 0, out=pin_S[:d])
-        pin_S[d] = rho * len(workers)
-        if dist:
-            dev_S.copy_(pin_S, non_blocking=True)
-            dist.all_reduce(dev_S, group=nccl_grp)
-            pin_S.copy_(dev_S, non_blocking=True)
-            _t.cuda.current_stream().synchronize()
-        _t.div(pin_S[:d], LAM + pin_S[d], out=z_h)
-        _t.sub(z_h, X_h, out=T_h)
-        Y_h.add_(T_h, alpha=rho)
-        return hv
+        # one WorkerPool round through the worker ABI (nadmm_workers_solve): z and y_i host -> device
+        # (the reference's scatter sends z to every worker), the solves (concurrent on the GPU),
+        # x_i device -> pinned host; then the host coordinator with spectral penalty selection
+        zbuf[:] = coord.z
+        _, sts = nadmm.workers_solve(workers, coord.rho, zbuf, ybufs, cfg.newton, 1, outs=xbufs)
+        coord.step(Xn)
+        return sum(s.cg_iters + s.inner_iters for s in sts)
 
     for _ in range(args.warmup):
         e2e_step()
@@ -363,49 +501,41 @@ def main():
     hv_e2e = sum(e2e_step() for _ in range(args.steps))
     t_e2e = max_over_ranks(time.perf_counter() - t0)
     hv_e2e = sum_over_ranks(hv_e2e)
-    coord_bytes = (d + 1) * 8 * world if dist else 0  # z_update sum staged through HBM for NCCL
+    coord_bytes = (d + 1) * 8 * world if dist else 0  # coordinator sum staged through HBM for NCCL
     e2e = {"value": hv_e2e / t_e2e, "unit": "Hv/s", "h2d_bytes_per_step": per * 2 * d * 8 * world + coord_bytes,
            "d2h_bytes_per_step": per * d * 8 * world + coord_bytes,
-           "path": "nadmm_workers_solve per round (scatter z,y_i / gather x_i for all local nodes) + host coordinator"}
+           "path": "nadmm_workers_solve per round (scatter z, y_i / gather x_i for all local nodes) + host "
+                   "coordinator (paper_1807_07132_b200.dist.HostCoordinator, spectral penalty selection)"}
 
     # ---------------- time to target: theta = (F - F*)/F* <= 0.05 ----------------
-    ttt = {}
+    ttt, parity, cpu, fstar_info = {}, None, None, {}
     if not args.no_ttt:
-        fstar = [None]
+        fstar = [None, None]
         if rank == 0:
-            full = nadmm.Dataset.dense(Xtr, ytr, C, ctx=ctx)
-            ref = nadmm.newton_solve(nadmm.make_softmax_objective(full, LAM), np.zeros(d),
-                                     nadmm.NewtonConfig(cg_tol=1e-10, cg_max_iters=200, grad_tol=1e-10,
-                                                        newton_max_iters=60))  # compute_reference
-            fstar = [ref.trace[-1].objective if ref.trace else nadmm.loss(full, ref.x, LAM)]
-            full.close()
+            fstar = list(compute_f_star(nadmm, ctx, Xtr, ytr, d))
         if dist:
             dist.broadcast_object_list(fstar, src=0)
+        f_star, fstar_info = fstar
         tcfg = nadmm.AdmmConfig(n_workers=NODES, lam=LAM, penalty=sps, stopping=nadmm.StoppingConfig(max_outer_iters=300))
         barrier()
-        s2 = nadmm.AdmmSession(shards, tcfg, nadmm.EvalContext(True, fstar[0], THETA_TARGET), comm)
+        s2 = nadmm.AdmmSession(shards, tcfg, nadmm.EvalContext(True, f_star, THETA_TARGET), comm)
         s2.step(300)
         res = s2.result()
         rows = res.metrics
         hit = [r for r in rows if r["theta"] == r["theta"] and r["theta"] <= THETA_TARGET]
         t_hit = max_over_ranks(hit[0]["wall_seconds"] if hit else float("nan"))
         ttt = {"time_to_target_s": t_hit if hit else None, "ttt_outer_iters": hit[0]["iteration"] if hit else None,
-               "theta_target": THETA_TARGET, "f_star": fstar[0], "final_theta": rows[-1]["theta"] if rows else None,
+               "theta_target": THETA_TARGET, "f_star": f_star, "final_theta": rows[-1]["theta"] if rows else None,
                "ttt_converged_flag": res.converged}
         Xte_ds = nadmm.Dataset.dense(Xte, yte, C, ctx=ctx)
-        ttt["test_accuracy"] = nadmm.accuracy(nadmm.predict(Xte_ds, res.z), yte)
+        pred_gpu = nadmm.predict(Xte_ds, res.z)
+        ttt["test_accuracy"] = nadmm.accuracy(pred_gpu, yte)
+        Xte_ds.close()
         s2.close()
 
-    # ---------------- CPU baseline (rank 0, N = 1 only) ----------------
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        # torch and the reference share one libgomp: undo the e2e coordinator's thread cap so the
-        # reference's OpenMP regions get the `cores` this line reports
-        torch.set_num_threads(threads)
-        kind, hv, dt = reference_worker_bench(Xtr[owner == 0], ytr[owner == 0], args.cpu_steps, 1, threads)
-        cpu = {"value": hv / dt, "unit": "Hv/s", "cores": threads, "kind": kind,
-               "sample": f"{args.cpu_steps} run_worker ADMM solves of node 0 (6250x3072) after 1 warm-up"}
+        # ---- CPU reference on the same run (rank 0, N = 1): parity + cpu_baseline ----
+        if rank == 0 and world == 1 and not args.no_cpu:
+            parity, cpu = cpu_reference_leg(Xtr, ytr, Xte, yte, owner, f_star, rows, res.z, pred_gpu, args)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "Hv/s", "n_gpus": world, "steps": args.steps,
@@ -416,7 +546,7 @@ def main():
                            "admm_nodes": NODES, "nodes_per_gpu": per, "inner_iters": 1, "cg_max_iters": 10,
                            "ls_max_iters": 10, "penalty": "spectral (SPS, rho0=1, T_f=2)",
                            "l2": "no flush: per-step inputs 1.23 GB/GPU at N=1 >> 126 MB L2"},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(st["kernel_launches"]),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity, "f_star_check": fstar_info, "gpu_launches": int(st["kernel_launches"]),
                 "clocks": clk.summary(), "outer_iters_per_s": args.steps / (ms * 1e-3),
                 "hv_per_step": hv_total / args.steps}
         line.update(ttt)

@@ -215,7 +215,7 @@ nadmm_status nadmm_worker_solve(nadmm_worker w, double rho, const double* z, con
 /* One scatter -> gather round for several workers of this process (the reference's WorkerPool,
  * src/worker.cpp:222-240): worker i gets (rho[i], z, y[i]) from host memory and returns x_out[i]
  * and stats[i], exactly as n calls of nadmm_worker_solve, but the workers run concurrently on the
- * GPU (NADMM_NODE_STREAMS streams, default 2) with a single synchronisation for the round. */
+ * GPU (NADMM_NODE_STREAMS streams, default 4) with a single synchronisation for the round. */
 nadmm_status nadmm_workers_solve(const nadmm_worker* workers, int32_t n, const double* rho, const double* z,
                                  const double* const* y, const nadmm_newton_cfg* cfg, int32_t inner_iters,
                                  double* const* x_out, nadmm_inner_stats* stats);

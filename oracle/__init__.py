@@ -425,6 +425,10 @@ class Ref:
                                                      C.byref(gn)))
         return dict(x=x, trace=_trace_rows(tr, nt.value), converged=bool(conv.value), final_grad_norm=gn.value)
 
+    def set_threads(self, n: int) -> int:
+        """OpenMP threads of the calling host thread (nadmm_ref_set_threads)."""
+        return int(self.lib.nadmm_ref_set_threads(C.c_int(int(n))))
+
     def rng_stream(self, seed, kind, count, bound=0):
         out = np.zeros(count)
         self._chk(self.lib.nadmm_ref_rng_stream(C.c_uint64(seed), C.c_int(kind), C.c_uint64(bound),
@@ -597,6 +601,99 @@ class RefWorker:
         self.ds.ref._chk(self.ds.ref.lib.nadmm_ref_worker_solve(self.h, C.c_double(rho), _dp(_f64(z)), _dp(_f64(y)),
                                                                  _dp(_cfg(cfg)), C.c_int(inner_iters), _dp(x), _dp(st)))
         return x, dict(zip(("grad_norm", "inner_iters", "cg_iters", "fn_evals", "flags"), st.tolist()))
+
+
+class RefAdmm:
+    """Newton-ADMM with the REFERENCE's own worker solves (run_worker ADMM branch through
+    ``RefWorker``) and the port's coordinator (the reference declares the coordinator in
+    inc/admm.hpp:58-140 but ships no implementation, restated in
+    nor_admm_run_cb). One ``step()`` = one outer iteration in SPEC order: scatter ->
+    solves -> z-update -> y-hat / y-update -> residuals / tolerances -> spectral penalty -> metrics.
+
+    ``workers_parallel``: the workers' solves run on one host thread each, like the reference's
+    WorkerPool (src/worker.cpp:225-242); ``threads_per_worker`` OpenMP threads each (the Eigen
+    stand-in's GEMM loops). ctypes releases the GIL during the calls.
+    """
+
+    def __init__(self, ref: "Ref", shards, cfg: NorAdmmCfg, workers_parallel: bool = True,
+                 threads_per_worker: int | None = None, eval_objective: bool = False):
+        import concurrent.futures as cf
+
+        self.ref, self.cfg, self.port = ref, cfg, Port()
+        self.N = cfg.n_workers
+        assert len(shards) == self.N
+        self.shards = shards
+        self.ds = [ref.dataset(s) for s in shards]
+        self.workers = [ds.worker() for ds in self.ds]
+        self.d = shards[0].d
+        N, d = self.N, self.d
+        self.x, self.y, self.yh = np.zeros((N, d)), np.zeros((N, d)), np.zeros((N, d))
+        self.z, self.rho = np.zeros(d), np.full(N, cfg.rho0)
+        self.xs, self.ys, self.yhs, self.zs = np.zeros((N, d)), np.zeros((N, d)), np.zeros((N, d)), np.zeros(d)
+        self.k, self.snap_it, self.converged = 0, 0, False
+        self.newton = list(cfg.newton)
+        self.eval_objective = eval_objective
+        self.metrics = []
+        self.hv = 0  # Hessian-vector products applied (CG + certificate), as the GPU counts them
+        self.solve_seconds = 0.0  # wall time inside the workers' solves
+        cores = os.cpu_count() or 1
+        self.tpw = threads_per_worker or (max(1, cores // N) if workers_parallel else cores)
+        self.pool = cf.ThreadPoolExecutor(N) if workers_parallel else None
+        if not workers_parallel:
+            ref.set_threads(self.tpw)
+
+    def _solve(self, i):
+        if self.pool is not None:
+            self.ref.set_threads(self.tpw)
+        return self.workers[i].solve(self.rho[i], self.z, self.y[i], cfg=self.newton,
+                                     inner_iters=self.cfg.inner_iters)
+
+    def objective(self, z) -> float:
+        """F(z) = sum_i loss(D_i, z) + (lambda/2)|z|^2 (port_fval: global objective of Eq. (5))."""
+        return sum(ds.loss(z, 0.0) for ds in self.ds) + 0.5 * self.cfg.lam * float(np.dot(z, z))
+
+    def step(self) -> dict:
+        import time
+
+        cfg, P, N, d = self.cfg, self.port, self.N, self.d
+        t0 = time.perf_counter()
+        if self.pool is not None:
+            res = list(self.pool.map(self._solve, range(N)))
+        else:
+            res = [self._solve(i) for i in range(N)]
+        self.solve_seconds += time.perf_counter() - t0
+        inner = cg = fe = flags = 0
+        for i, (xi, st) in enumerate(res):
+            self.x[i] = xi
+            inner += int(st["inner_iters"])
+            cg += int(st["cg_iters"])
+            fe += int(st["fn_evals"])
+            flags |= int(st["flags"])
+        self.hv += cg + inner
+        pz = self.z.copy()
+        self.z = P.z_update(self.x, self.y, self.rho, cfg.lam)
+        self.yh = self.y + self.rho[:, None] * (pz[None, :] - self.x)  # SPEC.md:303
+        self.y = P.y_update(self.y, self.x, self.z, self.rho)
+        self.k += 1
+        pr, du, pt, dt = P.residuals(self.x, self.z, pz, self.rho)
+        ep, ed = P.tolerances(self.x, self.y, self.z, cfg.eps_abs, cfg.eps_rel, bool(cfg.standard_norms))
+        self.converged = bool(np.all(pr <= ep) and np.all(du <= ed))
+        if cfg.penalty_kind == 1 and self.k - self.snap_it >= cfg.update_period:
+            for i in range(N):
+                self.rho[i] = P.spectral_rho(self.x[i] - self.xs[i], self.yh[i] - self.yhs[i], self.z - self.zs,
+                                             self.y[i] - self.ys[i], self.rho[i], cfg.eps_cor, cfg.rho_min,
+                                             cfg.rho_max)[0]
+            self.xs, self.ys, self.yhs, self.zs = self.x.copy(), self.y.copy(), self.yh.copy(), self.z.copy()
+            self.snap_it = self.k
+        row = dict(iteration=self.k, train_objective=self.objective(self.z) if self.eval_objective else float("nan"),
+                   primal_norm=pt, dual_norm=dt, eps_pri=ep, eps_dual=ed, inner_iterations=inner, cg_iters=cg,
+                   fn_evals=fe, flags=flags, rho_mean=float(np.mean(self.rho)))
+        self.metrics.append(row)
+        return row
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.shutdown()
 
 
 def port() -> Port:

@@ -15,6 +15,8 @@
 #include "nadmm/objective.hpp"
 #include "nadmm/softmax.hpp"
 
+#include <omp.h>
+
 #include <atomic>
 #include <cstdint>
 #include <cstring>
@@ -99,6 +101,13 @@ void pack_trace(const NewtonResult& r, double* trace, int cap, int* ntrace) {
 extern "C" {
 
 const char* nadmm_ref_last_error(void) { return g_err.c_str(); }
+
+// OpenMP threads of the CALLING host thread's parallel regions (the Eigen stand-in's GEMM loops):
+// a WorkerPool-style run gives each worker thread its share of the cores (src/worker.cpp:225-242).
+int nadmm_ref_set_threads(int n) {
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+}
 
 int nadmm_ref_dataset_dense(const double* X, std::int64_t n, std::int64_t p, const std::int32_t* labels, int C,
                             void** out) {

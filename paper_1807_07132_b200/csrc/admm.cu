@@ -309,7 +309,7 @@ struct AdmmRun {
             NADMM_NCCL(ncclAllGather(cnt + rank, cnt, 1, ncclInt, comm->comm, st));
             std::vector<int> h(nranks);
             NADMM_CUDA(cudaMemcpyAsync(h.data(), cnt, sizeof(int) * nranks, cudaMemcpyDeviceToHost, st));
-            NADMM_CUDA(cudaStreamSynchronize(st));
+            stream_sync(st);
             n_total = 0;
             for (int v : h) n_total += v;
         }
@@ -463,7 +463,7 @@ struct AdmmRun {
         NADMM_CUDA(cudaMemcpyAsync(hred.data(), wred, sizeof(double) * hred.size(), cudaMemcpyDeviceToHost, st));
         if (cfg.eval_objective)
             NADMM_CUDA(cudaMemcpyAsync(hfz.data(), fz, sizeof(double) * n_local, cudaMemcpyDeviceToHost, st));
-        NADMM_CUDA(cudaStreamSynchronize(st));
+        stream_sync(st);
         for (int i = 0; i < n_local; ++i) {  // gather the workers' inner stats
             Shard& s = *shards[i];
             if (pending[i] == 2) continue;  // L-BFGS stats already gathered
@@ -493,7 +493,7 @@ struct AdmmRun {
             NADMM_CUDA(cudaMemcpyAsync(rstat, rs, sizeof rs, cudaMemcpyHostToDevice, st));
             NADMM_NCCL(ncclAllGather(rstat, gstat, kStats, ncclDouble, comm->comm, st));
             NADMM_CUDA(cudaMemcpyAsync(hstat.data(), gstat, sizeof(double) * hstat.size(), cudaMemcpyDeviceToHost, st));
-            NADMM_CUDA(cudaStreamSynchronize(st));
+            stream_sync(st);
         } else {
             std::memcpy(hstat.data(), rs, sizeof rs);
         }
@@ -560,7 +560,7 @@ struct AdmmRun {
         }
         NADMM_LAUNCH_CHECK();
         NADMM_CUDA(cudaMemcpyAsync(hred.data(), wred, sizeof(double) * n_local * 6, cudaMemcpyDeviceToHost, st));
-        NADMM_CUDA(cudaStreamSynchronize(st));
+        stream_sync(st);
         for (int i = 0; i < n_local; ++i) {
             const double* w = hred.data() + (int64_t)i * 6;
             double ah = 0.0, bh = 0.0;
@@ -594,7 +594,7 @@ struct AdmmRun {
 
     void result(double* z_out, double* rho_out) {
         if (z_out) NADMM_CUDA(cudaMemcpyAsync(z_out, z, sizeof(double) * d, cudaMemcpyDeviceToHost, st));
-        NADMM_CUDA(cudaStreamSynchronize(st));
+        stream_sync(st);
         if (rho_out)
             for (int i = 0; i < n_local; ++i) rho_out[i] = rho[i];
     }
@@ -700,12 +700,12 @@ nadmm_status nadmm_sgd_run(const nadmm_shard* shards, int32_t n_local, nadmm_com
                 NADMM_CUDA(cudaMemcpyAsync(hb, v, sizeof(double) * n, cudaMemcpyHostToDevice, st));
                 NADMM_NCCL(ncclAllReduce(hb, hb, (size_t)n, ncclDouble, ncclSum, comm->comm, st));
                 NADMM_CUDA(cudaMemcpyAsync(v, hb, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-                NADMM_CUDA(cudaStreamSynchronize(st));
+                stream_sync(st);
             };
         }
         const SgdOutcome o = sgd_run(sh, comm ? &red : nullptr, *cfg, lambda, x, rows, row_cap);
         NADMM_CUDA(cudaMemcpyAsync(x_inout, x, sizeof(double) * (size_t)d, cudaMemcpyDeviceToHost, st));
-        NADMM_CUDA(cudaStreamSynchronize(st));
+        stream_sync(st);
         if (epochs_done) *epochs_done = o.epochs;
         return NADMM_OK;
     } catch (const Error& e) {

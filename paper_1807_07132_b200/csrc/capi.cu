@@ -122,7 +122,7 @@ void upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
 
 void download(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     NADMM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
-    NADMM_CUDA(cudaStreamSynchronize(st));
+    stream_sync(st);
 }
 
 bool same_point(const std::vector<double>& memo, const double* w, int64_t d) {
@@ -222,6 +222,7 @@ nadmm_status nadmm_ctx_create(int32_t device, nadmm_ctx* out) {
             raise(NADMM_ECUDA, std::string("built for sm_100a (B200); device is ") + prop.name + " sm_" +
                                    std::to_string(prop.major * 10 + prop.minor));
         NADMM_CUDA(cudaSetDevice(device));
+        barrier_configure();
         auto* c = new nadmm_ctx_s();
         c->device = device;
         c->num_sms = prop.multiProcessorCount;
@@ -263,7 +264,7 @@ int32_t nadmm_ctx_node_streams(nadmm_ctx ctx) { return ctx ? ctx->node_streams :
 nadmm_status nadmm_ctx_synchronize(nadmm_ctx ctx) {
     return guard([&] {
         check_ctx(ctx);
-        NADMM_CUDA(cudaStreamSynchronize(ctx->stream));
+        stream_sync(ctx->stream);
     });
 }
 
@@ -274,7 +275,7 @@ nadmm_status nadmm_ctx_stats(nadmm_ctx ctx, nadmm_stats* out) {
         check_ctx(ctx);
         unsigned long long h[4];
         NADMM_CUDA(cudaMemcpyAsync(h, ctx->dctr, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
-        NADMM_CUDA(cudaStreamSynchronize(ctx->stream));
+        stream_sync(ctx->stream);
         *out = ctx->stats;
         out->hv_products = (int64_t)h[0];
     });
@@ -320,7 +321,7 @@ nadmm_status nadmm_shard_dense(nadmm_ctx ctx, const double* X, int64_t n, int64_
         NADMM_CUDA(cudaMemsetAsync(s->labels, 0, sizeof(int32_t) * (n + kRowPad), ctx->stream));
         upload(s->labels, labels, sizeof(int32_t) * n, ctx->stream);
         alloc_work(*s);
-        NADMM_CUDA(cudaStreamSynchronize(ctx->stream));
+        stream_sync(ctx->stream);
         *out = s.release();
     });
 }
@@ -440,7 +441,7 @@ nadmm_status nadmm_shard_csr(nadmm_ctx ctx, const int64_t* indptr, const int32_t
             s->lsum = dev_alloc<double>(*s, n * (C - 1));
         }
         alloc_work(*s);
-        NADMM_CUDA(cudaStreamSynchronize(ctx->stream));
+        stream_sync(ctx->stream);
         *out = s.release();
     });
 }
@@ -659,7 +660,7 @@ nadmm_status nadmm_worker_solve(nadmm_worker w, double rho, const double* z, con
         const bool done = solve_launch(s, c, 0.0, true, rho, inner_iters);
         if (x_out) NADMM_CUDA(cudaMemcpyAsync(x_out, s.x, sizeof(double) * s.d, cudaMemcpyDeviceToHost, s.ctx->stream));
         if (!done) solve_readback_async(s);
-        NADMM_CUDA(cudaStreamSynchronize(s.ctx->stream));
+        stream_sync(s.ctx->stream);
         SolveResult r = done ? solve_collect(s, c, false) : solve_result(s, c);
         if (r.error == NADMM_ESOLVER) raise(NADMM_ESOLVER, "newton_solve: non-finite objective");
         if (r.error == NADMM_ECONFIG) raise(NADMM_ECONFIG, "cg_solve requires ||g|| > 0");
@@ -721,7 +722,7 @@ nadmm_status nadmm_workers_solve(const nadmm_worker* ws, int32_t n, const double
                 NADMM_CUDA(cudaEventRecord(ctx.node_join[k], ctx.node_stream[k]));
                 NADMM_CUDA(cudaStreamWaitEvent(st, ctx.node_join[k], 0));
             }
-        NADMM_CUDA(cudaStreamSynchronize(st));  // one synchronisation for the whole round
+        stream_sync(st);  // one synchronisation for the whole round
         for (int i = 0; i < n; ++i) {
             Shard& s = *sh[(size_t)i];
             SolveResult r = done[(size_t)i] ? solve_collect(s, c, false) : solve_result(s, c);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -82,10 +83,57 @@ __device__ __forceinline__ double reduce_partials(const double* parts, int n) {
     return warp_sum(s);
 }
 
-// Software grid barrier for kernels whose whole grid is co-resident (small persistent grids on the
-// context's stream). `ctr` is a monotonically increasing per-kernel counter that only launches of
-// the same grid size touch, so it is a multiple of gridDim.x whenever such a launch starts; every
-// block must reach every barrier (callers branch only on grid-uniform values).
+// Software grid barrier for kernels whose whole grid is co-resident (persistent grids launched
+// cooperatively where the runtime allows it, else sized from occupancy). `ctr` is a monotonically
+// increasing per-kernel counter that only launches of the same grid size touch, so it is a multiple
+// of gridDim.x whenever such a launch starts; every block must reach every barrier (callers branch
+// only on grid-uniform values).
+//
+// Watchdog (opt-out): a grid that is not fully co-resident would spin forever. After
+// NADMM_BARRIER_TIMEOUT_MS of wall time (%globaltimer; default 60 s, 0 = off) the waiting block sets
+// the translation unit's fault flag and every barrier of the launch falls through; the host raises
+// NADMM_ECUDA at its next synchronisation (stream_sync) instead of the context dying on a trap.
+struct BarrierCtl {
+    unsigned long long timeout_ns;
+    unsigned long long fault;
+};
+struct BarrierTU {
+    void (*set_timeout)(unsigned long long ns);
+    unsigned long long (*take_fault)();
+};
+void barrier_register(BarrierTU tu);  // host registry (newton.cu): one entry per translation unit
+
+namespace {
+// Without relocatable device code every translation unit owns its copy of the control block; each
+// registers its accessors at static-initialisation time.
+__device__ BarrierCtl g_barrier_ctl = {0ull, 0ull};
+
+void barrier_set_timeout_tu(unsigned long long ns) {
+    const BarrierCtl c{ns, 0ull};
+    cudaMemcpyToSymbol(g_barrier_ctl, &c, sizeof c);
+}
+
+unsigned long long barrier_take_fault_tu() {
+    BarrierCtl c{};
+    if (cudaMemcpyFromSymbol(&c, g_barrier_ctl, sizeof c) != cudaSuccess) return 0;
+    if (c.fault) {
+        c.fault = 0;
+        cudaMemcpyToSymbol(g_barrier_ctl, &c, sizeof c);
+    }
+    return c.fault ? 1ull : 0ull;
+}
+
+struct BarrierReg {
+    BarrierReg() { barrier_register(BarrierTU{barrier_set_timeout_tu, barrier_take_fault_tu}); }
+} g_barrier_reg;
+}  // namespace
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -93,14 +141,20 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
         __threadfence();
         const unsigned long long old = atomicAdd(ctr, 1ULL);
         const unsigned long long target = (old / nb + 1) * nb;
+        const unsigned long long limit = g_barrier_ctl.timeout_ns;
+        const unsigned long long t0 = limit ? global_ns() : 0ull;
         unsigned long long cur;
-        const long long t0 = clock64();
-        do {
+        for (;;) {
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(cur) : "l"(ctr) : "memory");
-            // watchdog: a grid that is not fully co-resident would spin forever; fail the launch
-            // (an error the host reports) instead of hanging the device (~4 s at 2 GHz)
-            if (cur < target && clock64() - t0 > (8LL << 30)) __trap();
-        } while (cur < target);
+            if (cur >= target) break;
+            if (limit) {
+                if (*(volatile unsigned long long*)&g_barrier_ctl.fault) break;  // an earlier barrier timed out
+                if (global_ns() - t0 > limit) {
+                    atomicExch(&g_barrier_ctl.fault, 1ull);
+                    break;
+                }
+            }
+        }
     }
     __syncthreads();
 }
@@ -115,19 +169,44 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\
 #define NADMM_PDL 0  // measured: no gain on the Newton graph (kept switchable)
 #endif
 
+// Persistent grids that synchronise through grid_barrier are launched cooperatively (the runtime
+// then guarantees co-residency, or fails the launch); NADMM_COOP=0 falls back to plain launches
+// (co-residency from the occupancy-sized grid, guarded by the barrier watchdog).
+inline bool coop_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("NADMM_COOP");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <typename... KArgs, typename... Args>
-void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+void launch_ex(bool coop, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+               Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = NADMM_PDL;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = (coop && coop_enabled()) ? 2 : 1;
     NADMM_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    launch_ex(false, kernel, grid, block, smem, st, args...);
+}
+
+// Grid-barrier kernels (grid_barrier inside): cooperative launch.
+template <typename... KArgs, typename... Args>
+void launch_coop(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    launch_ex(true, kernel, grid, block, smem, st, args...);
 }
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }

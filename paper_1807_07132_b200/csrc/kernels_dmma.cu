@@ -96,7 +96,8 @@ std::vector<Layout> candidate_layouts(int64_t p, int K) {
     return out;
 }
 
-cudaLaunchConfig_t make_cfg(Shard& s, const Layout& L, int clusters, cudaLaunchAttribute* attr) {  // attr[2]
+cudaLaunchConfig_t make_cfg(Shard& s, const Layout& L, int clusters, cudaLaunchAttribute* attr,
+                            bool coop = false) {  // attr[3]
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(clusters * L.cs, 1, 1);
     cfg.blockDim = dim3(32 * (L.nw + kDmmaAux), 1, 1);
@@ -108,8 +109,10 @@ cudaLaunchConfig_t make_cfg(Shard& s, const Layout& L, int clusters, cudaLaunchA
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = NADMM_PDL;
+    attr[2].id = cudaLaunchAttributeCooperative;  // the solver tails synchronise the grid (grid_barrier)
+    attr[2].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = (coop && coop_enabled()) ? 3 : 2;
     return cfg;
 }
 
@@ -120,7 +123,7 @@ int setup_one(Shard& s, const Layout& L) {
     auto kern = dmma_pass_kernel<MT, 1, 1, kBM, kPipes[PIPE].lag, kPipes[PIPE].stages, MODE>;
     NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit));
     NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     cudaLaunchConfig_t cfg = make_cfg(s, L, 1, attr);
     int nc = 0;
     if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess) {
@@ -167,8 +170,8 @@ int setup_layout(Shard& s, const Layout& L) {
 template <int MT, int PIPE, int MODE>
 void launch_one(Shard& s, const Layout& L, const DmmaArgs& a, int clusters) {
     auto kern = dmma_pass_kernel<MT, 1, 1, kBM, kPipes[PIPE].lag, kPipes[PIPE].stages, MODE>;
-    cudaLaunchAttribute attr[2];
-    cudaLaunchConfig_t cfg = make_cfg(s, L, clusters, attr);
+    cudaLaunchAttribute attr[3];
+    cudaLaunchConfig_t cfg = make_cfg(s, L, clusters, attr, a.tail != kTailNone);
     NADMM_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
 }
 

@@ -671,7 +671,7 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
                                           (const double*)s.part, chunks, (const double*)s.g, s.pd, s.r, s.dv, s.hd,
                                           (const double*)s.blk, ncurv, chunks > 0 ? s.ctx->dctr : nullptr));
         } else {
-            launch_pdl(k_cg_tail, grid, 256, 0, st, it, s.d, s.st, s.prm, s.part, chunks, s.g, s.pd, s.r, s.dv, s.hd,
+            launch_coop(k_cg_tail, grid, 256, 0, st, it, s.d, s.st, s.prm, s.part, chunks, s.g, s.pd, s.r, s.dv, s.hd,
                        s.blk, ncurv, chunks > 0 ? s.ctx->dctr : nullptr, s.gbar + 0);
         }
         tl_mark(s, "cg_tail");
@@ -692,7 +692,7 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
         op_hv_split(s, s.pd, s.hd, nullptr, 0, &s.st->cert_act, &chunks);
         s.hv_write_lp = false;
         s.hv_timer_site = -1;
-        launch_pdl(k_cert_tail, grid, 256, 0, st, s.d, s.st, s.prm, s.part, chunks, lp_from_cert ? 1 : 0, s.g, s.pd,
+        launch_coop(k_cert_tail, grid, 256, 0, st, s.d, s.st, s.prm, s.part, chunks, lp_from_cert ? 1 : 0, s.g, s.pd,
                    s.hd, s.blk, grid, chunks > 0 ? s.ctx->dctr : nullptr, s.gbar + 1);
         LAUNCH_COUNT(s);
     }
@@ -717,7 +717,7 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
     } else {
         chunks = op_cache_split(s, s.x, it_act);
         tl_mark(s, "cache_pass");
-        launch_pdl(k_newton_tail, grid, 256, 0, st, s.d, s.st, s.prm, s.part, chunks, s.x, s.z, s.y, s.gbase, s.g,
+        launch_coop(k_newton_tail, grid, 256, 0, st, s.d, s.st, s.prm, s.part, chunks, s.x, s.z, s.y, s.gbase, s.g,
                    s.t, s.blk, s.rows_grid, s.scal, s.trace, kTraceCap, s.gbar + 2, it_act);
         tl_mark(s, "newton_tail");
         LAUNCH_COUNT(s);

@@ -231,7 +231,7 @@ struct Lbfgs {
         const int64_t need = 2 * hist + 6 * d + 3 * (int64_t)kLbMaxBlocks + 4;
         if (sh.lb_ws_len < need) {
             if (sh.lb_ws) {
-                NADMM_CUDA(cudaStreamSynchronize(st));
+                stream_sync(st);
                 cudaFree(sh.lb_ws);
                 sh.bytes -= 8 * sh.lb_ws_len;
                 sh.lb_ws = nullptr;
@@ -256,7 +256,7 @@ struct Lbfgs {
 
     void fetch(int n) {
         NADMM_CUDA(cudaMemcpyAsync(host, out, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-        NADMM_CUDA(cudaStreamSynchronize(st));
+        stream_sync(st);
     }
 
     // f(w), |g(w)|^2 and g(w)'p (p may be null); the gradient lands in gout.
@@ -468,7 +468,7 @@ LbfgsResult device_lbfgs_solve(Shard& s, const LbfgsCfg& cfg, double lambda, boo
         throw;
     }
     NADMM_CUDA(cudaMemcpyAsync(s.x, run.x, sizeof(double) * s.d, cudaMemcpyDeviceToDevice, run.st));
-    NADMM_CUDA(cudaStreamSynchronize(run.st));
+    stream_sync(run.st);
     s.cache_at = Shard::kNone;  // the cache holds the last trial point, not s.x
     return res;
 }

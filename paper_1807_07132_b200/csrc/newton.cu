@@ -6,11 +6,42 @@
 // once per Newton iteration (once per outer ADMM iteration with inner_iters = 1).
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "solver.h"
 #include "solver_kernels.h"
 
 namespace nadmm {
+
+// ---- grid-barrier watchdog registry (common.cuh) ----
+namespace {
+std::vector<BarrierTU>& barrier_tus() {
+    static std::vector<BarrierTU> v;
+    return v;
+}
+}  // namespace
+
+void barrier_register(BarrierTU tu) { barrier_tus().push_back(tu); }
+
+void barrier_configure() {
+    unsigned long long ms = 60000;  // watchdog bound; 0 disables it
+    if (const char* e = getenv("NADMM_BARRIER_TIMEOUT_MS")) ms = strtoull(e, nullptr, 10);
+    for (const BarrierTU& tu : barrier_tus()) tu.set_timeout(ms * 1000000ull);
+}
+
+void barrier_check() {
+    bool fault = false;
+    for (const BarrierTU& tu : barrier_tus()) fault = tu.take_fault() != 0 || fault;
+    if (fault)
+        raise(NADMM_ECUDA, "grid barrier timed out (persistent grid not co-resident, or a hung peer); results of "
+                           "the last launch are invalid");
+}
+
+void stream_sync(cudaStream_t st) {
+    NADMM_CUDA(cudaStreamSynchronize(st));
+    barrier_check();
+}
+
 
 // ---------------------------------------------------------------------------------------------
 // Composite ops (one or two data passes each)
@@ -237,7 +268,7 @@ static void readback_finish(Shard& s, int cg_max) {
 // Reads back the solver state and trace (one async copy each, one sync).
 static void readback(Shard& s, int cg_max) {
     solve_readback_async(s);
-    NADMM_CUDA(cudaStreamSynchronize(s.ctx->stream));
+    stream_sync(s.ctx->stream);
     readback_finish(s, cg_max);
 }
 

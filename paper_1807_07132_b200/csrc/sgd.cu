@@ -205,14 +205,14 @@ void sgd_worker_grad(Shard& s, const nadmm_sgd_cfg& c, uint32_t iteration, const
         std::vector<int32_t> perm((size_t)s.n);
         epoch_permutation(nadmm_mix_seed(c.seed, (uint64_t)epoch), s.n, perm.data());
         NADMM_CUDA(cudaMemcpyAsync(s.sgd_perm, perm.data(), sizeof(int32_t) * (size_t)s.n, cudaMemcpyHostToDevice, st));
-        NADMM_CUDA(cudaStreamSynchronize(st));  // the host vector goes out of scope
+        stream_sync(st);  // the host vector goes out of scope
         s.sgd_epoch = epoch;
         s.sgd_seed = c.seed;
     }
     const int64_t m = c.batch, step = (int64_t)iteration % c.steps_per_epoch;
     if (s.sgd_u_len < m * s.K) {
         if (s.sgd_u) {
-            NADMM_CUDA(cudaStreamSynchronize(st));
+            stream_sync(st);
             cudaFree(s.sgd_u);
             s.bytes -= 8 * s.sgd_u_len;
         }
@@ -286,7 +286,7 @@ SgdOutcome sgd_run(std::vector<Shard*>& shards, const SgdReduce* red, const nadm
         for (Shard* s : shards) {
             op_value(*s, x_dev, scratch + vg, 0, nullptr);
             NADMM_CUDA(cudaMemcpyAsync(&h, scratch + vg, sizeof(double), cudaMemcpyDeviceToHost, st));
-            NADMM_CUDA(cudaStreamSynchronize(st));
+            stream_sync(st);
             f += h;
         }
         double buf[1] = {f};
@@ -297,7 +297,7 @@ SgdOutcome sgd_run(std::vector<Shard*>& shards, const SgdReduce* red, const nadm
         NADMM_LAUNCH_CHECK();
         double xx = 0.0;
         NADMM_CUDA(cudaMemcpyAsync(&xx, scratch + vg + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
-        NADMM_CUDA(cudaStreamSynchronize(st));
+        stream_sync(st);
         return buf[0] + 0.5 * lambda * xx;
     };
     SgdOutcome out;
@@ -329,14 +329,15 @@ SgdOutcome sgd_run(std::vector<Shard*>& shards, const SgdReduce* red, const nadm
             r.inner_iterations = cfg.steps_per_epoch;
             r.fn_evals = cfg.steps_per_epoch * (int)shards.size();
             r.rho_mean = NAN;
-            r.messages = (int64_t)(2.0 * n_workers) * cfg.steps_per_epoch;  // 2N per mini-batch step
+            // cumulative like the ADMM rows (MetricsRow.messages, inc/metrics.hpp:23): 2N per mini-batch step
+            r.messages = (int64_t)(2.0 * n_workers) * cfg.steps_per_epoch * (int64_t)(e + 1);
         }
         out.epochs = e + 1;
         out.final_objective = F;
         if (!(F <= 1e3 * f0))  // unstable step sizes abort the run
             raise(NADMM_ESOLVER, "sync_sgd: objective diverged at epoch " + std::to_string(e));
     }
-    NADMM_CUDA(cudaStreamSynchronize(st));
+    stream_sync(st);
     return out;
 }
 

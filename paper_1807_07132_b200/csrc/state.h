@@ -268,5 +268,14 @@ void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
 
 }  // namespace nadmm
 
+namespace nadmm {
+// Grid-barrier watchdog control (common.cuh): push NADMM_BARRIER_TIMEOUT_MS to every translation
+// unit's control block on the current device; raise NADMM_ECUDA if any barrier timed out.
+void barrier_configure();
+void barrier_check();
+// cudaStreamSynchronize + the barrier fault check: every host synchronisation of the library.
+void stream_sync(cudaStream_t st);
+}  // namespace nadmm
+
 struct nadmm_ctx_s : nadmm::Ctx {};
 struct nadmm_shard_s : nadmm::Shard {};

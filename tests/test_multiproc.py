@@ -11,7 +11,11 @@ import torch.multiprocessing as mp
 
 from paper_1807_07132_b200 import dist as nd
 
-NODES, D, LAM = 4, 37, 1e-3
+NODES, D, LAM, STEPS = 4, 37, 1e-3, 5
+
+
+def _x(i, step):
+    return np.random.default_rng(100 * i + step).normal(size=D) * (1.0 + 0.1 * step)
 
 
 def _free_port() -> int:
@@ -35,12 +39,13 @@ def _worker(rank, world, port, out):
         mine = nd.node_range(NODES, world, rank)
         uid = nd.share_unique_id(dist, rank, lambda: bytes(range(128)))
         xs, ys, rhos = _fixture()
-        co = nd.HostCoordinator(D, LAM, nd.torch_allreduce(dist))
-        my_y = [ys[i].copy() for i in mine]
+        co = nd.HostCoordinator(D, LAM, len(mine), penalty="spectral", allreduce=nd.torch_allreduce(dist))
+        co.y[:] = [ys[i] for i in mine]
+        co.rho[:] = [rhos[i] for i in mine]
         zs = []
-        for step in range(3):  # three consensus rounds with fixed x (only z/y evolve)
-            zs.append(co.step([xs[i] for i in mine], my_y, [rhos[i] for i in mine]).copy())
-        out[rank] = {"nodes": list(mine), "uid": uid, "z": zs, "y": my_y}
+        for step in range(STEPS):  # consensus rounds on a fixed x trajectory (z / y / rho evolve)
+            zs.append(co.step(np.stack([_x(i, step) for i in mine])).copy())
+        out[rank] = {"nodes": list(mine), "uid": uid, "z": zs, "y": co.y.copy(), "rho": co.rho.copy()}
     finally:
         dist.destroy_process_group()
 
@@ -52,24 +57,65 @@ def test_node_range():
         nd.node_range(8, 3, 0)
 
 
+def _single(xs_rows, ys, rhos):
+    co = nd.HostCoordinator(D, LAM, NODES, penalty="spectral")
+    co.y[:] = ys
+    co.rho[:] = rhos
+    zs = [co.step(np.stack([_x(i, s) for i in range(NODES)])).copy() for s in range(STEPS)]
+    return co, zs
+
+
 def test_world2_coordinator_matches_single_process(port):
     world = 2
     out = mp.Manager().dict()
     p = _free_port()
     mp.start_processes(_worker, args=(world, p, out), nprocs=world, join=True, start_method="spawn")
     xs, ys, rhos = _fixture()
-    co = nd.HostCoordinator(D, LAM)
-    y1 = [y.copy() for y in ys]
-    zs1 = [co.step(xs, y1, rhos).copy() for _ in range(3)]
+    co, zs1 = _single(xs, ys, rhos)
     assert out[0]["uid"] == out[1]["uid"] == bytes(range(128))
     assert out[0]["nodes"] + out[1]["nodes"] == list(range(NODES))
     for r in range(world):
         for za, zb in zip(out[r]["z"], zs1):
             np.testing.assert_allclose(za, zb, rtol=1e-14, atol=1e-15)
-    y2 = list(out[0]["y"]) + list(out[1]["y"])
-    for a, b in zip(y2, y1):
-        np.testing.assert_allclose(a, b, rtol=1e-14, atol=1e-15)
-    # the oracle's z_update / y_update (ascending-id pairwise tree) on the first round
-    y0 = [y.copy() for y in ys]
-    z_or = port.z_update(xs, y0, rhos, LAM)
-    np.testing.assert_allclose(zs1[0], z_or, rtol=1e-13, atol=1e-15)
+    y2 = np.concatenate([out[0]["y"], out[1]["y"]])
+    np.testing.assert_allclose(y2, co.y, rtol=1e-14, atol=1e-15)
+    np.testing.assert_allclose(np.concatenate([out[0]["rho"], out[1]["rho"]]), co.rho, rtol=1e-14)
+
+
+def test_host_coordinator_matches_oracle_coordinator(port):
+    """The host coordinator's z / y-hat / y / spectral-penalty sequence against the oracle's
+    coordinator pieces (nor_z_update pairwise tree, nor_y_update, nor_spectral_rho)."""
+    xs, ys, rhos = _fixture()
+    co, zs1 = _single(xs, ys, rhos)
+    z, y, rho = np.zeros(D), np.array(ys), np.array(rhos)
+    snap = None
+    for s in range(STEPS):
+        X = np.stack([_x(i, s) for i in range(NODES)])
+        pz = z
+        z = port.z_update(X, y, rho, LAM)
+        yh = y + rho[:, None] * (pz[None, :] - X)
+        y = port.y_update(y, X, z, rho)
+        k = s + 1
+        if snap is None:
+            snap = (np.zeros((NODES, D)), np.zeros((NODES, D)), np.zeros((NODES, D)), np.zeros(D), 0)
+        xs_, ys_, yhs_, zs_, it = snap
+        if k - it >= 2:
+            rho = np.array([port.spectral_rho(X[i] - xs_[i], yh[i] - yhs_[i], z - zs_, y[i] - ys_[i], rho[i])[0]
+                            for i in range(NODES)])
+            snap = (X.copy(), y.copy(), yh.copy(), z.copy(), k)
+        np.testing.assert_allclose(zs1[s], z, rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(co.y, y, rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(co.rho, rho, rtol=1e-12)
+    assert not np.allclose(rho, rhos)  # the spectral update actually fired
+
+
+def test_spectral_rho_matches_oracle(port):
+    rng = np.random.default_rng(5)
+    for trial in range(40):
+        a, b, c, d = (rng.normal(size=D) for _ in range(4))
+        if trial % 3 == 0:
+            b = a * 2.0 + 0.1 * b  # correlated x-side
+        if trial % 4 == 0:
+            d = -c * 0.5 + 0.05 * d  # correlated z-side
+        want = port.spectral_rho(a, b, c, d, 1.3)[0]
+        assert abs(nd.spectral_rho(a, b, c, d, 1.3) - want) <= 1e-12 * abs(want)

@@ -252,6 +252,32 @@ def test_admm_port_converges(port):
     assert min(theta) <= 0.05
 
 
+@pytest.mark.parametrize("penalty,parallel", [("spectral", True), ("fixed", False)])
+def test_ref_admm_matches_port_coordinator(port, ref, penalty, parallel):
+    """The reference arm's consensus loop (reference worker solves + the port coordinator, stepped
+    from Python, workers on a thread pool) reproduces the port's nor_admm_run: identical iteration
+    trace (cg_iters / fn_evals / flags per outer iteration), z and F(z^k) to 1e-12."""
+    Xtr, ytr, _, _ = port.generate_synthetic(1200, 12, 4, separation=3.0, noise=1.0, seed=0)
+    owner = port.partition_owner(len(ytr), 4)
+    parts = [oracle.Shard(Xtr[owner == i], ytr[owner == i], 4) for i in range(4)]
+    cfg = oracle.admm_cfg(n_workers=4, lam=1e-3, penalty=penalty, max_outer_iters=25)
+    want = port.admm_run(parts, cfg)
+    run = oracle.RefAdmm(ref, parts, cfg, workers_parallel=parallel, threads_per_worker=1, eval_objective=True)
+    try:
+        for _ in range(want["iterations"]):
+            run.step()
+            if run.converged:
+                break
+    finally:
+        run.close()
+    assert run.k == want["iterations"] and run.converged == want["converged"]
+    for a, b in zip(run.metrics, want["metrics"]):
+        assert (a["cg_iters"], a["fn_evals"], a["flags"]) == (b["cg_iters"], b["fn_evals"], b["flags"])
+        assert abs(a["train_objective"] - b["train_objective"]) <= 1e-12 * abs(b["train_objective"])
+        assert abs(a["rho_mean"] - b["rho_mean"]) <= 1e-12 * abs(b["rho_mean"])
+    assert rel(run.z, want["z"]) <= 1e-12
+
+
 # ---- golden fixtures ------------------------------------------------------------------------------
 def test_golden_fixtures(port):
     files = sorted(GOLDEN.glob("*.npz"))
