@@ -17,5 +17,5 @@ for i in "${!pids[@]}"; do
   if ! wait "${pids[$i]}"; then echo "compile failed: ${SRCS[$i]}"; cat "build/${SRCS[$i]}.ptxas.log"; rc=1; fi
 done
 [ $rc -eq 0 ] || exit 1
-"$NVCC" -shared -gencode arch=compute_100a,code=sm_100a -o lib/libnadmm_cuda.so build/*.o -lnccl -lcublas
+"$NVCC" -shared -gencode arch=compute_100a,code=sm_100a -o lib/libnadmm_cuda.so build/*.o -lnccl
 echo "built $(pwd)/lib/libnadmm_cuda.so"

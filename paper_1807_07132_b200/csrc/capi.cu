@@ -156,6 +156,7 @@ namespace nadmm {
 
 Shard::~Shard() {
     if (g_iter) cudaGraphExecDestroy(g_iter);
+    gemm_free(*this);
     for (auto& t : hv_timers) {
         if (t.start) cudaEventDestroy(t.start);
         if (t.stop) cudaEventDestroy(t.stop);
@@ -248,7 +249,6 @@ nadmm_status nadmm_ctx_destroy(nadmm_ctx ctx) {
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
         if (ctx->dctr) cudaFree(ctx->dctr);
-        gemm_teardown(*ctx);
         for (int i = 0; i < Ctx::kMaxNodeStreams; ++i) {
             if (ctx->node_stream[i]) cudaStreamDestroy(ctx->node_stream[i]);
             if (ctx->node_join[i]) cudaEventDestroy(ctx->node_join[i]);

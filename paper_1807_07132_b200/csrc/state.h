@@ -78,8 +78,6 @@ struct Ctx {
     static constexpr int kMaxNodeStreams = 8;
     cudaStream_t node_stream[kMaxNodeStreams] = {};
     cudaEvent_t node_fork = nullptr, node_join[kMaxNodeStreams] = {};
-    void* blas = nullptr;     // cublasHandle_t of the GEMM path (created with the first dense shard)
-    void* blas_ws = nullptr;  // its fixed workspace
 };
 
 struct HvTimer {
@@ -144,6 +142,7 @@ struct Shard {
     unsigned long long* gbar = nullptr;  // grid-barrier counters of the persistent vector kernels
     int rows_grid = 0;  // blocks of the last rows pass (partials count)
     int last_chunks = 0;    // split-K partial chunks written by the last fused DMMA pass
+    void* gemm = nullptr;   // GemmState of the two-GEMM DMMA path (kernels_gemm.cu), null when unused
     int dmma_clusters = 0;  // co-resident clusters of the fused DMMA pass (0: path unavailable)
     int dmma_mt = 0, dmma_nw = 0, dmma_cs = 0, dmma_fs = 0, dmma_S = 0, dmma_pipe = 0;  // chosen layout
     size_t dmma_smem = 0;
@@ -250,7 +249,7 @@ void smallp_setup(Shard& s);
 void smallp_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
 // ---- GEMM path (kernels_gemm.cu): dense shards outside the fused passes' shapes ----
 void gemm_setup(Shard& s);
-void gemm_teardown(Ctx& c);
+void gemm_free(Shard& s);
 bool gemm_supported(const Shard& s);
 void gemm_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
 bool fused_supported(const Shard& s);

@@ -37,10 +37,10 @@ def share_unique_id(dist, rank: int, make_id: Callable[[], bytes]) -> bytes:
     return box[0]
 
 
-def _spectral_side(a: np.ndarray, b: np.ndarray, eps_cor: float):
-    """Hybrid spectral estimate of one side with the correlation safeguard:
-    alpha_SD = |b|^2/<a,b>, alpha_MG = <a,b>/|a|^2; None when the safeguard fails (or a zero secant)."""
-    ab, aa, bb = float(np.dot(a, b)), float(np.dot(a, a)), float(np.dot(b, b))
+def _spectral_est(ab: float, aa: float, bb: float, eps_cor: float):
+    """Hybrid spectral estimate of one side from its secant inner products <a,b>, |a|^2, |b|^2, with
+    the correlation safeguard (SPEC.md:262-270): alpha_SD = |b|^2/<a,b>, alpha_MG = <a,b>/|a|^2;
+    None when the safeguard fails (or a zero-norm secant)."""
     if not (aa > 0.0 and bb > 0.0 and ab > 0.0):
         return None
     if not ab / (np.sqrt(aa) * np.sqrt(bb)) > eps_cor:
@@ -49,11 +49,8 @@ def _spectral_side(a: np.ndarray, b: np.ndarray, eps_cor: float):
     return mg if 2.0 * mg > sd else sd - mg / 2.0
 
 
-def spectral_rho(dx, dyhat, dz, dy, rho, eps_cor=0.2, rho_min=1e-6, rho_max=1e6) -> float:
-    """Spectral penalty of one worker (inc/admm.hpp:26-47): x-side pairs (Δx, Δŷ), z-side pairs
-    (Δz, −Δy); sqrt(a b) if both pass, sqrt of the passing one otherwise, clamped."""
-    a = _spectral_side(dx, dyhat, eps_cor)
-    b = _spectral_side(dz, -dy, eps_cor)
+def _spectral_combine(a, b, rho, rho_min, rho_max) -> float:
+    """sqrt(a b) if both sides pass, sqrt of the passing one otherwise, clamped."""
     r = rho
     if a is not None and b is not None:
         r = np.sqrt(a * b)
@@ -62,6 +59,14 @@ def spectral_rho(dx, dyhat, dz, dy, rho, eps_cor=0.2, rho_min=1e-6, rho_max=1e6)
     elif b is not None:
         r = np.sqrt(b)
     return float(min(max(r, rho_min), rho_max))
+
+
+def spectral_rho(dx, dyhat, dz, dy, rho, eps_cor=0.2, rho_min=1e-6, rho_max=1e6) -> float:
+    """Spectral penalty of one worker (inc/admm.hpp:26-47): x-side pairs (Δx, Δŷ), z-side pairs
+    (Δz, −Δy)."""
+    a = _spectral_est(float(np.dot(dx, dyhat)), float(np.dot(dx, dx)), float(np.dot(dyhat, dyhat)), eps_cor)
+    b = _spectral_est(-float(np.dot(dz, dy)), float(np.dot(dz, dz)), float(np.dot(dy, dy)), eps_cor)
+    return _spectral_combine(a, b, rho, rho_min, rho_max)
 
 
 class HostCoordinator:
@@ -116,10 +121,18 @@ class HostCoordinator:
         self.y += T
         self.k += 1
         if self.penalty == "spectral" and self.k - self.snap_it >= self.T:
+            # the secant pairs of every local worker at once: x-side (Δx, Δŷ), z-side (Δz, −Δy)
+            DX = X - self.xs
+            DH = self.yh - self.yhs
+            DY = self.y - self.ys
             dz = self.z - self.zs
+            ab_x, aa_x, bb_x = (np.einsum("ij,ij->i", DX, DH), np.einsum("ij,ij->i", DX, DX),
+                                np.einsum("ij,ij->i", DH, DH))
+            ab_z, aa_z, bb_z = -(DY @ dz), float(np.dot(dz, dz)), np.einsum("ij,ij->i", DY, DY)
             for i in range(len(rho)):
-                rho[i] = spectral_rho(X[i] - self.xs[i], self.yh[i] - self.yhs[i], dz, self.y[i] - self.ys[i],
-                                      rho[i], self.eps_cor, self.rho_min, self.rho_max)
+                rho[i] = _spectral_combine(_spectral_est(ab_x[i], aa_x[i], bb_x[i], self.eps_cor),
+                                           _spectral_est(ab_z[i], aa_z, bb_z[i], self.eps_cor), rho[i],
+                                           self.rho_min, self.rho_max)
             self.xs[:] = X
             self.ys[:] = self.y
             self.yhs[:] = self.yh

@@ -18,7 +18,9 @@ TOL_ADMM = 1e-9
 
 DENSE_SHAPES = [(50, 7, 4), (200, 33, 10), (129, 5, 2), (300, 28, 2), (1000, 784, 10), (96, 3072, 10), (77, 65, 21),
                 (64, 31, 3), (100, 60, 2), (3000, 28, 2),
-                (1003, 784, 10), (101, 3072, 10)]  # DMMA shapes with a partial last row tile
+                (1003, 784, 10), (101, 3072, 10),  # DMMA shapes with a partial last row tile
+                # two-GEMM DMMA path (K != 9, even p): partial row / feature tiles, 1..13 class frags
+                (300, 34, 5), (129, 66, 2), (257, 200, 21), (130, 200, 100), (500, 96, 3), (389, 2048, 100)]
 
 
 def shards(nadmm, X, y, C):
