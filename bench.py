@@ -507,6 +507,9 @@ def main():
            "path": "nadmm_workers_solve per round (scatter z, y_i / gather x_i for all local nodes) + host "
                    "coordinator (paper_1807_07132_b200.dist.HostCoordinator, spectral penalty selection)"}
 
+    for w in workers:  # the shards' solver state is bound to the workers until they are released
+        w.close()
+
     # ---------------- time to target: theta = (F - F*)/F* <= 0.05 ----------------
     ttt, parity, cpu, fstar_info = {}, None, None, {}
     if not args.no_ttt:

@@ -262,6 +262,10 @@ typedef struct {                  /* AdmmConfig + PenaltyPolicy + StoppingConfig
     /* inner solver of the workers (InnerSolverKind, inc/admm.hpp:105-114; src/worker.cpp:170-195) */
     int32_t inner_solver;         /* 0 newton, 1 lbfgs (its max_iters is set to inner_iters) */
     nadmm_lbfgs_cfg lbfgs;
+    /* 1: bitwise-deterministic consensus: all-gather of the per-worker terms and the
+     * oracle's ascending-id pairwise tree for z on every rank (same worker count per rank, <= 64
+     * workers); 0: one allreduce of the rank sums */
+    int32_t consensus_tree;
 } nadmm_admm_cfg;
 
 void nadmm_admm_cfg_default(nadmm_admm_cfg* cfg);
@@ -284,8 +288,11 @@ typedef struct {                  /* MetricsRow subset (inc/metrics.hpp:15-27) *
 /* Runs the consensus loop over `n_local` shards resident on this rank's GPU (one ADMM worker per
  * shard). With comm == NULL the run is single-process over the given shards; otherwise every rank
  * calls this collectively and the global worker set is the concatenation of all ranks' shards in
- * rank order. The only data-path collective is one ncclAllReduce of the consensus sum per outer
- * iteration (+ one small allgather of per-rank scalars). z_out (d) is the final consensus vector on
+ * rank order. The only data-path collective is one ncclAllReduce per outer iteration of
+ * [consensus sum | sum rho | per-rank scalar slots] (the slots carry the previous iteration's residuals,
+ * norms and F_i(z), so rows, convergence and theta are completed one iteration late with N > 1 ranks;
+ * a stop drops the speculative iteration and returns z^k); consensus_tree = 1 replaces it by one
+ * ncclAllGather of the per-worker terms. z_out (d) is the final consensus vector on
  * every rank; rho_out (n_local) the final penalties of this rank's workers. */
 nadmm_status nadmm_admm_run(const nadmm_shard* shards, int32_t n_local, nadmm_comm comm, const nadmm_admm_cfg* cfg,
                             double* z_out, double* rho_out, nadmm_metrics_row* rows, int32_t row_cap,

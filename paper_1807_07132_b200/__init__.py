@@ -580,9 +580,15 @@ class Worker:
             raise ConfigError(f"out must be a contiguous float64 array of length {d}")
         return out
 
+    def close(self) -> None:
+        """Release the worker (and its binding of the shard's solver state)."""
+        if getattr(self, "handle", None):
+            L.lib().nadmm_worker_free(self.handle)
+            self.handle = None
+
     def __del__(self):
         try:
-            L.lib().nadmm_worker_free(self.handle)
+            self.close()
         except Exception:
             pass
 
@@ -616,6 +622,9 @@ class AdmmConfig:  # inc/admm.hpp:107-117
     inner_iters: int = 1
     inner_solver: str = "newton"  # InnerSolverKind (inc/admm.hpp:105-114): "newton" | "lbfgs"
     lbfgs: LbfgsConfig = field(default_factory=LbfgsConfig)
+    # bitwise-deterministic consensus: all-gather of the per-worker terms and the
+    # oracle's ascending-id pairwise tree for z, identical for any number of ranks
+    consensus_tree: bool = False
 
     def to_c(self) -> L.AdmmCfg:
         c = L.AdmmCfg()
@@ -632,6 +641,7 @@ class AdmmConfig:  # inc/admm.hpp:107-117
             raise ConfigError(f"unknown inner solver {self.inner_solver!r}")
         c.inner_solver = 1 if self.inner_solver == "lbfgs" else 0
         c.lbfgs = self.lbfgs.to_c()
+        c.consensus_tree = int(self.consensus_tree)
         return c
 
 

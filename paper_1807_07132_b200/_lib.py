@@ -65,7 +65,8 @@ class AdmmCfg(C.Structure):  # AdmmConfig + PenaltyPolicy + StoppingConfig (inc/
                 ("eps_abs", C.c_double), ("eps_rel", C.c_double), ("max_outer_iters", C.c_int32),
                 ("standard_norms", C.c_int32), ("inner_iters", C.c_int32), ("newton", NewtonCfg),
                 ("eval_objective", C.c_int32), ("f_star", C.c_double), ("theta_stop", C.c_double),
-                ("ignore_convergence", C.c_int32), ("inner_solver", C.c_int32), ("lbfgs", LbfgsCfg)]
+                ("ignore_convergence", C.c_int32), ("inner_solver", C.c_int32), ("lbfgs", LbfgsCfg),
+                ("consensus_tree", C.c_int32)]
 
 
 class MetricsRow(C.Structure):  # MetricsRow (inc/metrics.hpp:15-27)

@@ -13,6 +13,7 @@
 #include <nccl.h>
 
 #include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -45,21 +46,94 @@ constexpr int kMaxLocal = 16;
 struct LocalPtrs {
     const double* x[kMaxLocal];
     const double* y[kMaxLocal];
-    double rho[kMaxLocal];
     int n;
 };
 
 #define GRID_STRIDE(j, d) \
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < (d); j += (int64_t)gridDim.x * blockDim.x)
 
-// S_local = sum_i (rho_i x_i - y_i), ascending local worker id.
-__global__ void k_local_sum(int64_t d, LocalPtrs lp, double rho_sum, double* __restrict__ buf) {
+// Rank scalars carried in the consensus buffer's per-rank slots: the slots of other
+// ranks are zero, so the allreduce sum is a gather and every rank combines them in rank order.
+enum RankStat : int {
+    kStSumX = 0,    // sum_i |x_i|^2
+    kStMaxY = 1,    // max_i |y_i|^2
+    kStMaxPri = 2,  // max_i primal_i
+    kStMaxDual = 3, // max_i dual_i
+    kStPriSq = 4,   // sum_i primal_i^2
+    kStDualSq = 5,  // sum_i dual_i^2
+    kStF = 6,       // sum_i F_i(z)
+    kStZZ = 7,      // |z|^2
+    kStats = 8
+};
+
+// Consensus buffer of this rank: [S_local (d) | sum rho | kStats slots per rank]. S_local = sum_i
+// (rho_i x_i - y_i) in ascending local worker id; the rank's own slot carries the previous iteration's
+// rank scalars (they ride in this iteration's allreduce), the other slots are zero.
+__global__ void k_local_sum(int64_t d, LocalPtrs lp, const double* __restrict__ rho, double* __restrict__ buf,
+                            const double* __restrict__ stats_prev, int rank, int nranks) {
     GRID_STRIDE(j, d) {
-        double s = lp.rho[0] * lp.x[0][j] - lp.y[0][j];
-        for (int i = 1; i < lp.n; ++i) s += lp.rho[i] * lp.x[i][j] - lp.y[i][j];
+        double s = rho[0] * lp.x[0][j] - lp.y[0][j];
+        for (int i = 1; i < lp.n; ++i) s += rho[i] * lp.x[i][j] - lp.y[i][j];
         buf[j] = s;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) buf[d] = rho_sum;
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        if (threadIdx.x == 0) {
+            double rs = rho[0];
+            for (int i = 1; i < lp.n; ++i) rs += rho[i];
+            buf[d] = rs;
+        }
+        for (int q = threadIdx.x; q < kStats * nranks; q += 32)
+            buf[d + 1 + q] = (q / kStats == rank && stats_prev) ? stats_prev[q % kStats] : 0.0;
+    }
+}
+
+// Flush of the last iteration's rank scalars: this rank's slot = stats, the others zero.
+__global__ void k_fill_slots(double* __restrict__ slots, const double* __restrict__ stats, int rank, int nranks) {
+    for (int q = threadIdx.x; q < kStats * nranks; q += blockDim.x)
+        slots[q] = (q / kStats == rank) ? stats[q % kStats] : 0.0;
+}
+
+// Bitwise-deterministic mode: this rank's per-worker terms rho_i x_i - y_i (no FMA
+// contraction, as the oracle evaluates them), its rho_i and its stats slot, to be all-gathered.
+__global__ void k_local_terms(int64_t d, LocalPtrs lp, const double* __restrict__ rho, double* __restrict__ out,
+                              const double* __restrict__ stats_prev) {
+    GRID_STRIDE(j, d) {
+        for (int i = 0; i < lp.n; ++i) out[(int64_t)i * d + j] = __dsub_rn(__dmul_rn(rho[i], lp.x[i][j]), lp.y[i][j]);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        for (int i = 0; i < lp.n; ++i) out[(int64_t)lp.n * d + i] = rho[i];
+        for (int q = 0; q < kStats; ++q) out[(int64_t)lp.n * d + lp.n + q] = stats_prev ? stats_prev[q] : 0.0;
+    }
+}
+
+// Ascending-id pairwise tree over v[lo, hi) -- the oracle's tree_sum (mid = lo + ceil((hi - lo) / 2)),
+// additions without contraction.
+__device__ double tree_sum_dev(const double* v, int lo, int hi) {
+    if (hi - lo == 1) return v[lo];
+    const int mid = lo + (hi - lo + 1) / 2;
+    return __dadd_rn(tree_sum_dev(v, lo, mid), tree_sum_dev(v, mid, hi));
+}
+
+// z = tree(terms) / (lambda + tree(rho)) over all n_total workers in global id order.
+__global__ void k_tree_z(int64_t d, const double* __restrict__ g, int n_local, int nranks, double lambda,
+                         double* __restrict__ z, double* __restrict__ pz, double* part) {
+    __shared__ double red[32];
+    const int64_t blk = (int64_t)n_local * d + n_local + kStats;  // one rank's gathered block
+    const int n = n_local * nranks;
+    // worker w = r * n_local + i: term at g[r * blk + i * d + j]
+    double rh[64], tv[64];
+    for (int w = 0; w < n; ++w) rh[w] = g[(int64_t)(w / n_local) * blk + (int64_t)n_local * d + (w % n_local)];
+    const double denom = __dadd_rn(lambda, tree_sum_dev(rh, 0, n));
+    double zz = 0.0;
+    GRID_STRIDE(j, d) {
+        for (int w = 0; w < n; ++w) tv[w] = g[(int64_t)(w / n_local) * blk + (int64_t)(w % n_local) * d + j];
+        const double v = __ddiv_rn(tree_sum_dev(tv, 0, n), denom);
+        pz[j] = z[j];
+        z[j] = v;
+        zz += v * v;
+    }
+    const double t = block_sum(zz, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
 }
 
 // z_update: z = S / (lambda + sum rho); prev_z kept; partials |z|^2.
@@ -80,15 +154,22 @@ __global__ void k_z_update(int64_t d, const double* __restrict__ buf, double lam
 
 // Per worker: y_hat = y + rho (z_prev - x); y += rho (z - x); partials
 // of |z - x|^2 (primal), |rho (z - z_prev)|^2 (dual), |x|^2 and |y_new|^2 (tolerances).
-__global__ void k_worker_update(int64_t d, double rho, const double* __restrict__ x, double* __restrict__ y,
-                                double* __restrict__ yh, const double* __restrict__ z, const double* __restrict__ pz,
-                                double* part /* 4 x kBlockPartials */) {
+__global__ void k_worker_update(int64_t d, const double* __restrict__ rho_p, const double* __restrict__ x,
+                                double* __restrict__ y, double* __restrict__ yh, const double* __restrict__ z,
+                                const double* __restrict__ pz, double* part /* 4 x kBlockPartials */, int exact) {
     __shared__ double red[32];
+    const double rho = *rho_p;
     double pr = 0.0, du = 0.0, xx = 0.0, yy = 0.0;
     GRID_STRIDE(j, d) {
         const double xj = x[j], yj = y[j];
-        if (yh) yh[j] = yj + rho * (pz[j] - xj);
-        const double yn = yj + rho * (z[j] - xj);
+        double yn;
+        if (exact) {  // the oracle's evaluation order, no contraction (bitwise-deterministic mode)
+            if (yh) yh[j] = __dadd_rn(yj, __dmul_rn(rho, __dsub_rn(pz[j], xj)));
+            yn = __dadd_rn(yj, __dmul_rn(rho, __dsub_rn(z[j], xj)));
+        } else {
+            if (yh) yh[j] = yj + rho * (pz[j] - xj);
+            yn = yj + rho * (z[j] - xj);
+        }
         y[j] = yn;
         const double r = z[j] - xj;
         const double q = rho * (z[j] - pz[j]);
@@ -138,14 +219,55 @@ __global__ void k_reduce_groups(const double* part, int n, int count, double* ou
     if (threadIdx.x == 0) out[g] = v;
 }
 
-// Hybrid spectral step of one side (same arithmetic as the oracle's spectral_side).
-bool spectral_side(double ab, double aa, double bb, double eps_cor, double* est) {
+// This rank's scalars of the iteration from the reduced worker partials (wred[6 i + 0..3] = primal^2,
+// dual^2, |x|^2, |y|^2; wred[6 n] = |z|^2) and the F_i(z) values; fixed worker order.
+__global__ void k_rank_stats(const double* __restrict__ wred, const double* __restrict__ fz, int n, int eval,
+                             double* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double s[kStats] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < n; ++i) {
+        const double* w = wred + 6 * i;
+        const double prim = sqrt(w[0]), dual = sqrt(w[1]);
+        s[kStSumX] += w[2];
+        s[kStMaxY] = fmax(s[kStMaxY], w[3]);
+        s[kStMaxPri] = (isnan(prim) || isnan(s[kStMaxPri])) ? NAN : fmax(s[kStMaxPri], prim);
+        s[kStMaxDual] = (isnan(dual) || isnan(s[kStMaxDual])) ? NAN : fmax(s[kStMaxDual], dual);
+        s[kStPriSq] += w[0];
+        s[kStDualSq] += w[1];
+        if (eval) s[kStF] += fz[i];
+    }
+    s[kStZZ] = wred[6 * n];
+    for (int q = 0; q < kStats; ++q) out[q] = s[q];
+}
+
+// Hybrid spectral step of one side (the oracle's spectral_side).
+__host__ __device__ inline bool spectral_side_dev(double ab, double aa, double bb, double eps_cor, double* est) {
     if (!(aa > 0.0) || !(bb > 0.0) || !(ab > 0.0)) return false;
-    const double cor = ab / (std::sqrt(aa) * std::sqrt(bb));
+    const double cor = ab / (sqrt(aa) * sqrt(bb));
     if (!(cor > eps_cor)) return false;
     const double sd = bb / ab, mg = ab / aa;
     *est = (2.0 * mg > sd) ? mg : sd - mg / 2.0;
     return true;
+}
+
+// Spectral penalty update of every local worker on the device (no host round trip): rho_i from the
+// reduced secant dots wred[6 i .. 6 i + 5]; the solver parameters of the next iteration read rho_i.
+__global__ void k_sps_rho(const double* __restrict__ wred, int n, double eps_cor, double rho_min, double rho_max,
+                          double* __restrict__ rho) {
+    const int i = threadIdx.x;
+    if (blockIdx.x != 0 || i >= n) return;
+    const double* w = wred + 6 * i;
+    double ah = 0.0, bh = 0.0;
+    const bool xo = spectral_side_dev(w[0], w[1], w[2], eps_cor, &ah);
+    const bool zo = spectral_side_dev(w[3], w[4], w[5], eps_cor, &bh);
+    double r = rho[i];
+    if (xo && zo)
+        r = sqrt(ah * bh);
+    else if (xo)
+        r = sqrt(ah);
+    else if (zo)
+        r = sqrt(bh);
+    rho[i] = fmin(fmax(r, rho_min), rho_max);
 }
 
 template <typename T>
@@ -244,8 +366,52 @@ nadmm_status nadmm_comm_destroy(nadmm_comm c) {
 namespace nadmm {
 void set_last_error(const std::string& m);
 
+// Synchronise the stream of a collective-bearing step, failing fast instead of hanging when a peer
+// dies or stalls (the reference's TransportError after per-phase timeouts, src/comm.cpp:182-191,
+// 270-303): poll the stream and ncclCommGetAsyncError; after NADMM_COMM_TIMEOUT_MS (default 120 s)
+// abort the communicator and raise NADMM_ETRANSPORT.
+void comm_sync(cudaStream_t st, ncclComm_t comm) {
+    static const long long timeout_ms = [] {
+        const char* e = getenv("NADMM_COMM_TIMEOUT_MS");
+        return e ? atoll(e) : 120000LL;
+    }();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int spin = 0;; ++spin) {
+        const cudaError_t q = cudaStreamQuery(st);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) NADMM_CUDA(q);
+        ncclResult_t ar = ncclSuccess;
+        if (ncclCommGetAsyncError(comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress) {
+            ncclCommAbort(comm);
+            raise(NADMM_ETRANSPORT, std::string("NCCL asynchronous error: ") + ncclGetErrorString(ar));
+        }
+        const long long ms =
+            std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+        if (timeout_ms > 0 && ms > timeout_ms) {
+            ncclCommAbort(comm);
+            raise(NADMM_ETRANSPORT, "consensus collective timed out after " + std::to_string(ms) +
+                                        " ms (peer rank hung or dead)");
+        }
+        if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+    barrier_check();
+}
+
 // One consensus run (AdmmState + the run_admm loop); stepping lets callers time exact iteration
 // windows (bench.py) while nadmm_admm_run drives it to completion.
+//
+// Per outer iteration: ONE collective and ONE host synchronisation.
+//   * The consensus buffer [sum_i (rho_i x_i - y_i) | sum rho | per-rank scalar slots] is reduced by one
+//     ncclAllReduce; the scalar slots carry the PREVIOUS iteration's rank scalars (residuals, norms,
+//     F_i(z)) -- zero outside the rank's own slot, so the sum is a gather. With more than one rank an
+//     iteration's metrics row, convergence and theta tests are therefore completed one iteration
+//     later; when they stop the run at iteration k, the speculative iteration k+1 is discarded and
+//     z^k (kept as prev_z) is restored. Each step() call ends with a flush of the last row's slots.
+//   * rho_i lives on the device: the spectral penalty update runs as a kernel and
+//     the solvers read rho_i from it, so no host round trip sits between the secant dots and the next
+//     solve.
+//   * consensus_tree: ncclAllGather of the per-worker terms instead of the sum; every
+//     rank forms z with the oracle's ascending-id pairwise tree (bitwise identical for any rank count).
 struct AdmmRun {
     std::vector<Shard*> shards;
     nadmm_comm comm = nullptr;
@@ -256,17 +422,22 @@ struct AdmmRun {
     cudaStream_t st = nullptr;
     int64_t d = 0;
     int n_local = 0, n_total = 0, nranks = 1, rank = 0;
-    bool sps = false;
+    bool sps = false, tree = false, deferred = false;
     RunBuffers rb;
-    double *buf = nullptr, *z = nullptr, *pz = nullptr, *zs = nullptr, *zpart = nullptr, *wpart = nullptr;
-    double *wred = nullptr, *fz = nullptr, *rstat = nullptr, *gstat = nullptr;
+    double *buf = nullptr, *gbuf = nullptr, *z = nullptr, *pz = nullptr, *zs = nullptr, *zpart = nullptr;
+    double *wpart = nullptr, *wred = nullptr, *fz = nullptr, *rho_dev = nullptr;
+    double *stats_cur = nullptr, *stats_prev = nullptr, *fslots = nullptr, *hbuf = nullptr;  // hbuf: pinned
+    int64_t buf_len = 0, slot_off = 0;
     std::vector<double*> yh, xs, ys, yhs;
-    std::vector<double> rho, hstat, hred;
+    std::vector<double> rho, rho_prev;
     int vg = 1;
     int k = 0, snap_it = 0;
     bool conv = false, stop = false;
     cudaEvent_t ev_start = nullptr, ev_now = nullptr;
-    static constexpr int kStats = 8;
+    // a metrics row whose rank scalars arrive with the next collective (deferred mode)
+    bool row_pending = false;
+    nadmm_metrics_row pend{};
+    nadmm_metrics_row* pend_out = nullptr;
 
     AdmmRun(const nadmm_shard* sh, int32_t nl, nadmm_comm c, const nadmm_admm_cfg* cfg_in) : comm(c), n_local(nl) {
         if (!sh || nl < 1 || nl > kMaxLocal) raise(NADMM_ECONFIG, "need 1..16 local shards");
@@ -289,6 +460,9 @@ struct AdmmRun {
         if (cfg.inner_solver == 1) validate_lbfgs_cfg(lcfg);
         for (int i = 0; i < nl; ++i) {
             if (!sh[i]) raise(NADMM_ECONFIG, "null shard");
+            if (sh[i]->owner) raise(NADMM_ECONFIG, "shard is already bound to a live worker or ADMM session");
+            for (int j = 0; j < i; ++j)
+                if (sh[j] == sh[i]) raise(NADMM_ECONFIG, "the same shard is listed twice");
             shards.push_back(sh[i]);
         }
         ctx = shards[0]->ctx;
@@ -303,18 +477,35 @@ struct AdmmRun {
         nranks = comm ? comm->nranks : 1;
         rank = comm ? comm->rank : 0;
         n_total = n_local;
+        tree = cfg.consensus_tree != 0;
+        bool uniform = true;
         if (comm) {  // global worker count; workers are concatenated in rank order
             int* cnt = rb.get<int>(nranks);
             NADMM_CUDA(cudaMemcpyAsync(cnt + rank, &n_local, sizeof(int), cudaMemcpyHostToDevice, st));
             NADMM_NCCL(ncclAllGather(cnt + rank, cnt, 1, ncclInt, comm->comm, st));
             std::vector<int> h(nranks);
             NADMM_CUDA(cudaMemcpyAsync(h.data(), cnt, sizeof(int) * nranks, cudaMemcpyDeviceToHost, st));
-            stream_sync(st);
+            comm_sync(st, comm->comm);
             n_total = 0;
-            for (int v : h) n_total += v;
+            for (int v : h) {
+                n_total += v;
+                uniform = uniform && v == n_local;
+            }
         }
+        if (tree && (!uniform || n_total > 64))
+            raise(NADMM_ECONFIG, "consensus_tree needs the same worker count on every rank and <= 64 workers");
+        deferred = comm != nullptr;
         sps = cfg.penalty_kind == 1;
-        buf = rb.get<double>(d + 1);
+        if (tree) {  // per rank: n_local term vectors | n_local rho | kStats scalars
+            buf_len = (int64_t)n_local * d + n_local + kStats;
+            buf = rb.get<double>(buf_len);
+            gbuf = rb.get<double>(buf_len * nranks);
+            slot_off = (int64_t)n_local * d + n_local;
+        } else {
+            buf_len = d + 1 + (int64_t)kStats * nranks;
+            buf = rb.get<double>(buf_len);
+            slot_off = d + 1;
+        }
         z = rb.get<double>(d);
         pz = rb.get<double>(d);
         zs = sps ? rb.get<double>(d) : nullptr;
@@ -323,8 +514,11 @@ struct AdmmRun {
         wpart = rb.get<double>((int64_t)n_local * 6 * kBlockPartials);
         wred = rb.get<double>((int64_t)n_local * 6 + 2);
         fz = rb.get<double>(n_local);
-        rstat = rb.get<double>(kStats);
-        gstat = rb.get<double>((int64_t)kStats * nranks);
+        rho_dev = rb.get<double>(n_local);
+        stats_cur = rb.get<double>(kStats);
+        stats_prev = rb.get<double>(kStats);
+        fslots = rb.get<double>((int64_t)kStats * nranks);
+        NADMM_CUDA(cudaMallocHost(&hbuf, sizeof(double) * (size_t)(kStats * (nranks + 1) + n_local)));
         yh.assign(n_local, nullptr);
         xs.assign(n_local, nullptr);
         ys.assign(n_local, nullptr);
@@ -343,19 +537,95 @@ struct AdmmRun {
             if (s.cache_at == Shard::kAtX) s.cache_at = Shard::kNone;
         }
         rho.assign(n_local, cfg.rho0);
-        hstat.assign((size_t)kStats * nranks, 0.0);
-        hred.assign((size_t)n_local * 6 + 2, 0.0);
+        rho_prev = rho;
+        NADMM_CUDA(cudaMemcpyAsync(rho_dev, rho.data(), sizeof(double) * n_local, cudaMemcpyHostToDevice, st));
+        for (int i = 0; i < n_local; ++i) {
+            shards[i]->rho_src = rho_dev + i;  // the worker solves read rho_i from the device
+            shards[i]->owner = this;
+        }
         NADMM_CUDA(cudaEventCreate(&ev_start));
         NADMM_CUDA(cudaEventCreate(&ev_now));
         NADMM_CUDA(cudaEventRecord(ev_start, st));
+        stream_sync(st);
     }
 
     ~AdmmRun() {
+        for (Shard* s : shards) {
+            if (s->owner == this) s->owner = nullptr;
+            s->rho_src = nullptr;
+        }
+        if (hbuf) cudaFreeHost(hbuf);
         if (ev_start) cudaEventDestroy(ev_start);
         if (ev_now) cudaEventDestroy(ev_now);
     }
 
-    // One outer iteration (solve, gather, z, y, penalty, metrics).
+    void sync() {
+        if (comm)
+            comm_sync(st, comm->comm);
+        else
+            stream_sync(st);
+    }
+
+    // Rank scalars of all ranks (rank order) -> the row's norms / tolerances / F; returns conv and
+    // fills theta. `h` holds nranks x kStats scalars.
+    bool finish_row(const double* h, nadmm_metrics_row& m) {
+        double sx = 0.0, ymax = 0.0, pmax = 0.0, dmax = 0.0, psq = 0.0, dsq = 0.0, F = 0.0;
+        for (int r = 0; r < nranks; ++r) {  // rank order: deterministic combination
+            const double* s = h + (size_t)r * kStats;
+            sx += s[kStSumX];
+            ymax = std::max(ymax, s[kStMaxY]);
+            pmax = std::max(pmax, s[kStMaxPri]);
+            dmax = std::max(dmax, s[kStMaxDual]);
+            psq += s[kStPriSq];
+            dsq += s[kStDualSq];
+            F += s[kStF];
+            if (std::isnan(s[kStMaxPri]) || std::isnan(s[kStMaxDual])) pmax = NAN;
+        }
+        const double zz = h[kStZZ];
+        // tolerances (PAPER.md:223-224; SPEC.md:244-252), squared norms unless standard_norms
+        double a = sx, b = n_total * zz, c = ymax;
+        if (cfg.standard_norms) {
+            a = std::sqrt(sx);
+            b = std::sqrt((double)n_total) * std::sqrt(zz);
+            c = std::sqrt(ymax);
+        }
+        const double eps_pri = std::sqrt((double)n_total) * cfg.eps_abs + cfg.eps_rel * std::max(a, b);
+        const double eps_dual = std::sqrt((double)d) * cfg.eps_abs + cfg.eps_rel * c;
+        const double Fz = cfg.eval_objective ? F + 0.5 * cfg.lambda * zz : NAN;
+        m.train_objective = Fz;
+        m.theta = (cfg.eval_objective && cfg.f_star > 0.0) ? (Fz - cfg.f_star) / cfg.f_star : NAN;
+        m.primal_norm = std::sqrt(psq);
+        m.dual_norm = std::sqrt(dsq);
+        m.eps_pri = eps_pri;
+        m.eps_dual = eps_dual;
+        return m.iteration >= 1 && pmax <= eps_pri && dmax <= eps_dual;  // has_converged
+    }
+
+    bool stops(const nadmm_metrics_row& m, bool c) const {
+        if (c && !cfg.ignore_convergence) return true;
+        if (cfg.theta_stop > 0.0 && !std::isnan(m.theta) && m.theta <= cfg.theta_stop) return true;
+        return false;
+    }
+
+    // A deferred row's scalars arrived (gathered slots `h`): complete it; on a stop at its iteration,
+    // drop the speculative iteration that already ran (restore z^k and its penalties).
+    void complete_pending(const double* h, bool speculative_ran) {
+        const bool c = finish_row(h, pend);
+        if (pend_out) *pend_out = pend;
+        row_pending = false;
+        conv = c;
+        if (stops(pend, c)) {
+            stop = true;
+            if (speculative_ran) {
+                NADMM_CUDA(cudaMemcpyAsync(z, pz, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+                rho = rho_prev;
+                k = pend.iteration;
+            }
+        }
+    }
+
+    // One outer iteration (solve, gather, z, y, penalty, metrics). In deferred mode the
+    // row lands in `row` when the next collective (or flush) brings its rank scalars.
     void iterate(nadmm_metrics_row* row) {
         int inner = 0, cg_sum = 0, fe_sum = 0, flags = 0;
         std::vector<char> pending(n_local, 0);
@@ -405,26 +675,33 @@ struct AdmmRun {
                 NADMM_CUDA(cudaEventRecord(ctx->node_join[k2], ctx->node_stream[k2]));
                 NADMM_CUDA(cudaStreamWaitEvent(st, ctx->node_join[k2], 0));
             }
-        LocalPtrs lp{};  // (2) consensus sum + one allreduce
+        LocalPtrs lp{};  // (2) consensus buffer + the iteration's one collective
         lp.n = n_local;
-        double rho_sum = 0.0;
         for (int i = 0; i < n_local; ++i) {
             lp.x[i] = shards[i]->x;
             lp.y[i] = shards[i]->y;
-            lp.rho[i] = rho[i];
-            rho_sum += rho[i];
         }
-        k_local_sum<<<vg, 256, 0, st>>>(d, lp, rho_sum, buf);
+        const double* slots_prev = (deferred && k >= 1) ? stats_prev : nullptr;
+        if (tree) {
+            k_local_terms<<<vg, 256, 0, st>>>(d, lp, rho_dev, buf, slots_prev);
+            NADMM_LAUNCH_CHECK();
+            if (comm)
+                NADMM_NCCL(ncclAllGather(buf, gbuf, (size_t)buf_len, ncclDouble, comm->comm, st));
+            else
+                NADMM_CUDA(cudaMemcpyAsync(gbuf, buf, sizeof(double) * buf_len, cudaMemcpyDeviceToDevice, st));
+            k_tree_z<<<vg, 256, 0, st>>>(d, gbuf, n_local, nranks, cfg.lambda, z, pz, zpart);  // (3) z
+        } else {
+            k_local_sum<<<vg, 256, 0, st>>>(d, lp, rho_dev, buf, slots_prev, rank, nranks);
+            NADMM_LAUNCH_CHECK();
+            if (comm) NADMM_NCCL(ncclAllReduce(buf, buf, (size_t)buf_len, ncclDouble, ncclSum, comm->comm, st));
+            k_z_update<<<vg, 256, 0, st>>>(d, buf, cfg.lambda, z, pz, zpart);  // (3) z, y, residual partials
+        }
         NADMM_LAUNCH_CHECK();
-        ctx->stats.kernel_launches++;
-        if (comm) NADMM_NCCL(ncclAllReduce(buf, buf, d + 1, ncclDouble, ncclSum, comm->comm, st));
-        k_z_update<<<vg, 256, 0, st>>>(d, buf, cfg.lambda, z, pz, zpart);  // (3) z, y, residual partials
-        NADMM_LAUNCH_CHECK();
-        ctx->stats.kernel_launches++;
+        ctx->stats.kernel_launches += 2;
         for (int i = 0; i < n_local; ++i) {
             Shard& s = *shards[i];
-            k_worker_update<<<vg, 256, 0, st>>>(d, rho[i], s.x, s.y, sps ? yh[i] : nullptr, z, pz,
-                                                wpart + (int64_t)i * 6 * kBlockPartials);
+            k_worker_update<<<vg, 256, 0, st>>>(d, rho_dev + i, s.x, s.y, sps ? yh[i] : nullptr, z, pz,
+                                                wpart + (int64_t)i * 6 * kBlockPartials, tree ? 1 : 0);
             NADMM_LAUNCH_CHECK();
             ctx->stats.kernel_launches++;
         }
@@ -456,14 +733,28 @@ struct AdmmRun {
             ctx->stats.kernel_launches++;
         }
         k_reduce_groups<<<1, 32, 0, st>>>(zpart, vg, 1, wred + (int64_t)n_local * 6);
-        ctx->stats.kernel_launches++;
+        k_rank_stats<<<1, 32, 0, st>>>(wred, fz, n_local, cfg.eval_objective, stats_cur);
+        ctx->stats.kernel_launches += 2;
         NADMM_LAUNCH_CHECK();
-        std::vector<double> hfz(n_local, 0.0);
         NADMM_CUDA(cudaEventRecord(ev_now, st));  // z^k and F(z^k) are complete: the row's wall time
-        NADMM_CUDA(cudaMemcpyAsync(hred.data(), wred, sizeof(double) * hred.size(), cudaMemcpyDeviceToHost, st));
-        if (cfg.eval_objective)
-            NADMM_CUDA(cudaMemcpyAsync(hfz.data(), fz, sizeof(double) * n_local, cudaMemcpyDeviceToHost, st));
-        stream_sync(st);
+        rho_prev = rho;
+        if (sps && k - snap_it >= cfg.update_period) spectral();  // (4) SPS against the last snapshot (device)
+        // (5) the single readback: this rank's scalars of k, the gathered slots of k-1, rho after SPS
+        NADMM_CUDA(cudaMemcpyAsync(hbuf, stats_cur, sizeof(double) * kStats, cudaMemcpyDeviceToHost, st));
+        if (deferred && k >= 2) {
+            if (tree)
+                for (int r = 0; r < nranks; ++r)
+                    NADMM_CUDA(cudaMemcpyAsync(hbuf + (size_t)(r + 1) * kStats, gbuf + (int64_t)r * buf_len + slot_off,
+                                               sizeof(double) * kStats, cudaMemcpyDeviceToHost, st));
+            else
+                NADMM_CUDA(cudaMemcpyAsync(hbuf + kStats, buf + slot_off, sizeof(double) * kStats * nranks,
+                                           cudaMemcpyDeviceToHost, st));
+        }
+        NADMM_CUDA(cudaMemcpyAsync(hbuf + kStats * (nranks + 1), rho_dev, sizeof(double) * n_local,
+                                   cudaMemcpyDeviceToHost, st));
+        if (deferred)
+            NADMM_CUDA(cudaMemcpyAsync(stats_prev, stats_cur, sizeof(double) * kStats, cudaMemcpyDeviceToDevice, st));
+        sync();
         for (int i = 0; i < n_local; ++i) {  // gather the workers' inner stats
             Shard& s = *shards[i];
             if (pending[i] == 2) continue;  // L-BFGS stats already gathered
@@ -474,80 +765,45 @@ struct AdmmRun {
             fe_sum += r.fe_sum;
             flags |= r.flags;
         }
-        // rank scalars: sum|x_i|^2, max|y_i|^2, max primal_i, max dual_i, sum primal^2, sum dual^2, sum F_i, |z|^2
-        double rs[kStats] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int i = 0; i < n_local; ++i) {
-            const double* w = hred.data() + (int64_t)i * 6;
-            const double prim = std::sqrt(w[0]), dual = std::sqrt(w[1]);
-            rs[0] += w[2];
-            rs[1] = std::max(rs[1], w[3]);
-            rs[2] = std::max(rs[2], prim);
-            rs[3] = std::max(rs[3], dual);
-            rs[4] += w[0];
-            rs[5] += w[1];
-            rs[6] += hfz[i];
-            if (std::isnan(prim) || std::isnan(dual)) rs[2] = NAN;
-        }
-        rs[7] = hred[(size_t)n_local * 6];
-        if (comm) {
-            NADMM_CUDA(cudaMemcpyAsync(rstat, rs, sizeof rs, cudaMemcpyHostToDevice, st));
-            NADMM_NCCL(ncclAllGather(rstat, gstat, kStats, ncclDouble, comm->comm, st));
-            NADMM_CUDA(cudaMemcpyAsync(hstat.data(), gstat, sizeof(double) * hstat.size(), cudaMemcpyDeviceToHost, st));
-            stream_sync(st);
-        } else {
-            std::memcpy(hstat.data(), rs, sizeof rs);
-        }
-        double sx = 0.0, ymax = 0.0, pmax = 0.0, dmax = 0.0, psq = 0.0, dsq = 0.0, F = 0.0;
-        for (int r = 0; r < nranks; ++r) {  // rank order: deterministic combination
-            const double* h = hstat.data() + (size_t)r * kStats;
-            sx += h[0];
-            ymax = std::max(ymax, h[1]);
-            pmax = std::max(pmax, h[2]);
-            dmax = std::max(dmax, h[3]);
-            psq += h[4];
-            dsq += h[5];
-            F += h[6];
-            if (std::isnan(h[2])) pmax = NAN;
-        }
-        const double zz = hstat[7];
-        // tolerances (PAPER.md:223-224; SPEC.md:244-252), squared norms unless standard_norms
-        double a = sx, b = n_total * zz, c = ymax;
-        if (cfg.standard_norms) {
-            a = std::sqrt(sx);
-            b = std::sqrt((double)n_total) * std::sqrt(zz);
-            c = std::sqrt(ymax);
-        }
-        const double eps_pri = std::sqrt((double)n_total) * cfg.eps_abs + cfg.eps_rel * std::max(a, b);
-        const double eps_dual = std::sqrt((double)d) * cfg.eps_abs + cfg.eps_rel * c;
-        conv = k >= 1 && pmax <= eps_pri && dmax <= eps_dual;  // has_converged
-        if (sps && k - snap_it >= cfg.update_period) spectral();  // (4) SPS against the last snapshot
+        for (int i = 0; i < n_local; ++i) rho[i] = hbuf[kStats * (nranks + 1) + i];
         float ms = 0.f;
         NADMM_CUDA(cudaEventElapsedTime(&ms, ev_start, ev_now));
-        double theta = NAN;
-        const double Fz = cfg.eval_objective ? F + 0.5 * cfg.lambda * zz : NAN;
-        if (cfg.eval_objective && cfg.f_star > 0.0) theta = (Fz - cfg.f_star) / cfg.f_star;
-        if (row) {
-            nadmm_metrics_row& m = *row;
-            m.iteration = k;
-            m.wall_seconds = ms * 1e-3;
-            m.train_objective = Fz;
-            m.theta = theta;
-            m.primal_norm = std::sqrt(psq);
-            m.dual_norm = std::sqrt(dsq);
-            m.eps_pri = eps_pri;
-            m.eps_dual = eps_dual;
-            m.inner_iterations = inner;
-            m.cg_iters = cg_sum;
-            m.fn_evals = fe_sum;
-            m.flags = flags;
-            double rsum = 0.0;
-            for (double v : rho) rsum += v;
-            m.rho_mean = rsum / n_local;
-            m.messages = 2LL * n_total * k;
+        nadmm_metrics_row m{};
+        m.iteration = k;
+        m.wall_seconds = ms * 1e-3;
+        m.inner_iterations = inner;
+        m.cg_iters = cg_sum;
+        m.fn_evals = fe_sum;
+        m.flags = flags;
+        double rsum = 0.0;
+        for (double v : rho) rsum += v;
+        m.rho_mean = rsum / n_local;
+        m.messages = 2LL * n_total * k;
+        if (deferred) {
+            if (row_pending) complete_pending(hbuf + kStats, true);  // row k-1
+            if (stop) return;  // iteration k was speculative and is dropped
+            pend = m;
+            pend_out = row;
+            row_pending = true;
+        } else {
+            const bool c = finish_row(hbuf, m);
+            if (row) *row = m;
+            conv = c;
+            if (stops(m, c)) stop = true;
         }
-        if (conv && !cfg.ignore_convergence) stop = true;
-        if (cfg.theta_stop > 0.0 && !std::isnan(theta) && theta <= cfg.theta_stop) stop = true;
         if (k >= cfg.max_outer_iters) stop = true;
+    }
+
+    // Deferred mode: gather the last iteration's rank scalars (a small allreduce of the slots only)
+    // and complete its row.
+    void flush() {
+        if (!deferred || !row_pending) return;
+        k_fill_slots<<<1, 32, 0, st>>>(fslots, stats_prev, rank, nranks);
+        NADMM_LAUNCH_CHECK();
+        NADMM_NCCL(ncclAllReduce(fslots, fslots, (size_t)kStats * nranks, ncclDouble, ncclSum, comm->comm, st));
+        NADMM_CUDA(cudaMemcpyAsync(hbuf + kStats, fslots, sizeof(double) * kStats * nranks, cudaMemcpyDeviceToHost, st));
+        sync();
+        complete_pending(hbuf + kStats, false);
     }
 
     void spectral() {
@@ -558,22 +814,10 @@ struct AdmmRun {
             k_reduce_groups<<<6, 32, 0, st>>>(part, vg, 6, wred + (int64_t)i * 6);
             ctx->stats.kernel_launches += 2;
         }
+        k_sps_rho<<<1, 32, 0, st>>>(wred, n_local, cfg.eps_cor, cfg.rho_min, cfg.rho_max, rho_dev);
+        ctx->stats.kernel_launches++;
         NADMM_LAUNCH_CHECK();
-        NADMM_CUDA(cudaMemcpyAsync(hred.data(), wred, sizeof(double) * n_local * 6, cudaMemcpyDeviceToHost, st));
-        stream_sync(st);
         for (int i = 0; i < n_local; ++i) {
-            const double* w = hred.data() + (int64_t)i * 6;
-            double ah = 0.0, bh = 0.0;
-            const bool xo = spectral_side(w[0], w[1], w[2], cfg.eps_cor, &ah);
-            const bool zo = spectral_side(w[3], w[4], w[5], cfg.eps_cor, &bh);
-            double r = rho[i];
-            if (xo && zo)
-                r = std::sqrt(ah * bh);
-            else if (xo)
-                r = std::sqrt(ah);
-            else if (zo)
-                r = std::sqrt(bh);
-            rho[i] = std::min(std::max(r, cfg.rho_min), cfg.rho_max);
             Shard& s = *shards[i];
             NADMM_CUDA(cudaMemcpyAsync(xs[i], s.x, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
             NADMM_CUDA(cudaMemcpyAsync(ys[i], s.y, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
@@ -583,13 +827,16 @@ struct AdmmRun {
         snap_it = k;
     }
 
+    // Runs up to n outer iterations; returns the number of iterations kept (= metrics rows written).
     int step(int n, nadmm_metrics_row* rows, int row_cap) {
+        const int k0 = k;
         int done = 0;
         while (done < n && !stop) {
             iterate(rows && done < row_cap ? rows + done : nullptr);
             ++done;
         }
-        return done;
+        flush();
+        return k - k0;  // a deferred stop drops the speculative iteration
     }
 
     void result(double* z_out, double* rho_out) {

@@ -57,6 +57,14 @@ void check_ctx(nadmm_ctx c) {
     NADMM_CUDA(cudaSetDevice(c->device));
 }
 
+// Solver-level calls own the shard's iterate / z / y buffers for their duration; a shard bound to a
+// live Worker or ADMM session keeps its state (the reference's workers own their x_local,
+// src/worker.cpp:135), so such calls on it fail instead of clobbering the session.
+void check_unbound(nadmm_shard s, const void* caller = nullptr) {
+    if (s && s->owner && s->owner != caller)
+        raise(NADMM_ECONFIG, "shard is bound to a live worker or ADMM session (free it first)");
+}
+
 void check_shard(nadmm_shard s) {
     if (!s) raise(NADMM_ECONFIG, "null shard");
     NADMM_CUDA(cudaSetDevice(s->ctx->device));
@@ -80,7 +88,9 @@ void alloc_work(Shard& s) {
     const int64_t nk = (s.n + kRowPad) * s.K;
     s.L0 = dev_alloc<double>(s, nk);
     s.P = dev_alloc<double>(s, nk);
-    s.U = dev_alloc<double>(s, nk);
+    // the nonzero-group sparse passes gather U rows with a padded class stride (kernels_sparse.cu)
+    const bool lanes = s.sparse && s.K <= 32;
+    s.U = dev_alloc<double>(s, lanes ? (s.n + kRowPad) * sparse_class_stride(s.K) : nk);
     s.Lp = dev_alloc<double>(s, nk);
     s.rowM = dev_alloc<double>(s, s.n);
     s.rowA = dev_alloc<double>(s, s.n);
@@ -90,7 +100,7 @@ void alloc_work(Shard& s) {
         s.part_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(2LL * s.ctx->num_sms, cap));
         s.part = dev_alloc<double>(s, s.part_chunks * s.d);
     }
-    if (s.sparse && s.K <= 32) s.wt = dev_alloc<double>(s, s.d);
+    if (lanes) s.wt = dev_alloc<double>(s, s.p * sparse_class_stride(s.K));
     s.blk = dev_alloc<double>(s, (int64_t)kSlotCount * kBlockPartials);
     NADMM_CUDA(cudaMemsetAsync(s.blk, 0, sizeof(double) * kSlotCount * kBlockPartials, s.ctx->stream));
     for (double** v : {&s.x, &s.g, &s.pd, &s.r, &s.dv, &s.hd, &s.z, &s.y, &s.t, &s.tmp, &s.gbase, &s.cache_x}) {
@@ -418,7 +428,7 @@ nadmm_status nadmm_shard_csr(nadmm_ctx ctx, const int64_t* indptr, const int32_t
         NADMM_CUDA(cudaMemsetAsync(s->labels, 0, sizeof(int32_t) * (n + kRowPad), ctx->stream));
         upload(s->labels, labels, sizeof(int32_t) * n, ctx->stream);
         // column blocks for the rows pass: transposed weights of one block within ~48 MB of L2
-        const int64_t wbytes = 8 * (int64_t)(C - 1) * p;
+        const int64_t wbytes = 8 * (int64_t)sparse_class_stride(C - 1) * p;
         int64_t kBlockBudget = int64_t(48) << 20;
         if (const char* e = getenv("NADMM_SPARSE_BLOCK_KB")) kBlockBudget = std::max<int64_t>(1, atoll(e)) << 10;
         std::vector<int64_t> rblk;
@@ -438,7 +448,7 @@ nadmm_status nadmm_shard_csr(nadmm_ctx ctx, const int64_t* indptr, const int32_t
             s->nblk = nb;
             s->rblk = dev_alloc<int64_t>(*s, (int64_t)rblk.size());
             upload(s->rblk, rblk.data(), sizeof(int64_t) * rblk.size(), ctx->stream);
-            s->lsum = dev_alloc<double>(*s, n * (C - 1));
+            s->lsum = dev_alloc<double>(*s, n * sparse_class_stride(C - 1));
         }
         alloc_work(*s);
         stream_sync(ctx->stream);
@@ -567,6 +577,7 @@ nadmm_status nadmm_newton_solve(nadmm_shard s, const nadmm_newton_cfg* cfg, doub
                                 double rho, const double* z, const double* y, double* x_inout,
                                 nadmm_newton_iter* trace, int32_t trace_cap, nadmm_newton_summary* out) {
     return guard([&] {
+        check_unbound(s);
         check_shard(s);
         const nadmm_newton_cfg c = cfg_or_default(cfg);
         validate_newton_cfg(c);
@@ -604,6 +615,7 @@ nadmm_status nadmm_lbfgs_solve(nadmm_shard s, const nadmm_lbfgs_cfg* cfg, double
         nadmm_lbfgs_cfg_default(&c);
         if (cfg) c = *cfg;
         validate_lbfgs_cfg(c);
+        check_unbound(s);
         check_shard(s);
         if (!x_inout) raise(NADMM_ECONFIG, "x_inout required");
         if (augmented) {
@@ -631,16 +643,21 @@ extern "C" {
 
 nadmm_status nadmm_worker_create(nadmm_shard s, nadmm_worker* out) {
     return guard([&] {
+        check_unbound(s);
         check_shard(s);
         if (!out) raise(NADMM_ECONFIG, "null output");
         NADMM_CUDA(cudaMemsetAsync(s->x, 0, sizeof(double) * s->d, s->ctx->stream));  // x_local = 0
         if (s->cache_at == Shard::kAtX) s->cache_at = Shard::kNone;
         *out = new nadmm_worker_s{s};
+        s->owner = *out;  // x_local lives in the shard: one worker per shard
     });
 }
 
 nadmm_status nadmm_worker_free(nadmm_worker w) {
-    return guard([&] { delete w; });
+    return guard([&] {
+        if (w && w->shard && w->shard->owner == w) w->shard->owner = nullptr;
+        delete w;
+    });
 }
 
 nadmm_status nadmm_worker_solve(nadmm_worker w, double rho, const double* z, const double* y,
@@ -649,6 +666,7 @@ nadmm_status nadmm_worker_solve(nadmm_worker w, double rho, const double* z, con
     return guard([&] {
         if (!w) raise(NADMM_ECONFIG, "null worker");
         Shard& s = *w->shard;
+        check_unbound(w->shard, w);
         check_shard(w->shard);
         if (rho <= 0.0) raise(NADMM_ECONFIG, "augmented objective requires rho > 0");
         if (!z || !y) raise(NADMM_ECONFIG, "z and y required");
@@ -682,6 +700,7 @@ nadmm_status nadmm_workers_solve(const nadmm_worker* ws, int32_t n, const double
         for (int i = 0; i < n; ++i) {
             if (!ws[i]) raise(NADMM_ECONFIG, "null worker");
             sh[(size_t)i] = ws[i]->shard;
+            check_unbound(ws[i]->shard, ws[i]);
             if (sh[(size_t)i]->ctx != sh[0]->ctx) raise(NADMM_ECONFIG, "all workers must share one context");
             if (sh[(size_t)i]->d != sh[0]->d) raise(NADMM_ECONFIG, "worker weight dimensions differ");
             if (rho[i] <= 0.0) raise(NADMM_ECONFIG, "augmented objective requires rho > 0");
@@ -746,6 +765,7 @@ nadmm_status nadmm_worker_solve_lbfgs(nadmm_worker w, double rho, const double* 
         if (cfg) c = *cfg;
         c.max_iters = inner_iters;  // src/worker.cpp:184
         validate_lbfgs_cfg(c);
+        check_unbound(w->shard, w);
         check_shard(w->shard);
         if (rho <= 0.0) raise(NADMM_ECONFIG, "augmented objective requires rho > 0");
         if (!z || !y) raise(NADMM_ECONFIG, "z and y required");
@@ -771,6 +791,7 @@ nadmm_status nadmm_worker_sgd_grad(nadmm_worker w, const nadmm_sgd_cfg* cfg, uin
         if (!cfg) raise(NADMM_ECONFIG, "sgd session config required");
         Shard& s = *w->shard;
         validate_sgd(s, *cfg);
+        check_unbound(w->shard, w);
         check_shard(w->shard);
         if (!z || !g_out) raise(NADMM_ECONFIG, "z and g_out required");
         upload(s.z, z, sizeof(double) * s.d, s.ctx->stream);

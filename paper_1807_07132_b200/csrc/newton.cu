@@ -13,6 +13,8 @@
 
 namespace nadmm {
 
+__global__ void k_copy_rho(const double* src, DevParams* prm) { prm->rho = *src; }
+
 // ---- grid-barrier watchdog registry (common.cuh) ----
 namespace {
 std::vector<BarrierTU>& barrier_tus() {
@@ -181,6 +183,10 @@ void set_params(Shard& s, const nadmm_newton_cfg& c, double lambda, bool aug, do
     h.grad_tol = c.grad_tol;
     *s.prm_host = h;
     NADMM_CUDA(cudaMemcpyAsync(s.prm, s.prm_host, sizeof(DevParams), cudaMemcpyHostToDevice, s.ctx->stream));
+    if (aug && s.rho_src) {  // ADMM session: rho_i comes from the device-side penalty update
+        k_copy_rho<<<1, 1, 0, s.ctx->stream>>>(s.rho_src, s.prm);
+        NADMM_LAUNCH_CHECK();
+    }
 }
 
 void set_lambda_only(Shard& s, double lambda) {

@@ -142,6 +142,8 @@ struct Shard {
     unsigned long long* gbar = nullptr;  // grid-barrier counters of the persistent vector kernels
     int rows_grid = 0;  // blocks of the last rows pass (partials count)
     int last_chunks = 0;    // split-K partial chunks written by the last fused DMMA pass
+    void* owner = nullptr;            // live Worker / ADMM session bound to this shard's solver state
+    const double* rho_src = nullptr;  // ADMM session: the augmentation penalty rho_i lives on the device
     void* gemm = nullptr;   // GemmState of the two-GEMM DMMA path (kernels_gemm.cu), null when unused
     int dmma_clusters = 0;  // co-resident clusters of the fused DMMA pass (0: path unavailable)
     int dmma_mt = 0, dmma_nw = 0, dmma_cs = 0, dmma_fs = 0, dmma_S = 0, dmma_pipe = 0;  // chosen layout
@@ -239,6 +241,7 @@ int op_hv_split(Shard& s, const double* v, double* out, const double* dotvec, in
 
 // ---- class-per-lane sparse passes (kernels_sparse.cu): CSR shards with C - 1 <= 32 ----
 bool sparse_lanes_supported(const Shard& s);
+int sparse_class_stride(int K);  // padded class stride of the gathered tables (K rounded up to even)
 void sparse_rows_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
 int sparse_cols_pass(Shard& s, XtuKind kind, const double* vin, double* out, const double* dotvec, int dot_slot,
                      const int32_t* guard);

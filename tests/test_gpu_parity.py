@@ -176,17 +176,19 @@ def test_worker_sequence_matches_reference(nadmm, ref):
         assert sg.inner_iters == sr["inner_iters"]
 
 
-@pytest.mark.parametrize("penalty", ["fixed", "spectral"])
+@pytest.mark.parametrize("penalty", ["fixed", "spectral", "tree"])
 def test_admm_run_matches_oracle(nadmm, port, penalty):
     N, C, p = 4, 4, 10
     Xtr, ytr, _, _ = port.generate_synthetic(1200, p, C, separation=3.0, noise=1.0, seed=0)
     owner = port.partition_owner(len(ytr), N)
     parts_o = [oracle.Shard(Xtr[owner == i], ytr[owner == i], C) for i in range(N)]
     parts_g = [nadmm.Dataset.dense(Xtr[owner == i], ytr[owner == i], C) for i in range(N)]
+    tree = penalty == "tree"  # bitwise-deterministic consensus mode: the oracle's pairwise z tree
+    penalty = "spectral" if tree else penalty
     cfg_o = oracle.admm_cfg(n_workers=N, lam=1e-5, penalty=penalty, max_outer_iters=40)
     ro = port.admm_run(parts_o, cfg_o)
     cfg = nadmm.AdmmConfig(n_workers=N, lam=1e-5, penalty=nadmm.PenaltyPolicy(kind=penalty),
-                           stopping=nadmm.StoppingConfig(max_outer_iters=40))
+                           stopping=nadmm.StoppingConfig(max_outer_iters=40), consensus_tree=tree)
     rg = nadmm.run_admm(parts_g, cfg, nadmm.EvalContext(eval_objective=True))
     assert rg.iterations == ro["iterations"]
     assert rg.converged == ro["converged"]
@@ -199,6 +201,33 @@ def test_admm_run_matches_oracle(nadmm, port, penalty):
     yall = np.concatenate([s.labels for s in parts_o])
     full_g = nadmm.Dataset.dense(Xall, yall, C)
     np.testing.assert_array_equal(nadmm.predict(full_g, rg.z), port.predict(oracle.Shard(Xall, yall, C), ro["z"]))
+
+
+def test_shard_binding(nadmm):
+    """A shard's solver state (x_local, z, y) belongs to one live Worker or ADMM session at a time
+    (the reference's workers own their x_local, src/worker.cpp:135): other solver-level calls on it
+    raise ConfigError instead of clobbering it; model-level calls stay allowed."""
+    rng = np.random.default_rng(8)
+    X, y = random_dense(rng, 120, 10, 3, scale=0.5)
+    ds = nadmm.Dataset.dense(X, y, 3)
+    d = ds.weight_dim()
+    w = nadmm.Worker(ds)
+    with pytest.raises(nadmm.ConfigError):
+        nadmm.Worker(ds)
+    with pytest.raises(nadmm.ConfigError):
+        nadmm.newton_solve(nadmm.make_softmax_objective(ds, 1e-3), np.zeros(d))
+    with pytest.raises(nadmm.ConfigError):
+        nadmm.run_admm([ds], nadmm.AdmmConfig(n_workers=1, lam=1e-3))
+    x1, _ = w.solve(1.0, np.zeros(d), np.zeros(d))
+    assert np.isfinite(nadmm.loss(ds, x1, 1e-3))  # model level: fine
+    x2, _ = w.solve(1.0, np.zeros(d), np.zeros(d))  # warm start survived the model-level call
+    w.close()
+    nadmm.newton_solve(nadmm.make_softmax_objective(ds, 1e-3), np.zeros(d))
+    sess = nadmm.AdmmSession([ds], nadmm.AdmmConfig(n_workers=1, lam=1e-3))
+    with pytest.raises(nadmm.ConfigError):
+        nadmm.Worker(ds)
+    sess.close()
+    nadmm.Worker(ds).close()
 
 
 def test_workers_round_matches_reference(nadmm, ref):

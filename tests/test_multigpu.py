@@ -31,6 +31,12 @@ def _data():
 
 
 def _cfg(nadmm, penalty):
+    if penalty == "tree":  # bitwise-deterministic consensus
+        return nadmm.AdmmConfig(n_workers=NODES, lam=LAM, penalty=nadmm.PenaltyPolicy(kind="spectral"),
+                                stopping=nadmm.StoppingConfig(max_outer_iters=25), consensus_tree=True)
+    if penalty == "theta":  # deferred theta_stop: the speculative iteration is dropped, z^k returned
+        return nadmm.AdmmConfig(n_workers=NODES, lam=LAM, penalty=nadmm.PenaltyPolicy(kind="spectral"),
+                                stopping=nadmm.StoppingConfig(max_outer_iters=25))
     if penalty == "lbfgs":  # L-BFGS inner solver (fixed penalty)
         return nadmm.AdmmConfig(n_workers=NODES, lam=LAM, stopping=nadmm.StoppingConfig(max_outer_iters=10),
                                 inner_iters=3, inner_solver="lbfgs", lbfgs=nadmm.LbfgsConfig(grad_tol=1e-6))
@@ -41,7 +47,13 @@ def _cfg(nadmm, penalty):
 SGD = dict(eta=0.05, batch=40, epochs=3, seed=4)
 
 
-def _rank(rank, world, port, penalty, out):
+def _eval(nadmm, penalty, f_star):
+    if penalty == "theta":
+        return nadmm.EvalContext(eval_objective=True, f_star=f_star, theta_stop=0.02)
+    return nadmm.EvalContext(eval_objective=True)
+
+
+def _rank(rank, world, port, penalty, out, f_star=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -60,7 +72,7 @@ def _rank(rank, world, port, penalty, out):
             out[rank] = {"z": res.x, "it": res.epochs, "conv": False,
                          "F": [r["train_objective"] for r in res.metrics]}
         else:
-            res = nadmm.run_admm(shards, _cfg(nadmm, penalty), nadmm.EvalContext(eval_objective=True), comm)
+            res = nadmm.run_admm(shards, _cfg(nadmm, penalty), _eval(nadmm, penalty, f_star), comm)
             out[rank] = {"z": res.z, "it": res.iterations, "conv": res.converged,
                          "F": [r["train_objective"] for r in res.metrics]}
         comm.close()
@@ -68,15 +80,19 @@ def _rank(rank, world, port, penalty, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("penalty", ["fixed", "spectral", "lbfgs", "sgd"])
+@pytest.mark.parametrize("penalty", ["fixed", "spectral", "lbfgs", "sgd", "tree", "theta"])
 def test_two_ranks_match_single_process(nadmm, penalty):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs two GPUs")
-    out = mp.Manager().dict()
-    mp.start_processes(_rank, args=(2, _free_port(), penalty, out), nprocs=2, join=True, start_method="spawn")
     Xtr, ytr, owner = _data()
     ctx = nadmm.Context(0)
     shards = [nadmm.Dataset.dense(Xtr[owner == i], ytr[owner == i], C, ctx=ctx) for i in range(NODES)]
+    f_star = None
+    if penalty == "theta":  # a target the loop reaches mid-run: F at iteration 25, minus 1 %
+        full = nadmm.run_admm(shards, _cfg(nadmm, "spectral"), nadmm.EvalContext(eval_objective=True))
+        f_star = 0.99 * full.metrics[-1]["train_objective"]
+    out = mp.Manager().dict()
+    mp.start_processes(_rank, args=(2, _free_port(), penalty, out, f_star), nprocs=2, join=True, start_method="spawn")
     if penalty == "sgd":  # cross-rank sums regroup the worker order: equal to rounding, not bitwise
         res = nadmm.sync_sgd(shards, nadmm.SgdConfig(**SGD), LAM)
         for r in range(2):
@@ -85,7 +101,12 @@ def test_two_ranks_match_single_process(nadmm, penalty):
             np.testing.assert_allclose(out[r]["F"], [m["train_objective"] for m in res.metrics], rtol=1e-9)
         np.testing.assert_array_equal(out[0]["z"], out[1]["z"])
         return
-    ref = nadmm.run_admm(shards, _cfg(nadmm, penalty), nadmm.EvalContext(eval_objective=True))
+    ref = nadmm.run_admm(shards, _cfg(nadmm, penalty), _eval(nadmm, penalty, f_star))
+    if penalty == "theta":
+        assert 1 <= ref.iterations < 25 and ref.metrics[-1]["theta"] <= 0.02
+    if penalty == "tree":  # same z bits for one and two ranks (x_i identical per worker)
+        for r in range(2):
+            np.testing.assert_array_equal(out[r]["z"], ref.z)
     for r in range(2):
         assert out[r]["it"] == ref.iterations and out[r]["conv"] == ref.converged
         np.testing.assert_allclose(out[r]["z"], ref.z, rtol=1e-9, atol=1e-12)
