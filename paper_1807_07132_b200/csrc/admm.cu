@@ -106,12 +106,13 @@ __global__ void k_local_terms(int64_t d, LocalPtrs lp, const double* __restrict_
     }
 }
 
-// Ascending-id pairwise tree over v[lo, hi) -- the oracle's tree_sum (mid = lo + ceil((hi - lo) / 2)),
-// additions without contraction.
-__device__ double tree_sum_dev(const double* v, int lo, int hi) {
-    if (hi - lo == 1) return v[lo];
+// Ascending-id pairwise tree over the gathered worker values (the oracle's tree_sum: mid = lo +
+// ceil((hi - lo) / 2)), additions without contraction. Worker w's value sits at
+// g[(w / nl) * blk + base + (w % nl) * stride] (rank-major gathered blocks). Recursion depth <= 7.
+__device__ double tree_sum_dev(const double* g, int64_t blk, int nl, int64_t base, int64_t stride, int lo, int hi) {
+    if (hi - lo == 1) return g[(int64_t)(lo / nl) * blk + base + (int64_t)(lo % nl) * stride];
     const int mid = lo + (hi - lo + 1) / 2;
-    return __dadd_rn(tree_sum_dev(v, lo, mid), tree_sum_dev(v, mid, hi));
+    return __dadd_rn(tree_sum_dev(g, blk, nl, base, stride, lo, mid), tree_sum_dev(g, blk, nl, base, stride, mid, hi));
 }
 
 // z = tree(terms) / (lambda + tree(rho)) over all n_total workers in global id order.
@@ -120,14 +121,10 @@ __global__ void k_tree_z(int64_t d, const double* __restrict__ g, int n_local, i
     __shared__ double red[32];
     const int64_t blk = (int64_t)n_local * d + n_local + kStats;  // one rank's gathered block
     const int n = n_local * nranks;
-    // worker w = r * n_local + i: term at g[r * blk + i * d + j]
-    double rh[64], tv[64];
-    for (int w = 0; w < n; ++w) rh[w] = g[(int64_t)(w / n_local) * blk + (int64_t)n_local * d + (w % n_local)];
-    const double denom = __dadd_rn(lambda, tree_sum_dev(rh, 0, n));
+    const double denom = __dadd_rn(lambda, tree_sum_dev(g, blk, n_local, (int64_t)n_local * d, 1, 0, n));
     double zz = 0.0;
     GRID_STRIDE(j, d) {
-        for (int w = 0; w < n; ++w) tv[w] = g[(int64_t)(w / n_local) * blk + (int64_t)(w % n_local) * d + j];
-        const double v = __ddiv_rn(tree_sum_dev(tv, 0, n), denom);
+        const double v = __ddiv_rn(tree_sum_dev(g, blk, n_local, j, d, 0, n), denom);
         pz[j] = z[j];
         z[j] = v;
         zz += v * v;
