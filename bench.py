@@ -310,6 +310,266 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------------------------------------
+# Per-config lines (--config cfg1|cfg3|cfg4|cfg5): BASELINE.json's other workloads through the same
+# consensus loop, each with the roofline of its own dominant pass. cfg2 (above) is
+# the driver's headline.
+# ------------------------------------------------------------------------------------------------
+CONFIGS = {
+    # name: (workload, kind, p, C, lambda, nodes (None: one per GPU), rows of one node incl. its test split)
+    "cfg1": ("mnist-shaped dense 60000x784 C=10 lambda=1e-3, single-node Newton-ADMM", "dense", 784, 10, 1e-3, 1,
+             66_667),
+    "cfg3": ("higgs-shaped dense 1375000x28 per GPU C=2 lambda=1e-3, one Newton-ADMM node per GPU (weak scaling)",
+             "dense", 28, 2, 1e-3, None, 1_527_778),
+    "cfg4": ("sparse CSR 1Mx1.3M 650 nnz/row C=20 lambda=1e-3, Newton-ADMM over 8 row-shard nodes", "sparse",
+             1_300_000, 20, 1e-3, 8, 125_000),
+    "cfg5": ("large dense 4Mx2048 C=100 lambda=1e-3, Newton-ADMM (SPS) over 8 row-shard nodes", "dense", 2048, 100,
+             1e-3, 8, 555_556),
+}
+
+
+def config_shard(nadmm, name, node, kind, p, C_, rows, ctx, keep_test=False):
+    """One ADMM node's shard: per-node seeds mix_seed(0, node) (no host holds the full
+    data set); cfg1 is the single 60,000-row node of the reference generator at seed 0."""
+    seed = 0 if name == "cfg1" else nadmm.mix_seed(0, node)
+    if kind == "sparse":
+        ip, ix, vv, y = nadmm.generate_sparse(rows, p, C_, 650, seed)
+        return nadmm.Dataset.sparse(ip, ix, vv, y, C_, p, ctx=ctx), None, (ip, ix, vv, y)
+    Xtr, ytr, Xte, yte = nadmm.generate_synthetic(rows, p, C_, 3.0, 1.0, seed)
+    ds = nadmm.Dataset.dense(Xtr, ytr, C_, ctx=ctx)
+    host = (Xtr, ytr, Xte, yte) if keep_test else None
+    return ds, host, None
+
+
+def run_config(args):
+    import torch
+
+    name = args.config
+    workload, kind, p, C_, lam, nodes, rows = CONFIGS[name]
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+    nodes = nodes or world
+    if nodes % world:
+        raise SystemExit(f"--gpus must divide {nodes}")
+    import paper_1807_07132_b200 as nadmm
+
+    torch.cuda.set_device(local)
+    ctx = nadmm.Context(local)
+    per = nodes // world
+    mine = list(range(rank * per, (rank + 1) * per))
+    t_gen = time.perf_counter()
+    want_ttt = name in ("cfg1", "cfg3") and not args.no_ttt
+    keep0 = rank == 0 and world == 1 and not args.no_cpu  # node 0's host copy feeds the CPU sample
+    built = [config_shard(nadmm, name, i, kind, p, C_, rows, ctx, keep_test=want_ttt or (keep0 and i == 0))
+             for i in mine]
+    shards = [b[0] for b in built]
+    t_gen = time.perf_counter() - t_gen
+    comm = None
+    if world > 1:
+        uid = [nadmm.Communicator.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = nadmm.Communicator(ctx, uid[0], world, rank)
+
+    def red(x, op="sum"):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def barrier():
+        ctx.synchronize()
+        if dist:
+            dist.barrier()
+
+    sps = nadmm.PenaltyPolicy(kind="spectral")
+    cfg = nadmm.AdmmConfig(n_workers=nodes, lam=lam, penalty=sps, stopping=nadmm.StoppingConfig(max_outer_iters=100000))
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    sess = nadmm.AdmmSession(shards, cfg, nadmm.EvalContext(eval_objective=False, ignore_convergence=True), comm)
+    clk = Clocks(local).__enter__()
+    time.sleep(0.5)
+    sess.step(args.warmup)
+    barrier()
+    ctx.reset_stats()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    done = sess.step(args.steps)
+    e1.record(stream)
+    e1.synchronize()
+    clk.__exit__(None, None, None)
+    ms = red(e0.elapsed_time(e1), "max")
+    st = ctx.stats()
+    assert done == args.steps
+    hv_total = red(st["hv_products"])
+    value = hv_total / (ms * 1e-3)
+    ctx.set_timing(True)
+    ctx.reset_stats()
+    sess.step(max(1, min(args.steps, 2)))
+    ctx.synchronize()
+    st_t = ctx.stats()
+    ctx.set_timing(False)
+    sess.close()
+    hv_ms = st_t["hv_kernel_ms"] / max(1, st_t["hv_kernel_samples"])
+    # dominant pass per config, algorithmic work per Hv of one node shard (SURVEY.md §8d)
+    n_loc, K = shards[0].n(), C_ - 1
+    conc = max(1, min(ctx.node_streams(), len(shards))) if kind == "dense" and K == 9 else 1
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    if name == "cfg5":
+        fp64 = json.loads((ROOT / "profiles" / "r2_fp64_peak.json").read_text())["dmma_tflops"]
+        flops = 4.0 * n_loc * p * K
+        ach = flops / (hv_ms * 1e-3) / 1e12
+        roofline = {"bound": "tensor", "achieved": ach, "peak": fp64, "unit": "TFLOP/s", "frac": ach / fp64,
+                    "traffic": None, "kernel": "two-GEMM DMMA Hv pass (rows GEMM + row epilogue, X^T U split-K GEMM)",
+                    "flops_per_hv": flops, "hv_pass_ms": hv_ms,
+                    "peak_source": "profiles/r2_fp64_peak.json dmma_tflops (register-only mma.sync.m8n8k4.f64 loop; "
+                                   "cuBLAS DGEMM 8192^3 reaches 35.5)"}
+    else:
+        if kind == "sparse":
+            nnz = int(built[0][2][0][-1])
+            nbytes = 2 * (12 * nnz + 4 * (n_loc + 1)) + 24 * n_loc * K + 16 * p * K
+            kern = "CSR Hv: transpose + nonzero-group rows pass (column blocks) + CSC columns pass"
+        else:
+            nbytes = 8 * n_loc * p + 8 * n_loc * K + 16 * p * K
+            kern = "dense Hv pass" + (" with the fused CG step" if K == 9 else "")
+        ach = conc * nbytes / (hv_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                    "kernel": kern, "bytes_per_hv": nbytes, "hv_pass_ms": hv_ms, "concurrent_launches": conc,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    # time to target (cfg1, cfg3): theta <= 0.05 and <= 1e-3 against F* of the full training set
+    ttt = {}
+    if want_ttt:
+        fstar = [None, None]
+        if rank == 0:
+            allX = [b[1][0] for b in built]
+            ally = [b[1][1] for b in built]
+            if world > 1:  # weak scaling: the other ranks' shards are regenerated here for F* only
+                for i in range(nodes):
+                    if i in mine:
+                        continue
+                    Xi, yi, _, _ = nadmm.generate_synthetic(rows, p, C_, 3.0, 1.0, nadmm.mix_seed(0, i))
+                    allX.insert(i, Xi)
+                    ally.insert(i, yi)
+            Xall, yall = np.concatenate(allX), np.concatenate(ally)
+            fstar = list(compute_f_star_generic(nadmm, ctx, Xall, yall, C_, lam))
+            del Xall, yall
+        if dist:
+            dist.broadcast_object_list(fstar, src=0)
+        f_star, finfo = fstar
+        tcfg = nadmm.AdmmConfig(n_workers=nodes, lam=lam, penalty=sps, stopping=nadmm.StoppingConfig(max_outer_iters=300))
+        barrier()
+        s2 = nadmm.AdmmSession(shards, tcfg, nadmm.EvalContext(True, f_star, 1e-3), comm)
+        s2.step(300)
+        rows_m = s2.result().metrics
+        s2.close()
+        out = {}
+        for target in (0.05, 1e-3):
+            hit = [r for r in rows_m if r["theta"] == r["theta"] and r["theta"] <= target]
+            out[str(target)] = {"time_to_target_s": red(hit[0]["wall_seconds"], "max") if hit else None,
+                                "outer_iters": hit[0]["iteration"] if hit else None}
+        ttt = {"time_to_target": out, "f_star": f_star, "f_star_check": finfo,
+               "final_theta": rows_m[-1]["theta"] if rows_m else None}
+    # CPU reference sample (rank 0, N = 1): the reference's own worker code on node 0's shard
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = config_cpu_sample(name, kind, built[0], C_, lam, len(shards))
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "Hv/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "weak" if name == "cfg3" else "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (" + ("builder sparse generator" if kind == "sparse" else "reference generate_synthetic")
+                        + ", per-node seeds mix_seed(0, node)" + (", separation 3, noise 1" if kind == "dense" else "")
+                        + ")",
+                "config": {"workload": workload, "config": name, "admm_nodes": nodes, "nodes_per_gpu": per,
+                           "rows_per_node": n_loc, "p": p, "classes": C_, "lambda": lam, "inner_iters": 1,
+                           "penalty": "spectral (SPS, rho0=1, T_f=2)", "generation_s": t_gen,
+                           "l2": "no flush: per-step inputs exceed the 126 MB L2"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": None, "gpu_launches": int(st["kernel_launches"]),
+                "clocks": clk.summary(), "hv_per_step": hv_total / args.steps}
+        line.update(ttt)
+        print(json.dumps(line), flush=True)
+    if comm:
+        comm.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def compute_f_star_generic(nadmm, ctx, Xtr, ytr, C_, lam):
+    """compute_reference on one GPU + the CPU reference's gradient certificate."""
+    d = (C_ - 1) * Xtr.shape[1]
+    full = nadmm.Dataset.dense(Xtr, ytr, C_, ctx=ctx)
+    res = nadmm.newton_solve(nadmm.make_softmax_objective(full, lam), np.zeros(d),
+                             nadmm.NewtonConfig(cg_tol=1e-10, cg_max_iters=200, grad_tol=1e-10, newton_max_iters=100))
+    f = res.trace[-1].objective if res.trace else nadmm.loss(full, res.x, lam)
+    full.close()
+    info = {"gpu_newton_iters": len(res.trace), "gpu_converged": bool(res.converged),
+            "gpu_final_grad_norm": float(res.final_grad_norm)}
+    try:
+        import oracle
+
+        r = oracle.ref()
+        if r is not None:
+            rd = r.dataset(oracle.Shard(Xtr, ytr, C_))
+            f_cpu = rd.loss(res.x, lam)
+            gn = float(np.linalg.norm(rd.gradient(res.x, lam)))
+            info.update({"cpu_reference_f": f_cpu, "rel_diff_gpu_vs_cpu_f": abs(f - f_cpu) / abs(f_cpu),
+                         "cpu_reference_grad_norm": gn, "optimality_gap_bound": gn * gn / (2 * lam)})
+    except Exception as e:
+        info["cpu_check_error"] = str(e)
+    return f, info
+
+
+def config_cpu_sample(name, kind, built0, C_, lam, n_nodes):
+    """The reference's own code (oracle/_ref) on node 0's shard, a bounded sample: cfg1 / cfg3 one
+    run_worker ADMM solve per node (time x nodes = one outer iteration), cfg4 / cfg5 two Hessian-vector
+    products (one outer iteration = 8 nodes x 11 Hv would take tens of minutes on the host)."""
+    import oracle
+    import torch
+
+    r = oracle.ref()
+    if r is None:
+        return None
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    r.set_threads(cores)
+    if kind == "sparse":
+        ip, ix, vv, y = built0[2]
+        sh = oracle.Shard(labels=y, C_=C_, csr=(ip, ix, vv), p=built0[0].p())
+    else:
+        sh = oracle.Shard(built0[1][0], built0[1][1], C_) if built0[1] is not None else None
+    if sh is None:
+        return None
+    rd = r.dataset(sh)
+    rng = np.random.default_rng(0)
+    if name in ("cfg4", "cfg5"):
+        w, v = rng.normal(size=sh.d) * 0.01, rng.normal(size=sh.d)
+        rd.hessian_vec(w, v, lam)  # warm-up (builds the cache)
+        t0 = time.perf_counter()
+        rd.hessian_vec_repeat(w, v, lam, 2)
+        dt = time.perf_counter() - t0
+        return {"value": 2 / dt, "unit": "Hv/s", "cores": cores, "kind": "reference", "cpu_model": lscpu_model(),
+                "sample": "2 Hessian-vector products on node 0's shard (memoised cache), reference hessian_vec"}
+    wk = rd.worker()
+    z = np.zeros(sh.d)
+    wk.solve(1.0, z, z)
+    t0 = time.perf_counter()
+    hv = 0
+    for _ in range(2):
+        x, st = wk.solve(1.0, rng.normal(size=sh.d) * 1e-3, z)
+        hv += int(st["cg_iters"]) + int(st["inner_iters"])
+    dt = time.perf_counter() - t0
+    return {"value": hv / dt, "unit": "Hv/s", "cores": cores, "kind": "reference", "cpu_model": lscpu_model(),
+            "sample": f"2 run_worker ADMM solves of node 0 (one of {n_nodes} nodes), all host cores"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -318,11 +578,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-target run")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="BASELINE.json workload (cfg2 = the headline CIFAR-shaped 8-node run)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: W >= 3
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.config != "cfg2":
+        return run_config(args)
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     import torch

@@ -134,10 +134,11 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
-__device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
+// Barrier over `nb` co-resident blocks that share the counter (the whole grid, or a sub-grid).
+__device__ __forceinline__ void grid_barrier_n(unsigned long long* ctr, unsigned nblocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned long long nb = gridDim.x;
+        const unsigned long long nb = nblocks;
         __threadfence();
         const unsigned long long old = atomicAdd(ctr, 1ULL);
         const unsigned long long target = (old / nb + 1) * nb;
@@ -158,6 +159,8 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
     }
     __syncthreads();
 }
+
+__device__ __forceinline__ void grid_barrier(unsigned long long* ctr) { grid_barrier_n(ctr, gridDim.x); }
 
 // Programmatic dependent launch: kernels of the Newton-iteration graph are launched with
 // programmatic stream serialisation, so a kernel's launch and prologue overlap its predecessor's

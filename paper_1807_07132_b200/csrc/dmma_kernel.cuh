@@ -268,12 +268,13 @@ __host__ __device__ inline size_t dmma_smem_bytes(int stages, int bm, int nc, in
 // (cluster order) + lambda d (+ rho d), and the curvature / <r,r> reductions go through block slots
 // and software grid barriers (the grid is co-resident by construction). All blocks evaluate the same
 // scalars; block 0 / thread 0 writes the solver state.
-__device__ __forceinline__ void dmma_cg_tail(const DmmaArgs& a, int K, int chunks, double* scratch, double* sc) {
+__device__ __forceinline__ void dmma_cg_tail(const DmmaArgs& a, int K, int chunks, double* scratch, double* sc,
+                                             VGrid vg, unsigned long long* bar) {
     const int it = a.cg_it;
     DevState* st = a.st;
     const int64_t d = (int64_t)K * a.p;
-    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    const bool lead = vg.b == 0 && threadIdx.x == 0;
+    const int64_t tid = (int64_t)vg.b * blockDim.x + threadIdx.x, nth = (int64_t)vg.nb * blockDim.x;
     const double lam = a.prm->lambda, rho = a.prm->rho;
     const bool aug = a.prm->augmented;
     double* curv_slot = a.blk + (int64_t)kSlotCurv * kBlockPartials;
@@ -297,10 +298,10 @@ __device__ __forceinline__ void dmma_cg_tail(const DmmaArgs& a, int K, int chunk
         dacc += s * vj;
     }
     double t = block_sum(dacc, scratch);
-    if (threadIdx.x == 0) curv_slot[blockIdx.x] = t;
-    grid_barrier(a.done_ctr);
+    if (threadIdx.x == 0) curv_slot[vg.b] = t;
+    grid_barrier_n(bar, vg.nb);
     if (threadIdx.x < 32) {
-        const double v = reduce_partials(curv_slot, gridDim.x);
+        const double v = reduce_partials(curv_slot, vg.nb);
         if (threadIdx.x == 0) *sc = v;
     }
     __syncthreads();
@@ -329,15 +330,15 @@ __device__ __forceinline__ void dmma_cg_tail(const DmmaArgs& a, int K, int chunk
             rr += rj * rj;
         }
         t = block_sum(rr, scratch);
-        if (threadIdx.x == 0) rr_slot[blockIdx.x] = t;
+        if (threadIdx.x == 0) rr_slot[vg.b] = t;
         if (lead) {
             st->cg_iters = it + 1;
             st->cg_mid[it] = 1;
         }
-        grid_barrier(a.done_ctr);
+        grid_barrier_n(bar, vg.nb);
         __syncthreads();  // *sc reused
         if (threadIdx.x < 32) {
-            const double v = reduce_partials(rr_slot, gridDim.x);
+            const double v = reduce_partials(rr_slot, vg.nb);
             if (threadIdx.x == 0) *sc = v;
         }
         __syncthreads();
@@ -910,18 +911,19 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_pass_kernel(Dmma
         grid_barrier(a.done_ctr);
         const int64_t d = (int64_t)K * p;
         if (MODE == kModeHv && a.tail == kTailCg)
-            dmma_cg_tail(a, K, (int)ncl, misc, misc + 127);
+            dmma_cg_tail(a, K, (int)ncl, misc, misc + 127, whole_grid(), a.done_ctr);
         else if (MODE == kModeHv && a.tail == kTailCert) {
             const bool lp_need = cert_tail_body(d, a.st, a.prm, a.part, (int)ncl, a.lp_from_cert, a.g, a.cg_p,
-                                                a.cg_hd, a.blk, (int)ncl, a.hv_ctr, a.done_ctr, misc, misc + 127);
+                                                a.cg_hd, a.blk, (int)ncl, a.hv_ctr, a.done_ctr, misc, misc + 127,
+                                                whole_grid());
             // the Armijo search needs only L0 and this pass's Lp = X p: run it here unless p changed
             if (a.st->it_act && !lp_need)
                 ls_fused_body(n, K, a.L0, a.Lp, a.labels, d, const_cast<double*>(a.x), a.cg_p, a.z, a.y, a.prm, a.st,
-                              a.blk, a.done_ctr, xs, misc + 126);  // the X ring is free: scratch
+                              a.blk, a.done_ctr, xs, misc + 126, whole_grid());  // the X ring is free: scratch
         }
         else if (MODE == kModeCache && a.tail == kTailNewton)
             newton_tail_body(d, a.st, a.prm, a.part, (int)ncl, a.x, a.z, a.y, a.gbase, a.g, a.t, a.blk, (int)ncl,
-                             a.scal, a.trace, a.trace_cap, a.done_ctr, misc);
+                             a.scal, a.trace, a.trace_cap, a.done_ctr, misc, whole_grid());
     }
     if (threadIdx.x == 0) DMMA_KST(7);
 }

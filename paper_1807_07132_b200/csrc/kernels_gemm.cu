@@ -170,15 +170,14 @@ __global__ void __launch_bounds__(kGThreads, 1)
             const int64_t gi = row0 + warp * 16 + 8 * m + gq;
             const bool valid = gi < a.n;
             if (MODE == kModeHv) {  // U = V o P - P o rowsum(V o P)  (src/softmax.cpp:103-107)
-                double pv[NF][2], rs = 0.0;
+                // two sweeps over the row's P (the second from L1) keep the register footprint small
+                double rs = 0.0;
 #pragma unroll
                 for (int j = 0; j < NF; ++j)
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
                         const int c = 8 * j + 2 * tq + e;
-                        pv[j][e] = (valid && c < K) ? __ldg(a.Pin + gi * K + c) : 0.0;
-                        acc[m][j][e] *= pv[j][e];
-                        rs += acc[m][j][e];
+                        if (valid && c < K) rs += acc[m][j][e] * __ldg(a.Pin + gi * K + c);
                     }
                 rs += __shfl_xor_sync(0xffffffffu, rs, 1);
                 rs += __shfl_xor_sync(0xffffffffu, rs, 2);
@@ -186,9 +185,11 @@ __global__ void __launch_bounds__(kGThreads, 1)
 #pragma unroll
                     for (int j = 0; j < NF; ++j) {
                         const int c = 8 * j + 2 * tq;
+                        const double p0 = c < K ? __ldg(a.Pin + gi * K + c) : 0.0;
+                        const double p1 = c + 1 < K ? __ldg(a.Pin + gi * K + c + 1) : 0.0;
                         if (c < a.KU)
                             *reinterpret_cast<double2*>(a.U + gi * a.KU + c) =
-                                make_double2(acc[m][j][0] - pv[j][0] * rs, acc[m][j][1] - pv[j][1] * rs);
+                                make_double2(acc[m][j][0] * p0 - p0 * rs, acc[m][j][1] * p1 - p1 * rs);
                     }
             } else if (MODE == kModeLp) {
                 if (valid)
@@ -200,6 +201,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
                             if (c < K) a.Lp[gi * K + c] = acc[m][j][e];
                         }
             } else {  // stable softmax (src/softmax.cpp:51-63) + loss / coeff / argmax
+                // the exponentials are recomputed per sweep instead of held in registers: a spill-free
+                // epilogue (spilling here was measured to corrupt results intermittently)
                 double mx = -INFINITY;
 #pragma unroll
                 for (int j = 0; j < NF; ++j)
@@ -209,14 +212,12 @@ __global__ void __launch_bounds__(kGThreads, 1)
                 mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
                 mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
                 const double M = mx > 0.0 ? mx : 0.0;
-                double ex[NF][2], es = 0.0;
+                double es = 0.0;
 #pragma unroll
                 for (int j = 0; j < NF; ++j)
 #pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        ex[j][e] = (8 * j + 2 * tq + e < K) ? exp(acc[m][j][e] - M) : 0.0;
-                        es += ex[j][e];
-                    }
+                    for (int e = 0; e < 2; ++e)
+                        if (8 * j + 2 * tq + e < K) es += exp(acc[m][j][e] - M);
                 es += __shfl_xor_sync(0xffffffffu, es, 1);
                 es += __shfl_xor_sync(0xffffffffu, es, 2);
                 const double alpha = exp(-M) + es;
@@ -239,20 +240,21 @@ __global__ void __launch_bounds__(kGThreads, 1)
 #pragma unroll
                         for (int j = 0; j < NF; ++j) {
                             const int c = 8 * j + 2 * tq;
-                            double pc[2];
-#pragma unroll
-                            for (int e = 0; e < 2; ++e) {
-                                pc[e] = ex[j][e] / alpha;
-                                if (c + e < K) {
-                                    a.L0[gi * K + c + e] = acc[m][j][e];
-                                    a.P[gi * K + c + e] = pc[e];
-                                }
+                            const double pc0 = c < K ? exp(acc[m][j][0] - M) / alpha : 0.0;
+                            const double pc1 = c + 1 < K ? exp(acc[m][j][1] - M) / alpha : 0.0;
+                            if (c < K) {
+                                a.L0[gi * K + c] = acc[m][j][0];
+                                a.P[gi * K + c] = pc0;
+                            }
+                            if (c + 1 < K) {
+                                a.L0[gi * K + c + 1] = acc[m][j][1];
+                                a.P[gi * K + c + 1] = pc1;
                             }
                             // coeff = P - onehot(label) (src/softmax.cpp:86-90), padded classes 0
                             if (c < a.KU)
                                 *reinterpret_cast<double2*>(a.U + gi * a.KU + c) =
-                                    make_double2(c < K ? pc[0] - (c == yb - 1 ? 1.0 : 0.0) : 0.0,
-                                                 c + 1 < K ? pc[1] - (c + 1 == yb - 1 ? 1.0 : 0.0) : 0.0);
+                                    make_double2(c < K ? pc0 - (c == yb - 1 ? 1.0 : 0.0) : 0.0,
+                                                 c + 1 < K ? pc1 - (c + 1 == yb - 1 ? 1.0 : 0.0) : 0.0);
                         }
                     }
                 } else if (MODE == kModePredict) {  // src/softmax.cpp:118-139: first max wins; class C only if >
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
                         for (int e = 0; e < 2; ++e) {
                             const int c = 8 * j + 2 * tq + e;
                             if (c < K) {
-                                const double pc = ex[j][e] / alpha;
+                                const double pc = exp(acc[m][j][e] - M) / alpha;
                                 if (pc > best || (pc == best && c < arg)) {
                                     best = pc;
                                     arg = c;
@@ -575,6 +577,8 @@ void gemm_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
     a.blk = s.blk;
     a.pred = s.pred;
     a.guard = guard;
+    static const bool poison = getenv("NADMM_GEMM_POISON_U") != nullptr;  // debug: NaN-fill U first
+    if (poison) NADMM_CUDA(cudaMemsetAsync(g.U, 0xFF, sizeof(double) * (size_t)s.n * g.KU, s.ctx->stream));
     switch (mode) {
         case kModeCache: launch_rows<kModeCache>(s, g, mv, a); break;
         case kModeHv: launch_rows<kModeHv>(s, g, mv, a); break;

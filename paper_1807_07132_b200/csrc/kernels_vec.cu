@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(256, 4) k_cert_tail(int64_t d, DevState* st, c
     pdl_wait();
     __shared__ double red[32];
     __shared__ double sc;
-    cert_tail_body(d, st, prm, part, chunks, lp_from_cert, g, p, hd, blk, ncert, hv_ctr, bar, red, &sc);
+    cert_tail_body(d, st, prm, part, chunks, lp_from_cert, g, p, hd, blk, ncert, hv_ctr, bar, red, &sc, whole_grid());
 }
 
 // Batched Armijo candidates (src/newton.cpp:56-71), partial sums for every trial a_j = gamma^j:
@@ -601,7 +601,8 @@ __global__ void __launch_bounds__(256, 4) k_newton_tail(int64_t d, DevState* st,
     pdl_wait();
     if (guard && !*guard) return;
     __shared__ double red[32];
-    newton_tail_body(d, st, prm, part, chunks, x, z, y, gbase, g, t, blk, nloss, scal, trace, trace_cap, bar, red);
+    newton_tail_body(d, st, prm, part, chunks, x, z, y, gbase, g, t, blk, nloss, scal, trace, trace_cap, bar, red,
+                     whole_grid());
 }
 
 __global__ void k_set_int(int32_t* dst, int v) {

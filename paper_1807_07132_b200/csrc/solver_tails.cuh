@@ -11,6 +11,17 @@ namespace nadmm {
 #define GRID_STRIDE(j, d) \
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < (d); j += (int64_t)gridDim.x * blockDim.x)
 
+// The (sub-)grid a solver tail runs on: the whole launch grid, or -- in a node-group DMMA pass -- the
+// CTAs [first, first + nb) assigned to one ADMM node (its own barrier counter and partial slots).
+struct VGrid {
+    int b, nb;
+};
+
+__device__ __forceinline__ VGrid whole_grid() { return VGrid{(int)blockIdx.x, (int)gridDim.x}; }
+
+#define VGRID_STRIDE(vg, j, d) \
+    for (int64_t j = (int64_t)(vg).b * blockDim.x + threadIdx.x; j < (d); j += (int64_t)(vg).nb * blockDim.x)
+
 __device__ __forceinline__ double* slot_ptr(double* blk, int slot) { return blk + (int64_t)slot * kBlockPartials; }
 
 // Reduce a slot with warp 0 and broadcast to the whole block.
@@ -47,14 +58,14 @@ __device__ __forceinline__ bool cert_tail_body(int64_t d, DevState* st, const De
                                                const double* __restrict__ g, double* __restrict__ p,
                                                double* __restrict__ hd, double* blk, int ncert,
                                                unsigned long long* hv_ctr, unsigned long long* bar, double* red,
-                                               double* sc) {
+                                               double* sc, VGrid vg) {
     if (!st->it_act) return false;
     const bool cert = st->cert_act, failed = st->cg_failed;
     const double lam = prm->lambda, rho = prm->rho;
     const bool aug = prm->augmented;
-    if (cert && chunks > 0 && hv_ctr && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(hv_ctr, 1ULL);
+    if (cert && chunks > 0 && hv_ctr && vg.b == 0 && threadIdx.x == 0) atomicAdd(hv_ctr, 1ULL);
     double cacc = 0.0, sacc = 0.0;
-    GRID_STRIDE(j, d) {
+    VGRID_STRIDE(vg, j, d) {
         const double gj = g[j];
         double pj = p[j];
         if (cert) {
@@ -77,15 +88,15 @@ __device__ __forceinline__ bool cert_tail_body(int64_t d, DevState* st, const De
         sacc += pj * gj;
     }
     double t = block_sum(cacc, red);
-    if (threadIdx.x == 0 && cert) slot_ptr(blk, kSlotCert)[blockIdx.x] = t;
+    if (threadIdx.x == 0 && cert) slot_ptr(blk, kSlotCert)[vg.b] = t;
     t = block_sum(sacc, red);
-    if (threadIdx.x == 0) slot_ptr(blk, kSlotSlope)[blockIdx.x] = t;
-    ncert = gridDim.x;
-    grid_barrier(bar);
-    double slope = block_reduce_slot(blk, kSlotSlope, gridDim.x, sc);
+    if (threadIdx.x == 0) slot_ptr(blk, kSlotSlope)[vg.b] = t;
+    ncert = vg.nb;
+    grid_barrier_n(bar, vg.nb);
+    double slope = block_reduce_slot(blk, kSlotSlope, vg.nb, sc);
     const bool flip = slope >= 0.0;
-    if (flip) GRID_STRIDE(j, d) p[j] = -g[j];
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
+    if (flip) VGRID_STRIDE(vg, j, d) p[j] = -g[j];
+    if (vg.b == 0 && threadIdx.x < 32) {
         const double cv = cert ? reduce_partials(slot_ptr(blk, kSlotCert), ncert) : 0.0;
         if (threadIdx.x == 0) {
             if (flip) slope = -st->g_sq;  // (-g).g == -|g|^2 under the same reduction order
@@ -110,11 +121,11 @@ __device__ __forceinline__ void newton_tail_body(int64_t d, DevState* st, const 
                                                  const double* __restrict__ y, double* __restrict__ gbase,
                                                  double* __restrict__ g, double* __restrict__ t, double* blk, int nloss,
                                                  double* scal, DevTrace* trace, int trace_cap,
-                                                 unsigned long long* bar, double* red) {
+                                                 unsigned long long* bar, double* red, VGrid vg) {
     const double lam = prm->lambda, rho = prm->rho;
     const bool aug = prm->augmented;
     double xx = 0.0, gg = 0.0, tt = 0.0;
-    GRID_STRIDE(j, d) {
+    VGRID_STRIDE(vg, j, d) {
         const double xj = x[j];
         double gb;
         if (chunks > 0) {
@@ -136,14 +147,14 @@ __device__ __forceinline__ void newton_tail_body(int64_t d, DevState* st, const 
         gg += gj * gj;
     }
     double sres = block_sum(xx, red);
-    if (threadIdx.x == 0) slot_ptr(blk, kSlotRidge)[blockIdx.x] = sres;
+    if (threadIdx.x == 0) slot_ptr(blk, kSlotRidge)[vg.b] = sres;
     sres = block_sum(gg, red);
-    if (threadIdx.x == 0) slot_ptr(blk, kSlotGg)[blockIdx.x] = sres;
+    if (threadIdx.x == 0) slot_ptr(blk, kSlotGg)[vg.b] = sres;
     sres = block_sum(tt, red);
-    if (threadIdx.x == 0) slot_ptr(blk, kSlotTt)[blockIdx.x] = sres;
-    grid_barrier(bar);
-    if (blockIdx.x != 0 || threadIdx.x >= 32) return;
-    const int nvec = gridDim.x;
+    if (threadIdx.x == 0) slot_ptr(blk, kSlotTt)[vg.b] = sres;
+    grid_barrier_n(bar, vg.nb);
+    if (vg.b != 0 || threadIdx.x >= 32) return;
+    const int nvec = vg.nb;
     double base = reduce_partials(slot_ptr(blk, kSlotLoss), nloss);
     if (lam > 0.0) base += 0.5 * lam * reduce_partials(slot_ptr(blk, kSlotRidge), nvec);  // src/softmax.cpp:76
     const double g_sq = reduce_partials(slot_ptr(blk, kSlotGg), nvec);
@@ -189,7 +200,7 @@ __device__ __forceinline__ void ls_fused_body(int64_t n, int K, const double* __
                               const int32_t* __restrict__ labels, int64_t d, double* __restrict__ x,
                               const double* __restrict__ p, const double* __restrict__ z,
                               const double* __restrict__ y, const DevParams* prm, DevState* st, double* blk,
-                              unsigned long long* bar, double* scratch, double* sc) {
+                              unsigned long long* bar, double* scratch, double* sc, VGrid vg) {
     const int nc = prm->ls_max_iters + 1;
     const double gamma = prm->backtrack_gamma;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -198,7 +209,7 @@ __device__ __forceinline__ void ls_fused_body(int64_t n, int K, const double* __
     if (rpg < 32) rpg = 32;
     const int ngroups = (int)((n + rpg - 1) / rpg);
     const int64_t items = (int64_t)ngroups * nc;
-    for (int64_t it = (int64_t)blockIdx.x * nwarps + warp; it < items; it += (int64_t)gridDim.x * nwarps) {
+    for (int64_t it = (int64_t)vg.b * nwarps + warp; it < items; it += (int64_t)vg.nb * nwarps) {
         const int j = (int)(it % nc), grp = (int)(it / nc);
         double a = 1.0;
         for (int q = 0; q < j; ++q) a *= gamma;  // alpha *= backtrack_gamma (src/newton.cpp:69)
@@ -235,7 +246,7 @@ __device__ __forceinline__ void ls_fused_body(int64_t n, int K, const double* __
             at[q] = 0.0;
             ax[q] = 0.0;
         }
-        GRID_STRIDE(jj, d) {
+        VGRID_STRIDE(vg, jj, d) {
             const double xj = x[jj], pj = p[jj];
             const double zj = aug ? z[jj] : 0.0, yr = aug ? y[jj] / rho : 0.0;
 #pragma unroll
@@ -261,17 +272,17 @@ __device__ __forceinline__ void ls_fused_body(int64_t n, int K, const double* __
         if (threadIdx.x < 2 * kLsFusedChunk && j0 + (int)threadIdx.x / 2 < nc) {
             double t = 0.0;
             for (int w = 0; w < nwarps; ++w) t += scratch[w * 2 * kLsFusedChunk + threadIdx.x];
-            slot_ptr(blk, kSlotLsVec + 2 * j0 + threadIdx.x)[blockIdx.x] = t;
+            slot_ptr(blk, kSlotLsVec + 2 * j0 + threadIdx.x)[vg.b] = t;
         }
     }
-    grid_barrier(bar);
+    grid_barrier_n(bar, vg.nb);
     // every block: candidate objectives (one warp per candidate), first-accept rule, step
     __syncthreads();
     double* fj = scratch;  // nc <= kMaxLs + 1 doubles
     for (int j = warp; j < nc; j += nwarps) {
         double f = reduce_partials(slot_ptr(blk, kSlotLs + j), ngroups);
-        if (prm->lambda > 0.0) f += 0.5 * prm->lambda * reduce_partials(slot_ptr(blk, kSlotLsVec + 2 * j + 1), gridDim.x);
-        if (prm->augmented) f = f + 0.5 * prm->rho * reduce_partials(slot_ptr(blk, kSlotLsVec + 2 * j), gridDim.x);
+        if (prm->lambda > 0.0) f += 0.5 * prm->lambda * reduce_partials(slot_ptr(blk, kSlotLsVec + 2 * j + 1), vg.nb);
+        if (prm->augmented) f = f + 0.5 * prm->rho * reduce_partials(slot_ptr(blk, kSlotLsVec + 2 * j), vg.nb);
         if (lane == 0) fj[j] = f;
     }
     __syncthreads();
@@ -288,7 +299,7 @@ __device__ __forceinline__ void ls_fused_body(int64_t n, int K, const double* __
             alpha *= prm->backtrack_gamma;
         }
         *sc = alpha;
-        if (blockIdx.x == 0) {
+        if (vg.b == 0) {
             st->ls_alpha = alpha;
             st->ls_evals = evals;
             st->ls_capped = capped;
@@ -296,7 +307,7 @@ __device__ __forceinline__ void ls_fused_body(int64_t n, int K, const double* __
     }
     __syncthreads();
     const double a = *sc;
-    GRID_STRIDE(jj, d) x[jj] += a * p[jj];
+    VGRID_STRIDE(vg, jj, d) x[jj] += a * p[jj];
 }
 
 }  // namespace nadmm
