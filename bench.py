@@ -667,10 +667,16 @@ def main():
     st_t = ctx.stats()
     ctx.set_timing(False)
     hv_ms = st_t["hv_kernel_ms"] / max(1, st_t["hv_kernel_samples"])
-    # the local nodes' solves run on `conc` concurrent streams (each DMMA shard on a 1/conc-GPU grid),
-    # so the Hv kernels stream conc shards at once: aggregate rate = conc x bytes per launch / duration
-    conc = max(1, min(ctx.node_streams(), len(shards)))
-    achieved = conc * hv_bytes(n_loc) / (hv_ms * 1e-3) / 1e9
+    shards_per_launch = st_t["hv_kernel_shards"] / max(1, st_t["hv_kernel_samples"])
+    if shards_per_launch > 1.0:
+        # node-group passes: one whole-GPU launch streams every active node's shard
+        conc = 1
+        achieved = shards_per_launch * hv_bytes(n_loc) / (hv_ms * 1e-3) / 1e9
+    else:
+        # the local nodes' solves on `conc` concurrent streams (each DMMA shard on a 1/conc-GPU grid):
+        # the Hv kernels stream conc shards at once: aggregate rate = conc x bytes per launch / duration
+        conc = max(1, min(ctx.node_streams(), len(shards)))
+        achieved = conc * hv_bytes(n_loc) / (hv_ms * 1e-3) / 1e9
     peaks = {}
     try:
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -685,9 +691,9 @@ def main():
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "traffic_source": "profiles/r1_hv_kernel.json (ncu dram__bytes_read+write)", "kernel": "dense Hv pass with the fused CG step (shard 6250x3072), CUDA events around each launch",
-                "hv_pass_ms": hv_ms, "concurrent_launches": conc,
-                "per_launch_achieved": hv_bytes(n_loc) / (hv_ms * 1e-3) / 1e9,
+                "traffic": traffic, "traffic_source": "profiles/r1_hv_kernel.json (ncu dram__bytes_read+write)", "kernel": "dense Hv pass with the fused CG step (node-group launch over the GPU's 6250x3072 shards, or one shard per node stream), CUDA events around each launch",
+                "hv_pass_ms": hv_ms, "concurrent_launches": conc, "shards_per_launch": shards_per_launch,
+                "per_launch_achieved": shards_per_launch * hv_bytes(n_loc) / (hv_ms * 1e-3) / 1e9,
                 "step_check": "value x bytes_per_hv = whole-step Hv traffic rate (lower bound incl. non-Hv kernels)",
                 "bytes_per_hv": hv_bytes(n_loc), "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"}
     sess_res = sess.result()

@@ -71,6 +71,7 @@ typedef struct {
     int64_t data_passes;        /* full passes over shard feature matrices */
     double hv_kernel_ms;        /* device time inside Hv pass kernels (only when timing enabled) */
     int64_t hv_kernel_samples;  /* launches timed into hv_kernel_ms */
+    int64_t hv_kernel_shards;   /* shard products inside those launches (> samples for node-group passes) */
 } nadmm_stats;
 
 nadmm_status nadmm_ctx_stats(nadmm_ctx ctx, nadmm_stats* out);

@@ -56,7 +56,7 @@ class InnerStats(C.Structure):  # InnerStats (inc/comm.hpp:67-73)
 
 class Stats(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("hv_products", C.c_int64), ("data_passes", C.c_int64),
-                ("hv_kernel_ms", C.c_double), ("hv_kernel_samples", C.c_int64)]
+                ("hv_kernel_ms", C.c_double), ("hv_kernel_samples", C.c_int64), ("hv_kernel_shards", C.c_int64)]
 
 
 class AdmmCfg(C.Structure):  # AdmmConfig + PenaltyPolicy + StoppingConfig (inc/admm.hpp:37-117)

@@ -626,16 +626,28 @@ struct AdmmRun {
     void iterate(nadmm_metrics_row* row) {
         int inner = 0, cg_sum = 0, fe_sum = 0, flags = 0;
         std::vector<char> pending(n_local, 0);
+        // node group: all local nodes' Newton iterations as one graph of whole-GPU group passes
+        bool grouped = cfg.inner_solver == 0 && cfg.inner_iters == 1 && group_eligible(shards);
+        if (grouped) {
+            for (Shard* s : shards) NADMM_CUDA(cudaMemcpyAsync(s->z, z, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+            grouped = group_solve_launch(shards, ncfg, rho.data());
+            if (grouped)
+                for (int i = 0; i < n_local; ++i) {
+                    solve_readback_async(*shards[i]);
+                    pending[i] = 3;
+                }
+        }
         // concurrent nodes: node i's solve on node_stream[i % k] (forked from / joined back to st)
-        bool conc = ctx->node_streams > 1 && cfg.inner_solver == 0 && n_local > 1;
+        bool conc = !grouped && ctx->node_streams > 1 && cfg.inner_solver == 0 && n_local > 1;
         for (int i = 0; conc && i < n_local; ++i) conc = dmma_supported(*shards[i]);
         const int ks = conc ? std::min(ctx->node_streams, n_local) : 1;
-        for (int i = 0; i < n_local; ++i) use_layout_split(*shards[i], ks);
+        if (!grouped)
+            for (int i = 0; i < n_local; ++i) use_layout_split(*shards[i], ks);
         if (conc) {
             NADMM_CUDA(cudaEventRecord(ctx->node_fork, st));
             for (int k2 = 0; k2 < ks; ++k2) NADMM_CUDA(cudaStreamWaitEvent(ctx->node_stream[k2], ctx->node_fork, 0));
         }
-        for (int i = 0; i < n_local; ++i) {  // (1) scatter z / solve (all workers enqueued back to back)
+        for (int i = 0; i < n_local && !grouped; ++i) {  // (1) scatter z / solve (workers enqueued back to back)
             Shard& s = *shards[i];
             if (conc) {
                 ctx->stream = ctx->node_stream[i % ks];
@@ -762,6 +774,7 @@ struct AdmmRun {
             fe_sum += r.fe_sum;
             flags |= r.flags;
         }
+        if (grouped) group_timers_finish(*ctx);
         for (int i = 0; i < n_local; ++i) rho[i] = hbuf[kStats * (nranks + 1) + i];
         float ms = 0.f;
         NADMM_CUDA(cudaEventElapsedTime(&ms, ev_start, ev_now));

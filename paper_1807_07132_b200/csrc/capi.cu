@@ -165,6 +165,7 @@ nadmm_newton_cfg cfg_or_default(const nadmm_newton_cfg* c) {
 namespace nadmm {
 
 Shard::~Shard() {
+    group_forget(*this);
     if (g_iter) cudaGraphExecDestroy(g_iter);
     gemm_free(*this);
     for (auto& t : hv_timers) {
@@ -258,6 +259,7 @@ nadmm_status nadmm_ctx_destroy(nadmm_ctx ctx) {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
+        group_drop(*ctx);
         if (ctx->dctr) cudaFree(ctx->dctr);
         for (int i = 0; i < Ctx::kMaxNodeStreams; ++i) {
             if (ctx->node_stream[i]) cudaStreamDestroy(ctx->node_stream[i]);
@@ -710,17 +712,35 @@ nadmm_status nadmm_workers_solve(const nadmm_worker* ws, int32_t n, const double
         NADMM_CUDA(cudaSetDevice(ctx.device));
         const cudaStream_t st = ctx.stream;
         // the workers of one scatter round run concurrently (WorkerPool threads, src/worker.cpp:222-240):
-        // worker i on node_stream[i % k] with a 1/k-GPU layout, or back to back on the context stream
-        bool conc = ctx.node_streams > 1 && n > 1 && inner_iters == 1;
+        // as one node group (whole-GPU group passes), else worker i on node_stream[i % k] with a
+        // 1/k-GPU layout, or back to back on the context stream
+        std::vector<char> done((size_t)n, 0);
+        bool grouped = inner_iters == 1 && group_eligible(sh);
+        if (grouped) {
+            for (int i = 0; i < n; ++i) {
+                Shard& s = *sh[(size_t)i];
+                NADMM_CUDA(cudaMemcpyAsync(s.z, z, sizeof(double) * s.d, cudaMemcpyHostToDevice, st));
+                NADMM_CUDA(cudaMemcpyAsync(s.y, y[i], sizeof(double) * s.d, cudaMemcpyHostToDevice, st));
+            }
+            grouped = group_solve_launch(sh, c, rho);
+            if (grouped)
+                for (int i = 0; i < n; ++i) {
+                    Shard& s = *sh[(size_t)i];
+                    if (x_out && x_out[i])
+                        NADMM_CUDA(cudaMemcpyAsync(x_out[i], s.x, sizeof(double) * s.d, cudaMemcpyDeviceToHost, st));
+                    solve_readback_async(s);
+                }
+        }
+        bool conc = !grouped && ctx.node_streams > 1 && n > 1 && inner_iters == 1;
         for (Shard* s : sh) conc = conc && dmma_supported(*s);
         const int ks = conc ? std::min(ctx.node_streams, (int)n) : 1;
-        for (Shard* s : sh) use_layout_split(*s, ks);
+        if (!grouped)
+            for (Shard* s : sh) use_layout_split(*s, ks);
         if (conc) {
             NADMM_CUDA(cudaEventRecord(ctx.node_fork, st));
             for (int k = 0; k < ks; ++k) NADMM_CUDA(cudaStreamWaitEvent(ctx.node_stream[k], ctx.node_fork, 0));
         }
-        std::vector<char> done((size_t)n, 0);
-        for (int i = 0; i < n; ++i) {
+        for (int i = 0; i < n && !grouped; ++i) {
             Shard& s = *sh[(size_t)i];
             ctx.stream = conc ? ctx.node_stream[i % ks] : st;
             try {
@@ -742,6 +762,7 @@ nadmm_status nadmm_workers_solve(const nadmm_worker* ws, int32_t n, const double
                 NADMM_CUDA(cudaStreamWaitEvent(st, ctx.node_join[k], 0));
             }
         stream_sync(st);  // one synchronisation for the whole round
+        if (grouped) group_timers_finish(ctx);
         for (int i = 0; i < n; ++i) {
             Shard& s = *sh[(size_t)i];
             SolveResult r = done[(size_t)i] ? solve_collect(s, c, false) : solve_result(s, c);

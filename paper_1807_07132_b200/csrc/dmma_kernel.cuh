@@ -180,6 +180,7 @@ struct DmmaArgs {
     double *cg_p, *cg_r, *cg_d, *cg_hd;
     unsigned long long* hv_ctr;    // Hv products applied (device counter)
     unsigned long long* done_ctr;  // clusters finished with this launch (reset by the last one)
+    unsigned long long* sub_ctr;   // node-group passes: barrier counter of this node's tail sub-grid
     int fs;  // features per CTA (= NC * 8 * MT)
     int S;   // padded shared row stride (doubles, even)
 };

@@ -32,7 +32,7 @@
 #include <cstdlib>
 #include <vector>
 
-#include "dmma_kernel.cuh"
+#include "dmma_group.cuh"
 
 namespace nadmm {
 
@@ -323,9 +323,9 @@ void dmma_setup(Shard& s, int split) {
 
 int dmma_clusters(const Shard& s) { return s.dmma_clusters; }
 
-void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
-    const Layout L = shard_layout(s);
-    if (!L.ok) raise(NADMM_ECONFIG, "dmma: no layout for this shape");
+namespace {
+
+DmmaArgs make_args(Shard& s, PassMode mode, const double* W, const int32_t* guard, int tail, int cg_it, bool write_lp) {
     DmmaArgs a{};
     a.X = s.X;
     a.ldx = s.ldx;
@@ -340,12 +340,12 @@ void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
     a.rowM = s.rowM;
     a.rowA = s.rowA;
     a.pred = s.pred;
-    a.lp_out = (mode == kModeHv && s.hv_write_lp) ? s.Lp : nullptr;
+    a.lp_out = (mode == kModeHv && write_lp) ? s.Lp : nullptr;
     a.part = s.part;
     a.blk = s.blk;
     a.guard = guard;
-    a.tail = (mode == kModeHv || mode == kModeCache) ? s.dmma_tail : kTailNone;
-    a.cg_it = s.cg_fuse_it;
+    a.tail = (mode == kModeHv || mode == kModeCache) ? tail : kTailNone;
+    a.cg_it = cg_it;
     if (a.tail != kTailNone) {
         a.st = s.st;
         a.prm = s.prm;
@@ -356,6 +356,7 @@ void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
         a.cg_hd = s.hd;
         a.hv_ctr = s.ctx->dctr;
         a.done_ctr = s.gbar + 4;
+        a.sub_ctr = s.gbar + 6;
         a.lp_from_cert = 1;
         a.x = s.x;
         a.z = s.z;
@@ -366,8 +367,17 @@ void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
         a.trace = s.trace;
         a.trace_cap = kTraceCap;
     }
-    a.fs = L.fs;
-    a.S = L.S;
+    a.fs = s.dmma_fs;
+    a.S = s.dmma_S;
+    return a;
+}
+
+}  // namespace
+
+void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
+    const Layout L = shard_layout(s);
+    if (!L.ok) raise(NADMM_ECONFIG, "dmma: no layout for this shape");
+    const DmmaArgs a = make_args(s, mode, W, guard, s.dmma_tail, s.cg_fuse_it, s.hv_write_lp);
     const int clusters = dmma_clusters(s);
     switch (mode) {
         case kModeCache: launch_mode<kModeCache>(s, L, a, clusters); break;
@@ -382,6 +392,92 @@ void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
     s.ctx->stats.data_passes++;
 }
 
+// ---------------- node-group passes (dmma_group.cuh) ----------------
+namespace {
+
+template <int MT, int PIPE, int MODE>
+void group_launch_one(Shard& s, const Layout& L, const DmmaGroup& g, int clusters, bool query, int* active) {
+    auto kern = dmma_group_kernel<MT, kPipes[PIPE].lag, kPipes[PIPE].stages, MODE>;
+    cudaLaunchAttribute attr[3];
+    cudaLaunchConfig_t cfg = make_cfg(s, L, clusters, attr, true);
+    if (query) {
+        NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
+        NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cfg.gridDim = dim3(L.cs, 1, 1);
+        cfg.numAttrs = 2;  // occupancy query without the cooperative attribute
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            nc = 0;
+        }
+        *active = nc;
+        return;
+    }
+    NADMM_CUDA(cudaLaunchKernelEx(&cfg, kern, g));
+}
+
+template <int PIPE, int MODE>
+void group_pipe(Shard& s, const Layout& L, const DmmaGroup& g, int clusters, bool query, int* active) {
+    switch (L.mt) {
+        case 4: group_launch_one<4, PIPE, MODE>(s, L, g, clusters, query, active); break;
+        case 6: group_launch_one<6, PIPE, MODE>(s, L, g, clusters, query, active); break;
+        case 7: group_launch_one<7, PIPE, MODE>(s, L, g, clusters, query, active); break;
+        case 8: group_launch_one<8, PIPE, MODE>(s, L, g, clusters, query, active); break;
+        default: raise(NADMM_ECONFIG, "dmma group: unsupported layout");
+    }
+}
+
+template <int MODE>
+void group_mode(Shard& s, const Layout& L, const DmmaGroup& g, int clusters, bool query, int* active) {
+    switch (L.pipe) {
+        case 0: group_pipe<0, MODE>(s, L, g, clusters, query, active); break;
+        case 1: group_pipe<1, MODE>(s, L, g, clusters, query, active); break;
+        case 2: group_pipe<2, MODE>(s, L, g, clusters, query, active); break;
+        default: raise(NADMM_ECONFIG, "dmma group: unsupported pipeline");
+    }
+}
+
+}  // namespace
+
+// Co-resident clusters of the group kernel with shard s's (whole-GPU) layout; 0: unavailable.
+int dmma_group_clusters(Shard& s) {
+    const Layout L = shard_layout(s);
+    if (!L.ok || s.layout_split != 1) return 0;
+    DmmaGroup g{};
+    int hv = 0, cache = 0;
+    group_mode<kModeHv>(s, L, g, 0, true, &hv);
+    group_mode<kModeCache>(s, L, g, 0, true, &cache);
+    return std::min({hv, cache, s.dmma_clusters});
+}
+
+void dmma_group_pass(const std::vector<Shard*>& shards, int clusters, PassMode mode, const double* const* W,
+                     const int32_t* const* guards, int tail, int cg_it, bool write_lp) {
+    const int n = (int)shards.size();
+    if (n < 1 || n > kMaxGroup) raise(NADMM_ECONFIG, "dmma group: 1..8 shards");
+    Shard& s0 = *shards[0];
+    const Layout L = shard_layout(s0);
+    DmmaGroup g{};
+    g.n = n;
+    for (int k = 0; k < n; ++k) {
+        Shard& s = *shards[k];
+        g.node[k] = make_args(s, mode, W[k], guards[k], tail, cg_it, write_lp);
+    }
+    const int grid = clusters * L.cs;
+    for (int k = 0; k <= n; ++k) g.sub_start[k] = (int)((int64_t)k * grid / n);  // tail sub-grids
+    g.grid_ctr = s0.gbar + 7;
+    switch (mode) {
+        case kModeHv: group_mode<kModeHv>(s0, L, g, clusters, false, nullptr); break;
+        case kModeCache: group_mode<kModeCache>(s0, L, g, clusters, false, nullptr); break;
+        default: raise(NADMM_ECONFIG, "dmma group: unsupported mode");
+    }
+    for (Shard* s : shards) {
+        s->ctx->stats.data_passes++;
+        s->rows_grid = 0;
+        s->last_chunks = 0;
+    }
+    s0.ctx->stats.kernel_launches++;
+}
+
 }  // namespace nadmm
 
 #ifdef NADMM_DMMA_TRACE
@@ -392,3 +488,43 @@ extern "C" __attribute__((visibility("default"))) int nadmm_debug_dmma_kstamps(l
     return (int)cudaMemcpyFromSymbol(out, nadmm::g_dmma_kst, sizeof(nadmm::g_dmma_kst));
 }
 #endif
+
+// Profiling hook (not part of the ABI header): time `reps` node-group Hv passes (no solver tail) over
+// the given shards (whole-GPU layouts) and, for comparison, `reps` single-shard passes of each shard.
+extern "C" __attribute__((visibility("default"))) int nadmm_debug_group_hv(nadmm_shard* shards, int n,
+                                                                          const double* const* v_dev, int reps,
+                                                                          float* ms_group, float* ms_single) {
+    try {
+        std::vector<nadmm::Shard*> sh;
+        for (int i = 0; i < n; ++i) sh.push_back(shards[i]);
+        for (auto* s : sh) nadmm::use_layout_split(*s, 1);
+        const int clusters = nadmm::dmma_group_clusters(*sh[0]);
+        if (clusters < 1) return -2;
+        std::vector<const int32_t*> gd(n, nullptr);
+        cudaStream_t st = sh[0]->ctx->stream;
+        for (auto* s : sh) cudaMemsetAsync(s->gbar + 6, 0, 2 * sizeof(unsigned long long), st);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        nadmm::dmma_group_pass(sh, clusters, nadmm::kModeHv, v_dev, gd.data(), nadmm::kTailNone, 0, false);
+        cudaEventRecord(e0, st);
+        for (int r = 0; r < reps; ++r)
+            nadmm::dmma_group_pass(sh, clusters, nadmm::kModeHv, v_dev, gd.data(), nadmm::kTailNone, 0, false);
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(ms_group, e0, e1);
+        *ms_group /= reps;
+        cudaEventRecord(e0, st);
+        for (int r = 0; r < reps; ++r)
+            for (int i = 0; i < n; ++i) nadmm::dmma_pass(*sh[i], nadmm::kModeHv, v_dev[i], nullptr);
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(ms_single, e0, e1);
+        *ms_single /= reps;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return (int)cudaGetLastError();
+    } catch (...) {
+        return -1;
+    }
+}

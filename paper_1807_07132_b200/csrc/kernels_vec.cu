@@ -726,6 +726,56 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
     NADMM_LAUNCH_CHECK();
 }
 
+// One Newton iteration of a NODE GROUP (the local ADMM nodes of an outer iteration, equal (p, K),
+// whole-GPU DMMA layouts) as one launch sequence: the per-node loop heads, then every data pass of
+// the iteration as ONE group launch over all nodes (dmma_group.cuh) with the node's CG step /
+// certificate + line search / Newton tail on its own sub-grid; the rare Lp pass + stand-alone line
+// search per node behind its device flag. `timers` (optional): events around the group Hv passes.
+void launch_group_iteration(const std::vector<Shard*>& g, int clusters, int cg_max, HvTimer* timers) {
+    const int n = (int)g.size();
+    cudaStream_t st = g[0]->ctx->stream;
+    for (Shard* sp : g) {
+        Shard& s = *sp;
+        const int grid = vec_grid(*s.ctx, s.d);
+        launch_pdl(k_begin_init, grid, 256, 0, st, s.d, s.st, s.prm, s.g, s.pd, s.r, s.dv);
+        LAUNCH_COUNT(s);
+    }
+    std::vector<const double*> W(n);
+    std::vector<const int32_t*> gd(n);
+    for (int it = 0; it < cg_max; ++it) {
+        for (int k = 0; k < n; ++k) {
+            W[k] = g[k]->dv;
+            gd[k] = &g[k]->st->cg_act[it];
+        }
+        if (timers) NADMM_CUDA(cudaEventRecordWithFlags(timers[it].start, st, cudaEventRecordExternal));
+        dmma_group_pass(g, clusters, kModeHv, W.data(), gd.data(), kTailCg, it, false);
+        if (timers) NADMM_CUDA(cudaEventRecordWithFlags(timers[it].stop, st, cudaEventRecordExternal));
+    }
+    for (int k = 0; k < n; ++k) {  // certificate Hv (src/newton.cpp:52) + fallback / slope + Armijo search
+        W[k] = g[k]->pd;
+        gd[k] = &g[k]->st->it_act;
+    }
+    if (timers) NADMM_CUDA(cudaEventRecordWithFlags(timers[cg_max].start, st, cudaEventRecordExternal));
+    dmma_group_pass(g, clusters, kModeHv, W.data(), gd.data(), kTailCert, 0, true);
+    if (timers) NADMM_CUDA(cudaEventRecordWithFlags(timers[cg_max].stop, st, cudaEventRecordExternal));
+    for (Shard* sp : g) {  // p changed after the certificate pass (CG failure / descent flip): Lp + search
+        Shard& s = *sp;
+        const int grid = vec_grid(*s.ctx, s.d);
+        op_lp(s, s.pd, &s.st->lp_need);
+        const int rblocks = std::max(1, (int)std::min<int64_t>((s.n + 31) / 32, kBlockPartials));
+        launch_pdl(k_ls_partials, rblocks + grid, 256, 0, st, s.n, s.K, s.L0, s.Lp, s.labels, rblocks, s.d, s.x, s.pd,
+                   s.z, s.y, s.prm, s.blk, &s.st->lp_need);
+        launch_pdl(k_ls_step, grid, 256, 0, st, s.d, s.st, s.prm, s.blk, rblocks, grid, s.x, s.pd, &s.st->lp_need);
+        s.ctx->stats.kernel_launches += 2;
+    }
+    for (int k = 0; k < n; ++k) {  // cache at the new iterate + gradient / value / trace (Newton tail)
+        W[k] = g[k]->x;
+        gd[k] = &g[k]->st->it_act;
+    }
+    dmma_group_pass(g, clusters, kModeCache, W.data(), gd.data(), kTailNewton, 0, false);
+    NADMM_LAUNCH_CHECK();
+}
+
 // Once per shard, outside stream capture: can the CG tail run as one cluster (d small enough for the
 // cluster's registers, 16-CTA clusters co-resident)? 0 selects the grid-barrier kernel.
 void tail_setup(Shard& s) {

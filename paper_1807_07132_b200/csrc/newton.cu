@@ -4,6 +4,7 @@
 // iteration (CG with device-side stop flags, certificate Hv, fallbacks, batched Armijo search,
 // step, fused cache+gradient pass at the new point), replayed per iteration. The host synchronises
 // once per Newton iteration (once per outer ADMM iteration with inner_iters = 1).
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -257,7 +258,7 @@ void solve_readback_async(Shard& s) {
 
 // After the stream has passed the readback copies: accumulate the Hv timers of the passes that ran.
 static void readback_finish(Shard& s, int cg_max) {
-    if (s.g_timing && !s.hv_timers.empty()) {
+    if (s.g_timing && !s.last_group && !s.hv_timers.empty()) {
         const DevState& h = *s.st_host;
         for (int it = 0; it <= cg_max && it < (int)s.hv_timers.size(); ++it) {
             const bool ran = it < cg_max ? h.cg_act[it] != 0 : h.cert_act != 0;
@@ -266,6 +267,7 @@ static void readback_finish(Shard& s, int cg_max) {
             if (cudaEventElapsedTime(&ms, s.hv_timers[it].start, s.hv_timers[it].stop) == cudaSuccess) {
                 s.ctx->stats.hv_kernel_ms += ms;
                 s.ctx->stats.hv_kernel_samples++;
+                s.ctx->stats.hv_kernel_shards++;
             }
         }
     }
@@ -280,6 +282,7 @@ static void readback(Shard& s, int cg_max) {
 
 bool solve_launch(Shard& s, const nadmm_newton_cfg& cfg, double lambda, bool aug, double rho, int newton_max) {
     validate_newton_cfg(cfg);
+    s.last_group = false;
     if (aug && rho <= 0.0) raise(NADMM_ECONFIG, "augmented objective requires rho > 0");
     set_params(s, cfg, lambda, aug, rho);
     capture_iteration_graph(s, cfg.cg_max_iters, cfg.ls_max_iters);
@@ -334,6 +337,161 @@ SolveResult device_newton_solve(Shard& s, const nadmm_newton_cfg& cfg, double la
                                 int newton_max) {
     const bool done = solve_launch(s, cfg, lambda, aug, rho, newton_max);
     return solve_collect(s, cfg, !done);
+}
+
+}  // namespace nadmm
+
+namespace nadmm {
+
+// ---------------------------------------------------------------------------------------------
+// Node groups: the Newton iteration of several equal-shape DMMA shards (the local ADMM nodes of an
+// outer iteration) captured as ONE graph whose data passes are group launches over the whole GPU
+// (dmma_group.cuh) -- instead of one graph per node on a 1/k-GPU layout (node streams).
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+constexpr int kGroupMax = 8;
+
+struct GroupGraph {
+    std::vector<Shard*> shards;
+    int clusters = 0, cg_max = -1, ls_max = -1;
+    int64_t layout_sig = -1;
+    bool timing = false;
+    cudaGraphExec_t exec = nullptr;
+    int64_t nodes = 0;
+    std::vector<HvTimer> timers;
+    ~GroupGraph() {
+        if (exec) cudaGraphExecDestroy(exec);
+        for (auto& t : timers) {
+            if (t.start) cudaEventDestroy(t.start);
+            if (t.stop) cudaEventDestroy(t.stop);
+        }
+    }
+};
+
+}  // namespace
+
+void group_drop(Ctx& c) {
+    delete static_cast<GroupGraph*>(c.group);
+    c.group = nullptr;
+}
+
+void group_forget(Shard& s) {
+    if (!s.ctx || !s.ctx->group) return;
+    const auto* g = static_cast<GroupGraph*>(s.ctx->group);
+    for (Shard* x : g->shards)
+        if (x == &s) {
+            group_drop(*s.ctx);
+            return;
+        }
+}
+
+bool group_eligible(const std::vector<Shard*>& sh) {
+    // opt-in (NADMM_GROUP=1) until the group pass beats the node streams on the bench shape
+    static const bool off = [] {
+        const char* e = getenv("NADMM_GROUP");
+        return !(e && e[0] == '1');
+    }();
+    if (off || sh.size() < 2 || sh.size() > (size_t)kGroupMax) return false;
+    const Shard& a = *sh[0];
+    for (Shard* s : sh)
+        if (!dmma_supported(*s) || s->p != a.p || s->K != a.K || s->ldx != a.ldx || s->ctx != a.ctx) return false;
+    return true;
+}
+
+bool group_solve_launch(const std::vector<Shard*>& sh, const nadmm_newton_cfg& cfg, const double* rho) {
+    if (!group_eligible(sh)) return false;
+    Ctx& c = *sh[0]->ctx;
+    const cudaStream_t st = c.stream;
+    for (Shard* s : sh) use_layout_split(*s, 1);
+    auto* cached = static_cast<GroupGraph*>(c.group);
+    const Shard& s0 = *sh[0];
+    const int64_t sig = ((((int64_t)s0.dmma_mt * 64 + s0.dmma_nw) * 64 + s0.dmma_cs) * 64 + s0.dmma_pipe) * 4096 +
+                        s0.dmma_clusters;  // the whole-GPU layout the group kernel inherits
+    const int clusters = (cached && cached->shards == sh && cached->layout_sig == sig) ? cached->clusters
+                                                                                        : dmma_group_clusters(*sh[0]);
+    if (clusters < 1) return false;
+    for (Shard* s : sh)  // every cluster range must hold tiles of each node it spans (dmma_group.cuh)
+        if ((s->n + 7) / 8 < clusters || s->dmma_clusters < clusters) return false;
+    auto* g = static_cast<GroupGraph*>(c.group);
+    if (!g || g->shards != sh || g->cg_max != cfg.cg_max_iters || g->ls_max != cfg.ls_max_iters ||
+        g->timing != c.timing || g->clusters != clusters || g->layout_sig != sig) {
+        group_drop(c);
+        g = new GroupGraph();
+        g->shards = sh;
+        g->clusters = clusters;
+        g->layout_sig = sig;
+        g->cg_max = cfg.cg_max_iters;
+        g->ls_max = cfg.ls_max_iters;
+        g->timing = c.timing;
+        if (g->timing) {
+            g->timers.resize((size_t)cfg.cg_max_iters + 1);
+            for (auto& t : g->timers) {
+                NADMM_CUDA(cudaEventCreate(&t.start));
+                NADMM_CUDA(cudaEventCreate(&t.stop));
+            }
+        }
+        // the group's barrier counters (tail sub-grids, whole grid) restart for the new configuration
+        for (Shard* s : sh) NADMM_CUDA(cudaMemsetAsync(s->gbar + 6, 0, 2 * sizeof(unsigned long long), st));
+        const nadmm_stats saved = c.stats;
+        cudaGraph_t graph = nullptr;
+        NADMM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+            launch_group_iteration(sh, clusters, cfg.cg_max_iters, g->timing ? g->timers.data() : nullptr);
+        } catch (...) {
+            cudaStreamEndCapture(st, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            c.stats = saved;
+            delete g;
+            throw;
+        }
+        NADMM_CUDA(cudaStreamEndCapture(st, &graph));
+        g->nodes = c.stats.kernel_launches - saved.kernel_launches;
+        c.stats = saved;
+        const cudaError_t ie = cudaGraphInstantiate(&g->exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ie != cudaSuccess) {
+            delete g;
+            NADMM_CUDA(ie);
+        }
+        c.group = g;
+        if (getenv("NADMM_DMMA_VERBOSE"))
+            fprintf(stderr, "[nadmm] node group: %zu shards, %d clusters x %d CTAs, graph of %lld kernels\n",
+                    sh.size(), clusters, sh[0]->dmma_cs, (long long)g->nodes);
+    }
+    for (size_t i = 0; i < sh.size(); ++i) {  // each node's solve prologue (solve_launch's)
+        Shard& s = *sh[i];
+        if (rho[i] <= 0.0) raise(NADMM_ECONFIG, "augmented objective requires rho > 0");
+        set_params(s, cfg, 0.0, true, rho[i]);
+        ensure_cache_at_x(s, 0.0);
+        int nvec = 0;
+        launch_grad_aug(s, nullptr, &nvec);
+        launch_value_finish(s, nvec, 1, nullptr);
+        s.cache_at = Shard::kAtX;
+        s.cache_lambda = 0.0;
+        s.last_group = true;
+    }
+    NADMM_CUDA(cudaGraphLaunch(g->exec, st));
+    c.stats.kernel_launches += g->nodes;
+    return true;
+}
+
+// After the synchronisation that brought the group's DevStates back: the timed group Hv passes
+// (CG iterations and certificate) with the number of nodes that ran in each.
+void group_timers_finish(Ctx& c) {
+    auto* g = static_cast<GroupGraph*>(c.group);
+    if (!g || !g->timing || g->timers.empty()) return;
+    for (int it = 0; it <= g->cg_max; ++it) {
+        int64_t cnt = 0;
+        for (Shard* s : g->shards) cnt += it < g->cg_max ? (s->st_host->cg_act[it] != 0) : (s->st_host->cert_act != 0);
+        if (cnt == 0) continue;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, g->timers[it].start, g->timers[it].stop) == cudaSuccess) {
+            c.stats.hv_kernel_ms += ms;
+            c.stats.hv_kernel_samples++;
+            c.stats.hv_kernel_shards += cnt;
+        }
+    }
 }
 
 }  // namespace nadmm

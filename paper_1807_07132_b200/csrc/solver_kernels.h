@@ -12,6 +12,8 @@ void launch_value_finish(Shard& s, int nvec, int prologue, const int32_t* guard)
 // One full Newton iteration (CG, certificate, fallbacks, batched Armijo, step, new cache/grad).
 void launch_newton_iteration(Shard& s, int cg_max, int ls_max);
 void launch_set_int(Shard& s, int32_t* dst, int v);
+// One Newton iteration of a node group (dmma_group.cuh); timers: cg_max + 1 event pairs or null.
+void launch_group_iteration(const std::vector<Shard*>& g, int clusters, int cg_max, HvTimer* timers);
 // Picks the CG-tail variant for the shard's d (cluster kernel when it fits); outside stream capture.
 void tail_setup(Shard& s);
 

@@ -78,6 +78,7 @@ struct Ctx {
     static constexpr int kMaxNodeStreams = 8;
     cudaStream_t node_stream[kMaxNodeStreams] = {};
     cudaEvent_t node_fork = nullptr, node_join[kMaxNodeStreams] = {};
+    void* group = nullptr;  // cached node-group iteration graph (GroupGraph, newton.cu)
 };
 
 struct HvTimer {
@@ -180,6 +181,7 @@ struct Shard {
     std::vector<HvTimer> hv_timers;
     int hv_timer_site = -1;
     bool capture_timing = false;
+    bool last_group = false;  // the last solve ran in a node-group graph (its timers live there)
     // optional per-node timeline of the captured iteration graph (NADMM_GRAPH_TIMELINE=1, profiling)
     bool tl_capture = false;
     std::vector<const char*> tl_names;
@@ -267,10 +269,21 @@ void dmma_setup(Shard& s, int split = 1);
 void use_layout_split(Shard& s, int split);
 void invalidate_graphs(Shard& s);
 void dmma_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
+// Node-group passes (dmma_group.cuh): one full-GPU launch over several shards of equal (p, K) with
+// whole-GPU layouts; per-node V / guards; tails on per-node sub-grids.
+int dmma_group_clusters(Shard& s);
+void dmma_group_pass(const std::vector<Shard*>& shards, int clusters, PassMode mode, const double* const* W,
+                     const int32_t* const* guards, int tail, int cg_it, bool write_lp);
 
 }  // namespace nadmm
 
 namespace nadmm {
+// Node-group solves (newton.cu): the local ADMM nodes' Newton iterations as one graph of group passes.
+bool group_eligible(const std::vector<Shard*>& sh);
+bool group_solve_launch(const std::vector<Shard*>& sh, const nadmm_newton_cfg& cfg, const double* rho);
+void group_timers_finish(Ctx& c);
+void group_forget(Shard& s);
+void group_drop(Ctx& c);
 // Grid-barrier watchdog control (common.cuh): push NADMM_BARRIER_TIMEOUT_MS to every translation
 // unit's control block on the current device; raise NADMM_ECUDA if any barrier timed out.
 void barrier_configure();

@@ -10,5 +10,5 @@ mkdir -p /tmp/var_$name
 "$NVCC" -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
   --expt-relaxed-constexpr -Xptxas -v "$@" -c csrc/kernels_dmma.cu -o /tmp/var_$name/kernels_dmma.o > /tmp/var_$name/ptxas.log 2>&1 || { tail -20 /tmp/var_$name/ptxas.log; exit 1; }
 for o in build/*.o; do [ "$(basename $o)" = kernels_dmma.o ] || cp $o /tmp/var_$name/; done
-"$NVCC" -shared -gencode arch=compute_100a,code=sm_100a -o ../tools/prof/var_$name.so /tmp/var_$name/*.o -lnccl -lcublas
+"$NVCC" -shared -gencode arch=compute_100a,code=sm_100a -o ../tools/prof/var_$name.so /tmp/var_$name/*.o -lnccl
 echo "built tools/prof/var_$name.so"
