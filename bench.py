@@ -51,6 +51,16 @@ def env_int(k, d):
     return int(os.environ.get(k, d))
 
 
+# The one JSON line goes to the real stdout; everything native code prints there meanwhile (NCCL's
+# "NCCL version" banner, library diagnostics) is redirected to stderr.
+_JSON_FD = os.dup(1)
+os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    os.write(_JSON_FD, (json.dumps(line) + "\n").encode())
+
+
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
@@ -263,7 +273,7 @@ def run_reference_arm(args):
 
     r = oracle.ref()
     if r is None:
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libnadmm_ref.so not built"}), flush=True)
+        emit({"impl": "reference", "unavailable": "oracle/_ref/libnadmm_ref.so not built"})
         return
     cores = os.cpu_count() or 1
     shards, _ = ref_shards(oracle, r)
@@ -307,7 +317,7 @@ def run_reference_arm(args):
             "as_designed": as_designed,
             "e2e": {"value": v, "unit": "Hv/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     line.update(ttt)
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------------------------------------
@@ -495,7 +505,7 @@ def run_config(args):
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": None, "gpu_launches": int(st["kernel_launches"]),
                 "clocks": clk.summary(), "hv_per_step": hv_total / args.steps}
         line.update(ttt)
-        print(json.dumps(line), flush=True)
+        emit(line)
     if comm:
         comm.close()
     if dist:
@@ -823,7 +833,7 @@ def main():
                 "clocks": clk.summary(), "outer_iters_per_s": args.steps / (ms * 1e-3),
                 "hv_per_step": hv_total / args.steps}
         line.update(ttt)
-        print(json.dumps(line), flush=True)
+        emit(line)
     if comm:
         comm.close()
     if dist:

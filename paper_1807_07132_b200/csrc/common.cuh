@@ -162,16 +162,6 @@ __device__ __forceinline__ void grid_barrier_n(unsigned long long* ctr, unsigned
 
 __device__ __forceinline__ void grid_barrier(unsigned long long* ctr) { grid_barrier_n(ctr, gridDim.x); }
 
-// Programmatic dependent launch: kernels of the Newton-iteration graph are launched with
-// programmatic stream serialisation, so a kernel's launch and prologue overlap its predecessor's
-// tail; every such kernel calls pdl_wait() before touching memory its predecessor writes (a no-op
-// when the launch was not programmatic).
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
-
-#ifndef NADMM_PDL
-#define NADMM_PDL 0  // measured: no gain on the Newton graph (kept switchable)
-#endif
-
 // Persistent grids that synchronise through grid_barrier are launched cooperatively (the runtime
 // then guarantees co-residency, or fails the launch); NADMM_COOP=0 falls back to plain launches
 // (co-residency from the occupancy-sized grid, guarded by the barrier watchdog).
@@ -191,13 +181,11 @@ void launch_ex(bool coop, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = NADMM_PDL;
-    attr[1].id = cudaLaunchAttributeCooperative;
-    attr[1].val.cooperative = 1;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = (coop && coop_enabled()) ? 2 : 1;
+    cfg.numAttrs = (coop && coop_enabled()) ? 1 : 0;
     NADMM_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
 }
 

@@ -66,11 +66,6 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
         : "memory");
 }
 
-// L2 prefetch of a global range (no shared memory, no completion): HBM -> L2 runs ahead of the ring.
-__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
-}
-
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
@@ -107,14 +102,6 @@ __device__ __forceinline__ uint32_t mapa(uint32_t local_smem, uint32_t rank) {
     uint32_t r;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(local_smem), "r"(rank));
     return r;
-}
-
-// 16-byte DSMEM store into CTA `rank`'s shared memory that completes tx bytes on its mbarrier.
-__device__ __forceinline__ void st_async_v2(uint32_t remote_addr, double x, double y, uint32_t remote_bar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(
-                     remote_addr),
-                 "d"(x), "d"(y), "r"(remote_bar)
-                 : "memory");
 }
 
 // Bulk copy of a local shared-memory buffer into a peer CTA's shared memory (cluster addresses for
@@ -219,10 +206,6 @@ __device__ __forceinline__ long long gtimer() {
     } while (0)
 #endif
 
-#ifndef NADMM_DMMA_PREFETCH
-#define NADMM_DMMA_PREFETCH 0
-#endif
-constexpr int kDmmaPrefetch = NADMM_DMMA_PREFETCH;  // L2 prefetch distance in tiles (0: off)
 #ifndef NADMM_DMMA_CHAINS
 #define NADMM_DMMA_CHAINS 4
 #endif
@@ -231,10 +214,6 @@ constexpr int kDmmaChains = NADMM_DMMA_CHAINS;  // phase-A accumulator chains pe
 #ifndef NADMM_DMMA_RECV_BUFS
 #define NADMM_DMMA_RECV_BUFS 4
 #endif
-#ifndef NADMM_DMMA_BULK_PUSH
-#define NADMM_DMMA_BULK_PUSH 1
-#endif
-constexpr bool kDmmaBulkPush = NADMM_DMMA_BULK_PUSH;  // exchange by bulk smem->peer copies (else st.async)
 constexpr int kDmmaRecvBufs = NADMM_DMMA_RECV_BUFS;
 // Up to 8 compute warps per CTA (2 per SM sub-partition). Measured: 16 narrow (MT = 4) warps per
 // CTA spill under the 102-register cap and run 30-50 % slower on the CIFAR shapes.
@@ -438,7 +417,6 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_pass_kernel(Dmma
     fence_proxy_async();
     // everything above overlaps the predecessor kernel (programmatic launch); from here on we read
     // what it wrote (the guard flag, V, P)
-    pdl_wait();
     if (a.guard && !*a.guard) {  // uniform across the grid: no remote traffic has started
         if (MODE == kModeHv && a.tail == kTailCg && blockIdx.x == 0 && threadIdx.x == 0) {
             DevState* st = a.st;  // the CG iteration is switched off: its tail's bookkeeping
@@ -463,14 +441,6 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_pass_kernel(Dmma
             for (int i = 0; i < T; ++i) {
                 const int stage = i % STAGES;
                 if (i == 1) DMMA_KST(2);
-                // tile i + kDmmaPrefetch: HBM -> L2 now, so the ring refill after the empty wait hits L2
-                // (the ring alone keeps too few bytes in flight: most stages wait for phase B)
-                if (kDmmaPrefetch > 0 && i + kDmmaPrefetch < T && row_bytes) {
-                    const int64_t q0 = tile_of(i + kDmmaPrefetch) * BM;
-                    const int qrows = (n - q0) < BM ? (int)(n - q0) : BM;
-                    for (int r = 0; r < qrows; ++r) prefetch_l2(a.X + (q0 + r) * a.ldx + f_cta, row_bytes);
-                    if (NEED_P && crank == 0) prefetch_l2(a.Pin + q0 * K, BM * K * 8);
-                }
                 if (i >= STAGES) mbar_wait(&empty[stage], (uint32_t)(((i / STAGES) - 1) & 1));
                 const int64_t r0 = tile_of(i) * BM;
                 const int rows = (n - r0) < BM ? (int)(n - r0) : BM;
@@ -533,22 +503,16 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_pass_kernel(Dmma
             for (int j = 0; j < NPAIR; ++j) {
                 const int i2 = lane + 32 * j;
                 if (i2 >= PART / 2) continue;
-                if (kDmmaBulkPush)
-                    *reinterpret_cast<double2*>(sendb + (size_t)br * PART + 2 * i2) = make_double2(s0[j], s1[j]);
-                else
-                    for (uint32_t q = 0; q < csize; ++q)
-                        st_async_v2(mapa(dst_local + 16u * i2, q), s0[j], s1[j], mapa(bar_local, q));
+                *reinterpret_cast<double2*>(sendb + (size_t)br * PART + 2 * i2) = make_double2(s0[j], s1[j]);
             }
             DMMA_TRACE(i, 14);
-            if (kDmmaBulkPush) {
-                // the summed partial goes to every peer as one bulk copy each (lane q -> CTA q); the
-                // send buffer br is rewritten only after every peer returned its credit for br
-                fence_proxy_async();
-                __syncwarp();
-                if (lane < (int)csize)
-                    bulk_s2cluster(mapa(dst_local, (uint32_t)lane), smem_u32(sendb + (size_t)br * PART), PART * 8u,
-                                   mapa(bar_local, (uint32_t)lane));
-            }
+            // the summed partial goes to every peer as one bulk copy each (lane q -> CTA q); the send
+            // buffer br is rewritten only after every peer returned its credit for br
+            fence_proxy_async();
+            __syncwarp();
+            if (lane < (int)csize)
+                bulk_s2cluster(mapa(dst_local, (uint32_t)lane), smem_u32(sendb + (size_t)br * PART), PART * 8u,
+                               mapa(bar_local, (uint32_t)lane));
             __syncwarp();
             DMMA_TRACE(i, 3);
             if (lane == 0) mbar_arrive(&red_empty[b]);

@@ -49,11 +49,7 @@ constexpr int kBM = 8;
 struct Pipe {
     int lag, stages;
 };
-#ifdef NADMM_DMMA_PIPE6  // profiling: six-stage rings (needs fewer exchange buffers to fit)
-constexpr Pipe kPipes[] = {{4, 6}, {3, 5}, {2, 5}, {2, 6}, {3, 6}};
-#else
 constexpr Pipe kPipes[] = {{4, 6}, {3, 5}, {2, 5}};
-#endif
 constexpr int kNumPipes = sizeof(kPipes) / sizeof(kPipes[0]);
 
 struct Layout {
@@ -97,7 +93,7 @@ std::vector<Layout> candidate_layouts(int64_t p, int K) {
 }
 
 cudaLaunchConfig_t make_cfg(Shard& s, const Layout& L, int clusters, cudaLaunchAttribute* attr,
-                            bool coop = false) {  // attr[3]
+                            bool coop = false) {  // attr[2]
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(clusters * L.cs, 1, 1);
     cfg.blockDim = dim3(32 * (L.nw + kDmmaAux), 1, 1);
@@ -107,12 +103,10 @@ cudaLaunchConfig_t make_cfg(Shard& s, const Layout& L, int clusters, cudaLaunchA
     attr[0].val.clusterDim.x = L.cs;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = NADMM_PDL;
-    attr[2].id = cudaLaunchAttributeCooperative;  // the solver tails synchronise the grid (grid_barrier)
-    attr[2].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;  // the solver tails synchronise the grid (grid_barrier)
+    attr[1].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = (coop && coop_enabled()) ? 3 : 2;
+    cfg.numAttrs = (coop && coop_enabled()) ? 2 : 1;
     return cfg;
 }
 
@@ -123,7 +117,7 @@ int setup_one(Shard& s, const Layout& L) {
     auto kern = dmma_pass_kernel<MT, 1, 1, kBM, kPipes[PIPE].lag, kPipes[PIPE].stages, MODE>;
     NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit));
     NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cudaLaunchAttribute attr[3];
+    cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = make_cfg(s, L, 1, attr);
     int nc = 0;
     if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess) {
@@ -159,10 +153,6 @@ int setup_layout(Shard& s, const Layout& L) {
         case 0: return setup_pipe<0>(s, L);
         case 1: return setup_pipe<1>(s, L);
         case 2: return setup_pipe<2>(s, L);
-#ifdef NADMM_DMMA_PIPE6
-        case 3: return setup_pipe<3>(s, L);
-        case 4: return setup_pipe<4>(s, L);
-#endif
         default: return 0;
     }
 }
@@ -170,7 +160,7 @@ int setup_layout(Shard& s, const Layout& L) {
 template <int MT, int PIPE, int MODE>
 void launch_one(Shard& s, const Layout& L, const DmmaArgs& a, int clusters) {
     auto kern = dmma_pass_kernel<MT, 1, 1, kBM, kPipes[PIPE].lag, kPipes[PIPE].stages, MODE>;
-    cudaLaunchAttribute attr[3];
+    cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = make_cfg(s, L, clusters, attr, a.tail != kTailNone);
     NADMM_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
 }
@@ -192,10 +182,6 @@ void launch_mode(Shard& s, const Layout& L, const DmmaArgs& a, int clusters) {
         case 0: launch_pipe<0, MODE>(s, L, a, clusters); break;
         case 1: launch_pipe<1, MODE>(s, L, a, clusters); break;
         case 2: launch_pipe<2, MODE>(s, L, a, clusters); break;
-#ifdef NADMM_DMMA_PIPE6
-        case 3: launch_pipe<3, MODE>(s, L, a, clusters); break;
-        case 4: launch_pipe<4, MODE>(s, L, a, clusters); break;
-#endif
         default: raise(NADMM_ECONFIG, "dmma: unsupported pipeline");
     }
 }
@@ -398,13 +384,13 @@ namespace {
 template <int MT, int PIPE, int MODE>
 void group_launch_one(Shard& s, const Layout& L, const DmmaGroup& g, int clusters, bool query, int* active) {
     auto kern = dmma_group_kernel<MT, kPipes[PIPE].lag, kPipes[PIPE].stages, MODE>;
-    cudaLaunchAttribute attr[3];
+    cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = make_cfg(s, L, clusters, attr, true);
     if (query) {
         NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
         NADMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         cfg.gridDim = dim3(L.cs, 1, 1);
-        cfg.numAttrs = 2;  // occupancy query without the cooperative attribute
+        cfg.numAttrs = 1;  // occupancy query without the cooperative attribute
         int nc = 0;
         if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess) {
             cudaGetLastError();

@@ -96,7 +96,6 @@ __global__ void k_value_finish(DevState* st, const DevParams* prm, const double*
 __global__ void __launch_bounds__(256) k_begin_init(int64_t d, DevState* st, const DevParams* prm,
                                                     const double* __restrict__ g, double* __restrict__ p,
                                                     double* __restrict__ r, double* __restrict__ dv) {
-    pdl_wait();
     const double gn = st->g_norm;
     const bool run = st->active && !(gn < prm->grad_tol) && gn > 0.0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -152,7 +151,6 @@ __global__ void __launch_bounds__(256, 4) k_cg_tail(int it, int64_t d, DevState*
                                                     double* __restrict__ r, double* __restrict__ dv,
                                                     double* __restrict__ hd, double* blk, int ncurv,
                                                     unsigned long long* hv_ctr, unsigned long long* bar) {
-    pdl_wait();
     __shared__ double red[32];
     __shared__ double sc;
     const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
@@ -322,7 +320,6 @@ __global__ void __launch_bounds__(kClThreads, 1) k_cg_tail_cl(int it, int64_t d,
                                                               double* __restrict__ r, double* __restrict__ dv,
                                                               double* __restrict__ hd, const double* blk, int ncurv,
                                                               unsigned long long* hv_ctr) {
-    pdl_wait();
     namespace cgs = cooperative_groups;
     cgs::cluster_group cl = cgs::this_cluster();
     __shared__ double red[32];
@@ -440,7 +437,6 @@ __global__ void __launch_bounds__(256, 4) k_cert_tail(int64_t d, DevState* st, c
                                                       const double* __restrict__ g, double* __restrict__ p,
                                                       double* __restrict__ hd, double* blk, int ncert,
                                                       unsigned long long* hv_ctr, unsigned long long* bar) {
-    pdl_wait();
     __shared__ double red[32];
     __shared__ double sc;
     cert_tail_body(d, st, prm, part, chunks, lp_from_cert, g, p, hd, blk, ncert, hv_ctr, bar, red, &sc, whole_grid());
@@ -466,7 +462,6 @@ __global__ void __launch_bounds__(256) k_ls_partials(int64_t n, int K, const dou
                                                      const double* __restrict__ p, const double* __restrict__ z,
                                                      const double* __restrict__ y, const DevParams* prm, double* blk,
                                                      const int32_t* guard) {
-    pdl_wait();
     if (guard && !*guard) return;
     __shared__ double red[32];
     const int nc = prm->ls_max_iters + 1;
@@ -547,7 +542,6 @@ __global__ void __launch_bounds__(256) k_ls_partials(int64_t n, int K, const dou
 __global__ void __launch_bounds__(256) k_ls_step(int64_t d, DevState* st, const DevParams* prm, const double* blk,
                                                  int nrows, int nvec, double* __restrict__ x,
                                                  const double* __restrict__ p, const int32_t* guard) {
-    pdl_wait();
     if (guard && !*guard) return;
     __shared__ double fj[kMaxLs + 1];
     __shared__ double a_s;
@@ -598,7 +592,6 @@ __global__ void __launch_bounds__(256, 4) k_newton_tail(int64_t d, DevState* st,
                                                         double* __restrict__ g, double* __restrict__ t, double* blk,
                                                         int nloss, double* scal, DevTrace* trace, int trace_cap,
                                                         unsigned long long* bar, const int32_t* guard) {
-    pdl_wait();
     if (guard && !*guard) return;
     __shared__ double red[32];
     newton_tail_body(d, st, prm, part, chunks, x, z, y, gbase, g, t, blk, nloss, scal, trace, trace_cap, bar, red,
@@ -656,7 +649,7 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
             // nothing more to launch
         } else if (s.tail_cluster > 0) {
             cudaLaunchConfig_t cfg = {};
-            cudaLaunchAttribute attr[2];
+            cudaLaunchAttribute attr[1];
             cfg.gridDim = dim3(s.tail_cluster, 1, 1);
             cfg.blockDim = dim3(kClThreads, 1, 1);
             cfg.stream = st;
@@ -664,10 +657,8 @@ void launch_newton_iteration(Shard& s, int cg_max, int ls_max) {
             attr[0].val.clusterDim.x = s.tail_cluster;
             attr[0].val.clusterDim.y = 1;
             attr[0].val.clusterDim.z = 1;
-            attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            attr[1].val.programmaticStreamSerializationAllowed = NADMM_PDL;
             cfg.attrs = attr;
-            cfg.numAttrs = 2;
+            cfg.numAttrs = 1;
             NADMM_CUDA(cudaLaunchKernelEx(&cfg, k_cg_tail_cl, it, s.d, s.st, (const DevParams*)s.prm,
                                           (const double*)s.part, chunks, (const double*)s.g, s.pd, s.r, s.dv, s.hd,
                                           (const double*)s.blk, ncurv, chunks > 0 ? s.ctx->dctr : nullptr));
