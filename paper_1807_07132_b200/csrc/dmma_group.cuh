@@ -59,6 +59,10 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_group_kernel(con
         double *part, *lp_out, *L0, *P, *rowM, *rowA;
     };
     __shared__ NodeHot s_node[kMaxGroup];
+    // per ring stage: the node and first local row of the tile the producer loaded there (consumers
+    // read it after their full / u_full wait instead of searching the node table)
+    __shared__ int s_tile_k[STAGES];
+    __shared__ int64_t s_tile_r0[STAGES];
     const DmmaArgs& a0 = G.node[0];
     const int nc = (int)(blockDim.x >> 5) - kDmmaAux;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -160,6 +164,8 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_group_kernel(con
                 uint32_t bytes = row_bytes * (uint32_t)rows;
                 if (NEED_P) bytes += BM * K * 8;
                 if (NEED_Y) bytes += BM * 4;
+                s_tile_k[stage] = k;
+                s_tile_r0[stage] = r0;
                 fence_proxy_async();
                 mbar_expect_tx(&full[stage], bytes);
                 if (row_bytes)
@@ -221,20 +227,19 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_group_kernel(con
         double loss_acc = 0.0;
         int loss_node = -1;
         constexpr int NE = (BM * K + 31) / 32;
-        int k = -1;
         for (int i = ew; i < T; i += kDmmaEpiWarps) {
             const int stage = i % STAGES, br = i % kDmmaRecvBufs;
-            int64_t r0;
-            locate(i, k, r0);
+            if (lane == 0) mbar_expect_tx(&rbar[br], (uint32_t)csize * PART * 8u);
+            mbar_wait(&rbar[br], (uint32_t)((i / kDmmaRecvBufs) & 1));
+            mbar_wait(&full[stage], (uint32_t)((i / STAGES) & 1));
+            const int k = s_tile_k[stage];
+            const int64_t r0 = s_tile_r0[stage];
             const NodeHot& A = s_node[k];
             if (MODE == kModeCache && k != loss_node) {  // the node's loss share (rank-0 CTA rows)
                 if (loss_node >= 0) s_loss[loss_node][ew * 32 + lane] += loss_acc;
                 loss_acc = 0.0;
                 loss_node = k;
             }
-            if (lane == 0) mbar_expect_tx(&rbar[br], (uint32_t)csize * PART * 8u);
-            mbar_wait(&rbar[br], (uint32_t)((i / kDmmaRecvBufs) & 1));
-            mbar_wait(&full[stage], (uint32_t)((i / STAGES) & 1));
             const double* rv = recv + (size_t)br * csize * PART;
             {
                 double v[NE][8];
@@ -395,17 +400,14 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_group_kernel(con
         zero_b();
         int node_a = -1, node_b = -1;
 
-        int kA = -1, kB = -1;  // the phase-A / phase-B tile streams' current nodes (search hints)
         auto phase_a = [&](int i) {
             const int stage = i % STAGES, b = i % kDmmaRedBufs;
-            int64_t r0;
-            locate(i, kA, r0);
-            const int k = kA;
+            mbar_wait(&full[stage], (uint32_t)((i / STAGES) & 1));
+            const int k = s_tile_k[stage];
             if (k != node_a) {
                 load_v(s_node[k].V);
                 node_a = k;
             }
-            mbar_wait(&full[stage], (uint32_t)((i / STAGES) & 1));
             const double* xt = xs + (size_t)stage * BM * S;
             constexpr int NCH = (KSTEP_A % kDmmaChains == 0) ? kDmmaChains : ((KSTEP_A % 2 == 0) ? 2 : 1);
             double acca[NCH][G8][KT][2];
@@ -460,9 +462,9 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_group_kernel(con
         for (int i = 0; i < T; ++i) {
             const int stage = i % STAGES;
             if (i + LAG < T) phase_a(i + LAG);
-            int64_t r0;
-            locate(i, kB, r0);
-            const int k = kB;
+            mbar_wait(&u_full[stage], (uint32_t)((i / STAGES) & 1));
+            const int k = s_tile_k[stage];
+            const int64_t r0 = s_tile_r0[stage];
             if (k != node_b) {
                 if (node_b >= 0) {
                     flush_b(node_b);
@@ -470,7 +472,6 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_group_kernel(con
                 }
                 node_b = k;
             }
-            mbar_wait(&u_full[stage], (uint32_t)((i / STAGES) & 1));
             const double* xt = xs + (size_t)stage * BM * S;
             const double* utb = ut + (size_t)stage * BM * KS;
             const int64_t rows_left = s_node[k].n - r0;
