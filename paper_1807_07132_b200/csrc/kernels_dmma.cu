@@ -285,6 +285,17 @@ void dmma_setup(Shard& s, int split) {
         const double sa = a.L.nw * 10.0 - a.L.pipe - a.L.cs * 0.1, sb = b.L.nw * 10.0 - b.L.pipe - b.L.cs * 0.1;
         return sa > sb;
     });
+    // The split of the features over clusters and warps (cs, nw, mt) fixes the summation order of the
+    // split-K partials and warp trees, so it is chosen by the fixed rule above (deterministic across
+    // runs); only the pipeline shape (ring lag / stages, which leaves every sum's order unchanged) is
+    // timed on the shard itself.
+    {
+        const Layout& f = top[0].L;
+        std::vector<Cand> same;
+        for (const Cand& c : top)
+            if (c.L.cs == f.cs && c.L.nw == f.nw && c.L.mt == f.mt && c.active == top[0].active) same.push_back(c);
+        top.swap(same);
+    }
     size_t pick = 0;
     if (autotune && top.size() > 1) {
         float best_ms = 1e30f;

@@ -65,6 +65,31 @@ def test_sparse_model_ops(nadmm, port, n, p, C, dens):
     assert rel(nadmm.hessian_vec(dd, w, v, 0.0), nadmm.hessian_vec(ds, w, v, 0.0)) <= TOL_KERNEL
 
 
+@pytest.mark.parametrize("n,p,C,sparse", [(50_000, 3072, 10, False), (60_000, 784, 10, False), (40_000, 2048, 100, False),
+                                          (300_000, 28, 2, False), (20_000, 200_000, 20, True)])
+def test_products_bitwise_repeatable(nadmm, n, p, C, sparse):
+    """Race detector (compute-sanitizer is closed on this pool): every pass implementation --
+    clustered DMMA (K = 9), two-GEMM DMMA with >= 3 tiles per CTA (C = 100), small-p ring, CSR
+    gathers -- returns bit-identical gradients and products on repeated calls (fixed-order
+    reductions, no atomics), so any data race in the mbarrier / DSMEM pipelines shows up here."""
+    rng = np.random.default_rng(n + p)
+    if sparse:
+        ip, ix, vv, y = nadmm.generate_sparse(n, p, C, 100, 3)
+        ds = nadmm.Dataset.sparse(ip, ix, vv, y, C, p)
+    else:
+        X = rng.normal(size=(n, p)) / np.sqrt(p)
+        ds = nadmm.Dataset.dense(X, (np.arange(n) % C + 1).astype(np.int32), C)
+    d = ds.weight_dim()
+    w, v = rng.normal(size=d) * 0.1, rng.normal(size=d)
+    g0 = nadmm.gradient(ds, w, 1e-3)
+    h0 = nadmm.hessian_vec(ds, w, v, 1e-3)
+    for _ in range(3):
+        np.testing.assert_array_equal(nadmm.hessian_vec(ds, w, v, 1e-3), h0)
+        ds2w = w * (1.0 + 1e-9)  # a new point forces a fresh cache pass, then back
+        nadmm.gradient(ds, ds2w, 1e-3)
+        np.testing.assert_array_equal(nadmm.gradient(ds, w, 1e-3), g0)
+
+
 def test_spec_known_answers(nadmm):
     # loss, any data, w = 0, lambda = 0 -> n log C (SPEC.md:55)
     X = np.arange(12.0).reshape(4, 3)
