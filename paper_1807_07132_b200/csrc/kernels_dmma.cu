@@ -256,6 +256,12 @@ void dmma_setup(Shard& s, int split) {
     s.layout_split = split;
     static const bool disabled = getenv("NADMM_DISABLE_DMMA") != nullptr;
     if (disabled || s.sparse || s.ldx % 2 != 0) return;
+    for (const auto& m : s.dmma_memo)  // chosen before for this split: re-apply (kernel attributes are set)
+        if (m.split == split) {
+            if (m.active > 0)
+                apply_layout(s, Layout{true, m.mt, m.nw, m.cs, m.fs, m.S, m.pipe, m.smem, 0.0}, m.active);
+            return;
+        }
     const char* force_cs = getenv("NADMM_DMMA_CS");  // profiling: restrict the cluster size
     const char* force_pipe = getenv("NADMM_DMMA_PIPE");
     const char* at = getenv("NADMM_DMMA_AUTOTUNE");
@@ -280,7 +286,10 @@ void dmma_setup(Shard& s, int split) {
     std::vector<Cand> top;
     for (const Cand& c : cands)
         if (c.sms >= 0.98 * best_sms) top.push_back(c);
-    if (top.empty()) return;
+    if (top.empty()) {
+        s.dmma_memo.push_back({split, 0, 0, 0, 0, 0, 0, 0, 0});
+        return;
+    }
     std::sort(top.begin(), top.end(), [](const Cand& a, const Cand& b) {
         const double sa = a.L.nw * 10.0 - a.L.pipe - a.L.cs * 0.1, sb = b.L.nw * 10.0 - b.L.pipe - b.L.cs * 0.1;
         return sa > sb;
@@ -310,6 +319,7 @@ void dmma_setup(Shard& s, int split) {
     }
     const Layout& best = top[pick].L;
     apply_layout(s, best, top[pick].active);
+    s.dmma_memo.push_back({split, best.mt, best.nw, best.cs, best.fs, best.S, best.pipe, top[pick].active, best.smem});
     if (getenv("NADMM_DMMA_VERBOSE"))
         fprintf(stderr,
                 "[nadmm] dmma layout p=%lld: cluster %d x %d clusters (%d SMs), %d warps x %d features, lag %d, "

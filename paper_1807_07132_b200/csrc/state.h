@@ -188,6 +188,11 @@ struct Shard {
     std::vector<cudaEvent_t> tl_events;
     // L-BFGS workspace (lbfgs.cu), kept across solves: curvature history + work vectors
     int layout_split = 1;  // concurrent shards the DMMA layout was tuned for
+    struct DmmaLayoutMemo {  // layouts already chosen per split (switching modes re-applies, no re-tune)
+        int split, mt, nw, cs, fs, S, pipe, active;
+        size_t smem;
+    };
+    std::vector<DmmaLayoutMemo> dmma_memo;
     // column-blocked CSR rows pass (kernels_sparse.cu): when the transposed weights exceed an L2-sized
     // budget, the rows pass runs once per column block so each block's weights stay L2-resident.
     // rblk[i * (nblk + 1) + b] = first nonzero of row i in column block b; lsum = running logits
