@@ -761,10 +761,10 @@ def main():
         _t.cuda.current_stream().synchronize()
         buf[:] = pin_S.numpy()
 
-    coord = ndist.HostCoordinator(d, LAM, len(mine), penalty="spectral", allreduce=nccl_sum if dist else None,
-                                  y=Y_h.numpy())
+    coord_threads = max(1, min(8, (os.cpu_count() or 1) // (2 * world)))
+    coord = ndist.NativeHostCoordinator(d, LAM, len(mine), penalty="spectral", allreduce=nccl_sum if dist else None,
+                                        y=Y_h.numpy(), threads=coord_threads)
     ybufs = [row for row in coord.y]
-    _t.set_num_threads(max(1, min(8, (os.cpu_count() or 1) // (2 * world))))
 
     def e2e_step():
         # one WorkerPool round through the worker ABI (nadmm_workers_solve): z and y_i host -> device
@@ -786,10 +786,11 @@ def main():
     e2e = {"value": hv_e2e / t_e2e, "unit": "Hv/s", "h2d_bytes_per_step": per * 2 * d * 8 * world + coord_bytes,
            "d2h_bytes_per_step": per * d * 8 * world + coord_bytes,
            "path": "nadmm_workers_solve per round (scatter z, y_i / gather x_i for all local nodes) + host "
-                   "coordinator (paper_1807_07132_b200.dist.HostCoordinator, spectral penalty selection)"}
+                   "coordinator (nadmm_hcoord_*: the library's fused host coordinator, spectral penalty selection)"}
 
     for w in workers:  # the shards' solver state is bound to the workers until they are released
         w.close()
+    coord.close()
 
     # ---------------- time to target: theta = (F - F*)/F* <= 0.05 ----------------
     ttt, parity, cpu, fstar_info = {}, None, None, {}

@@ -319,6 +319,25 @@ nadmm_status nadmm_admm_result(nadmm_admm run, double* z_out, double* rho_out, i
                                int32_t* converged);
 nadmm_status nadmm_admm_free(nadmm_admm run);
 
+/* Host-side consensus coordinator over HOST buffers (no GPU needed): the reference's coordinator
+ * (inc/admm.hpp:58-140) for callers that drive the workers themselves through
+ * nadmm_workers_solve / nadmm_worker_solve (the worker-transport deployment). One round =
+ *   nadmm_hcoord_sum    : S[0..d) = sum_i (rho_i x_i - y_i), S[d] = sum_i rho_i (local workers, ascending)
+ *   (the caller sums S over processes when there are several)
+ *   nadmm_hcoord_update : z = S / (lambda + S[d]); y_hat_i = y_i + rho_i (z_prev - x_i);
+ *                         y_i += rho_i (z - x_i) (in place); spectral penalty selection every
+ *                         update_period rounds; z_out (d), rho_out (n_local).
+ * Two fused OpenMP sweeps per round over `threads` host threads. */
+typedef struct nadmm_hcoord_s* nadmm_hcoord;
+nadmm_status nadmm_hcoord_create(int64_t d, int32_t n_local, double lambda, int32_t spectral, double rho0,
+                                 int32_t update_period, double eps_cor, double rho_min, double rho_max,
+                                 int32_t threads, nadmm_hcoord* out);
+nadmm_status nadmm_hcoord_sum(nadmm_hcoord c, const double* const* x, const double* const* y, double* S);
+nadmm_status nadmm_hcoord_update(nadmm_hcoord c, const double* const* x, double* const* y, const double* S,
+                                 double* z_out, double* rho_out);
+nadmm_status nadmm_hcoord_free(nadmm_hcoord c);
+const char* nadmm_hcoord_last_error(void);
+
 /* ------------------------------------------------------------------------------------------ */
 /* Host-only data fixtures (no GPU needed) -- src/data_io.cpp:16-43, 300-370                    */
 /* ------------------------------------------------------------------------------------------ */

@@ -142,6 +142,12 @@ SIGNATURES = {
     "nadmm_libsvm_free": (None, [VP]),
     "nadmm_idx_info": (S, [C.c_char_p, C.c_char_p, I64, I64]),
     "nadmm_idx_load": (S, [C.c_char_p, C.c_char_p, D, I32, I32, D]),
+    "nadmm_hcoord_create": (S, [C.c_int64, C.c_int32, C.c_double, C.c_int32, C.c_double, C.c_int32, C.c_double,
+                                C.c_double, C.c_double, C.c_int32, C.POINTER(VP)]),
+    "nadmm_hcoord_sum": (S, [VP, C.POINTER(D), C.POINTER(D), D]),
+    "nadmm_hcoord_update": (S, [VP, C.POINTER(D), C.POINTER(D), D, D, D]),
+    "nadmm_hcoord_free": (S, [VP]),
+    "nadmm_hcoord_last_error": (C.c_char_p, []),
 }
 
 _lib = None

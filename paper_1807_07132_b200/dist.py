@@ -149,6 +149,68 @@ class HostCoordinator:
         return self.z
 
 
+class NativeHostCoordinator:
+    """The same coordinator as `HostCoordinator`, run by the library's host code (nadmm_hcoord_*:
+    two fused OpenMP sweeps per round over caller-owned buffers, no GPU needed). `X` and `y` are
+    (n_local, d) float64 arrays (e.g. pinned); `y` is updated in place; `allreduce(buf)` sums the
+    (d + 1)-long consensus buffer over processes when there are several."""
+
+    def __init__(self, d: int, lam: float, n_local: int = 1, penalty: str = "fixed", rho0: float = 1.0,
+                 update_period: int = 2, eps_cor: float = 0.2, rho_min: float = 1e-6, rho_max: float = 1e6,
+                 allreduce: Optional[Callable[[np.ndarray], None]] = None, y: Optional[np.ndarray] = None,
+                 threads: int = 8):
+        import ctypes as C
+
+        from . import _lib as L
+
+        if penalty not in ("fixed", "spectral"):
+            raise ValueError(f"unknown penalty {penalty!r}")
+        self._C, self._L = C, L
+        self.d, self.n, self.allreduce = d, n_local, allreduce
+        self.y = y if y is not None else np.zeros((n_local, d))
+        self.y[:] = 0.0
+        self.z = np.zeros(d)
+        self.rho = np.full(n_local, float(rho0))
+        self._S = np.zeros(d + 1)
+        h = C.c_void_p()
+        rc = L.lib().nadmm_hcoord_create(d, n_local, lam, 1 if penalty == "spectral" else 0, rho0, update_period,
+                                         eps_cor, rho_min, rho_max, threads, C.byref(h))
+        if rc:
+            raise ValueError(L.lib().nadmm_hcoord_last_error().decode())
+        self._h = h
+        D = L.D
+        self._yp = (D * n_local)(*[row.ctypes.data_as(D) for row in self.y])
+
+    def _ptrs(self, X):
+        D = self._L.D
+        return (D * self.n)(*[row.ctypes.data_as(D) for row in X])
+
+    def step(self, X: np.ndarray) -> np.ndarray:
+        L, D = self._L, self._L.D
+        xp = self._ptrs(X)
+        rc = L.lib().nadmm_hcoord_sum(self._h, xp, self._yp, self._S.ctypes.data_as(D))
+        if rc:
+            raise ValueError(L.lib().nadmm_hcoord_last_error().decode())
+        if self.allreduce is not None:
+            self.allreduce(self._S)
+        rc = L.lib().nadmm_hcoord_update(self._h, xp, self._yp, self._S.ctypes.data_as(D), self.z.ctypes.data_as(D),
+                                         self.rho.ctypes.data_as(D))
+        if rc:
+            raise ValueError(L.lib().nadmm_hcoord_last_error().decode())
+        return self.z
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._L.lib().nadmm_hcoord_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def torch_allreduce(dist, group=None) -> Callable[[np.ndarray], None]:
     """allreduce callback over a torch.distributed group (gloo on CPU tensors)."""
     import torch

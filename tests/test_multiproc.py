@@ -109,6 +109,27 @@ def test_host_coordinator_matches_oracle_coordinator(port):
     assert not np.allclose(rho, rhos)  # the spectral update actually fired
 
 
+@pytest.mark.parametrize("penalty", ["fixed", "spectral"])
+def test_native_host_coordinator_matches(penalty, port):
+    """nadmm_hcoord_* (the library's fused host coordinator) against the torch HostCoordinator:
+    z, y and rho over several rounds (the dot products and sums run in different orders: 1e-12)."""
+    xs, ys, rhos = _fixture()
+    a = nd.HostCoordinator(D, LAM, NODES, penalty=penalty)
+    b = nd.NativeHostCoordinator(D, LAM, NODES, penalty=penalty, threads=3)
+    a.y[:] = ys
+    b.y[:] = ys
+    for s in range(STEPS + 2):
+        X = np.stack([_x(i, s) for i in range(NODES)])
+        za = a.step(X).copy()
+        zb = b.step(X).copy()
+        np.testing.assert_allclose(zb, za, rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(b.y, a.y, rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(b.rho, a.rho, rtol=1e-12)
+    if penalty == "spectral":
+        assert not np.allclose(b.rho, 1.0)
+    b.close()
+
+
 def test_spectral_rho_matches_oracle(port):
     rng = np.random.default_rng(5)
     for trial in range(40):
