@@ -696,13 +696,13 @@ def main():
     peak = float(peaks.get("hbm_gbs", 6650.0))
     traffic = None  # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
     try:
-        prof = json.loads((ROOT / "profiles" / "r1_hv_kernel.json").read_text())
+        prof = json.loads((ROOT / "profiles" / "r2_hv_kernel.json").read_text())
         if n_loc == 6250 and P == 3072:
             traffic = int(prof["traffic_bytes_per_launch"])
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "traffic_source": "profiles/r1_hv_kernel.json (ncu dram__bytes_read+write)", "kernel": "dense Hv pass with the fused CG step (node-group launch over the GPU's 6250x3072 shards, or one shard per node stream), CUDA events around each launch",
+                "traffic": traffic, "traffic_source": "profiles/r2_hv_kernel.json (ncu dram__bytes_read+write of the bench's own Hv launch)", "kernel": "dense Hv pass with the fused CG step (node-group launch over the GPU's 6250x3072 shards, or one shard per node stream), CUDA events around each launch",
                 "hv_pass_ms": hv_ms, "concurrent_launches": conc, "shards_per_launch": shards_per_launch,
                 "per_launch_achieved": shards_per_launch * hv_bytes(n_loc) / (hv_ms * 1e-3) / 1e9,
                 "step_check": "value x bytes_per_hv = whole-step Hv traffic rate (lower bound incl. non-Hv kernels)",
@@ -766,13 +766,21 @@ def main():
                                         y=Y_h.numpy(), threads=coord_threads)
     ybufs = [row for row in coord.y]
 
+    e2e_prof = [0.0, 0.0, 0] if os.environ.get("NADMM_BENCH_E2E_PROFILE") else None
+
     def e2e_step():
         # one WorkerPool round through the worker ABI (nadmm_workers_solve): z and y_i host -> device
         # (the reference's scatter sends z to every worker), the solves (concurrent on the GPU),
         # x_i device -> pinned host; then the host coordinator with spectral penalty selection
         zbuf[:] = coord.z
+        t_a = time.perf_counter()
         _, sts = nadmm.workers_solve(workers, coord.rho, zbuf, ybufs, cfg.newton, 1, outs=xbufs)
+        t_b = time.perf_counter()
         coord.step(Xn)
+        if e2e_prof is not None:
+            e2e_prof[0] += t_b - t_a
+            e2e_prof[1] += time.perf_counter() - t_b
+            e2e_prof[2] += 1
         return sum(s.cg_iters + s.inner_iters for s in sts)
 
     for _ in range(args.warmup):
@@ -782,6 +790,10 @@ def main():
     hv_e2e = sum(e2e_step() for _ in range(args.steps))
     t_e2e = max_over_ranks(time.perf_counter() - t0)
     hv_e2e = sum_over_ranks(hv_e2e)
+    if e2e_prof is not None:  # profiling: per-rank split of the e2e round (solves vs host coordinator)
+        k = max(1, e2e_prof[2])
+        print(f"[e2e rank {rank}] workers_solve {1e3 * e2e_prof[0] / k:.3f} ms, coordinator "
+              f"{1e3 * e2e_prof[1] / k:.3f} ms per round (incl. warm-up)", file=sys.stderr)
     coord_bytes = (d + 1) * 8 * world if dist else 0  # coordinator sum staged through HBM for NCCL
     e2e = {"value": hv_e2e / t_e2e, "unit": "Hv/s", "h2d_bytes_per_step": per * 2 * d * 8 * world + coord_bytes,
            "d2h_bytes_per_step": per * d * 8 * world + coord_bytes,

@@ -344,6 +344,7 @@ nadmm_status nadmm_comm_create(nadmm_ctx ctx, const uint8_t id[128], int32_t nra
             delete c;
             raise(NADMM_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
         }
+        ctx->live++;
         *out = c;
         return NADMM_OK;
     } catch (const Error& e) {
@@ -354,7 +355,9 @@ nadmm_status nadmm_comm_create(nadmm_ctx ctx, const uint8_t id[128], int32_t nra
 nadmm_status nadmm_comm_destroy(nadmm_comm c) {
     if (!c) return NADMM_OK;
     if (c->comm) ncclCommDestroy(c->comm);
+    Ctx* ctx = c->ctx;
     delete c;
+    ctx_unref(ctx);
     return NADMM_OK;
 }
 
@@ -871,6 +874,7 @@ nadmm_status nadmm_admm_create(const nadmm_shard* shards, int32_t n_local, nadmm
         if (!out) raise(NADMM_ECONFIG, "null output");
         (void)cudaGetLastError();
         *out = new nadmm_admm_s(shards, n_local, comm, cfg);
+        for (Shard* s : (*out)->shards) shard_hold(s);
         return NADMM_OK;
     } catch (const Error& e) {
         set_last_error(e.what());
@@ -911,7 +915,10 @@ nadmm_status nadmm_admm_result(nadmm_admm run, double* z_out, double* rho_out, i
 }
 
 nadmm_status nadmm_admm_free(nadmm_admm run) {
+    if (!run) return NADMM_OK;
+    const std::vector<Shard*> held = run->shards;
     delete run;
+    for (Shard* s : held) shard_unhold(s);
     return NADMM_OK;
 }
 

@@ -204,6 +204,42 @@ void Shard::ensure_timers(int n) {
 
 }  // namespace nadmm
 
+namespace nadmm {
+
+static void ctx_release_now(Ctx* ctx) {
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    group_drop(*ctx);
+    if (ctx->dctr) cudaFree(ctx->dctr);
+    for (int i = 0; i < Ctx::kMaxNodeStreams; ++i) {
+        if (ctx->node_stream[i]) cudaStreamDestroy(ctx->node_stream[i]);
+        if (ctx->node_join[i]) cudaEventDestroy(ctx->node_join[i]);
+    }
+    if (ctx->node_fork) cudaEventDestroy(ctx->node_fork);
+    cudaStreamDestroy(ctx->stream);
+    delete static_cast<nadmm_ctx_s*>(ctx);
+}
+
+void ctx_unref(Ctx* c) {
+    if (c && --c->live == 0 && c->released) ctx_release_now(c);
+}
+
+static void shard_release_now(Shard* s) {
+    Ctx* c = s->ctx;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    delete static_cast<nadmm_shard_s*>(s);
+    ctx_unref(c);
+}
+
+void shard_hold(Shard* s) { ++s->holders; }
+
+void shard_unhold(Shard* s) {
+    if (--s->holders == 0 && s->released) shard_release_now(s);
+}
+
+}  // namespace nadmm
+
 extern "C" {
 
 const char* nadmm_last_error(void) { return g_last_error.c_str(); }
@@ -256,18 +292,9 @@ nadmm_status nadmm_ctx_create(int32_t device, nadmm_ctx* out) {
 
 nadmm_status nadmm_ctx_destroy(nadmm_ctx ctx) {
     return guard([&] {
-        if (!ctx) return;
-        cudaSetDevice(ctx->device);
-        cudaStreamSynchronize(ctx->stream);
-        group_drop(*ctx);
-        if (ctx->dctr) cudaFree(ctx->dctr);
-        for (int i = 0; i < Ctx::kMaxNodeStreams; ++i) {
-            if (ctx->node_stream[i]) cudaStreamDestroy(ctx->node_stream[i]);
-            if (ctx->node_join[i]) cudaEventDestroy(ctx->node_join[i]);
-        }
-        if (ctx->node_fork) cudaEventDestroy(ctx->node_fork);
-        cudaStreamDestroy(ctx->stream);
-        delete ctx;
+        if (!ctx || ctx->released) return;
+        ctx->released = true;
+        if (ctx->live == 0) ctx_release_now(ctx);  // else: the last shard / communicator releases it
     });
 }
 
@@ -334,6 +361,7 @@ nadmm_status nadmm_shard_dense(nadmm_ctx ctx, const double* X, int64_t n, int64_
         upload(s->labels, labels, sizeof(int32_t) * n, ctx->stream);
         alloc_work(*s);
         stream_sync(ctx->stream);
+        ctx->live++;
         *out = s.release();
     });
 }
@@ -454,16 +482,16 @@ nadmm_status nadmm_shard_csr(nadmm_ctx ctx, const int64_t* indptr, const int32_t
         }
         alloc_work(*s);
         stream_sync(ctx->stream);
+        ctx->live++;
         *out = s.release();
     });
 }
 
 nadmm_status nadmm_shard_free(nadmm_shard s) {
     return guard([&] {
-        if (!s) return;
-        cudaSetDevice(s->ctx->device);
-        cudaStreamSynchronize(s->ctx->stream);
-        delete s;
+        if (!s || s->released) return;
+        s->released = true;
+        if (s->holders == 0) shard_release_now(s);  // else: its last worker / session releases it
     });
 }
 
@@ -652,13 +680,17 @@ nadmm_status nadmm_worker_create(nadmm_shard s, nadmm_worker* out) {
         if (s->cache_at == Shard::kAtX) s->cache_at = Shard::kNone;
         *out = new nadmm_worker_s{s};
         s->owner = *out;  // x_local lives in the shard: one worker per shard
+        shard_hold(s);
     });
 }
 
 nadmm_status nadmm_worker_free(nadmm_worker w) {
     return guard([&] {
-        if (w && w->shard && w->shard->owner == w) w->shard->owner = nullptr;
+        if (!w) return;
+        Shard* s = w->shard;
+        if (s && s->owner == w) s->owner = nullptr;
         delete w;
+        if (s) shard_unhold(s);
     });
 }
 

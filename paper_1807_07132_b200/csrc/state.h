@@ -76,6 +76,11 @@ struct Ctx {
     // each DMMA shard's persistent grid sized to 1/k of the co-resident clusters so all k fit at once
     int node_streams = 1;
     static constexpr int kMaxNodeStreams = 8;
+    // objects created on this context (shards, communicators) that are still alive: destroying the
+    // context only marks it released, and the last of them to go releases it (any release order is
+    // safe, e.g. finalizers run in arbitrary order at interpreter exit)
+    int live = 0;
+    bool released = false;
     cudaStream_t node_stream[kMaxNodeStreams] = {};
     cudaEvent_t node_fork = nullptr, node_join[kMaxNodeStreams] = {};
     void* group = nullptr;  // cached node-group iteration graph (GroupGraph, newton.cu)
@@ -115,6 +120,9 @@ enum Slot : int {
 
 struct Shard {
     Ctx* ctx = nullptr;
+    // workers / ADMM sessions holding the shard: nadmm_shard_free defers to the last of them
+    int holders = 0;
+    bool released = false;
     int64_t n = 0, p = 0;
     int C = 0, K = 0;  // K = C - 1
     int64_t d = 0;
@@ -295,6 +303,11 @@ void barrier_configure();
 void barrier_check();
 // cudaStreamSynchronize + the barrier fault check: every host synchronisation of the library.
 void stream_sync(cudaStream_t st);
+// Deferred release (capi.cu): a context outlives its shards / communicators, a shard its workers /
+// sessions, whatever order the handles are freed in.
+void ctx_unref(Ctx* c);
+void shard_hold(Shard* s);
+void shard_unhold(Shard* s);
 }  // namespace nadmm
 
 struct nadmm_ctx_s : nadmm::Ctx {};
