@@ -57,6 +57,9 @@ int32_t nadmm_abi_version(void);
 /* Context                                                                                    */
 /* ------------------------------------------------------------------------------------------ */
 nadmm_status nadmm_ctx_create(int32_t device, nadmm_ctx* out);
+/* Handles may be freed in any order: destroying a context with live shards / communicators (or freeing
+ * a shard held by a live worker / ADMM session) only marks it released; the last dependent object to
+ * be freed releases it. A released handle must not be passed to new calls. */
 nadmm_status nadmm_ctx_destroy(nadmm_ctx ctx);
 /* Concurrent ADMM nodes per GPU (NADMM_NODE_STREAMS, default 4): run_admm / nadmm_workers_solve run
  * up to this many local nodes' solves at once, each DMMA shard on a 1/k-GPU persistent grid. */
