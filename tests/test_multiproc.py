@@ -1,6 +1,7 @@
 """N > 1 host logic on CPU: world_size-2 gloo process groups (127.0.0.1) drive the rank plumbing of
-the multi-GPU consensus loop (paper_1807_07132_b200/dist.py) and must reproduce the single-process
-coordinator and the oracle's z/y updates."""
+the multi-GPU consensus loop (paper_1807_07132_b200/dist.py) and the library's host coordinator
+(nadmm_hcoord_*, the bench's e2e coordinator), which must reproduce the single-process run, the
+oracle's z/y updates and the torch restatement in tests/coord_ref.py."""
 import os
 import socket
 
@@ -10,6 +11,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_1807_07132_b200 import dist as nd
+
+import coord_ref
 
 NODES, D, LAM, STEPS = 4, 37, 1e-3, 5
 
@@ -39,13 +42,14 @@ def _worker(rank, world, port, out):
         mine = nd.node_range(NODES, world, rank)
         uid = nd.share_unique_id(dist, rank, lambda: bytes(range(128)))
         xs, ys, rhos = _fixture()
-        co = nd.HostCoordinator(D, LAM, len(mine), penalty="spectral", allreduce=nd.torch_allreduce(dist))
+        co = nd.NativeHostCoordinator(D, LAM, len(mine), penalty="spectral", allreduce=nd.torch_allreduce(dist),
+                                      threads=2)
         co.y[:] = [ys[i] for i in mine]
-        co.rho[:] = [rhos[i] for i in mine]
         zs = []
         for step in range(STEPS):  # consensus rounds on a fixed x trajectory (z / y / rho evolve)
             zs.append(co.step(np.stack([_x(i, step) for i in mine])).copy())
         out[rank] = {"nodes": list(mine), "uid": uid, "z": zs, "y": co.y.copy(), "rho": co.rho.copy()}
+        co.close()
     finally:
         dist.destroy_process_group()
 
@@ -57,10 +61,9 @@ def test_node_range():
         nd.node_range(8, 3, 0)
 
 
-def _single(xs_rows, ys, rhos):
-    co = nd.HostCoordinator(D, LAM, NODES, penalty="spectral")
+def _single(xs_rows, ys):
+    co = nd.NativeHostCoordinator(D, LAM, NODES, penalty="spectral", threads=2)
     co.y[:] = ys
-    co.rho[:] = rhos
     zs = [co.step(np.stack([_x(i, s) for i in range(NODES)])).copy() for s in range(STEPS)]
     return co, zs
 
@@ -71,7 +74,7 @@ def test_world2_coordinator_matches_single_process(port):
     p = _free_port()
     mp.start_processes(_worker, args=(world, p, out), nprocs=world, join=True, start_method="spawn")
     xs, ys, rhos = _fixture()
-    co, zs1 = _single(xs, ys, rhos)
+    co, zs1 = _single(xs, ys)
     assert out[0]["uid"] == out[1]["uid"] == bytes(range(128))
     assert out[0]["nodes"] + out[1]["nodes"] == list(range(NODES))
     for r in range(world):
@@ -83,11 +86,11 @@ def test_world2_coordinator_matches_single_process(port):
 
 
 def test_host_coordinator_matches_oracle_coordinator(port):
-    """The host coordinator's z / y-hat / y / spectral-penalty sequence against the oracle's
+    """The library's host coordinator's z / y-hat / y / spectral-penalty sequence against the oracle's
     coordinator pieces (nor_z_update pairwise tree, nor_y_update, nor_spectral_rho)."""
     xs, ys, rhos = _fixture()
-    co, zs1 = _single(xs, ys, rhos)
-    z, y, rho = np.zeros(D), np.array(ys), np.array(rhos)
+    co, zs1 = _single(xs, ys)
+    z, y, rho = np.zeros(D), np.array(ys), np.ones(NODES)
     snap = None
     for s in range(STEPS):
         X = np.stack([_x(i, s) for i in range(NODES)])
@@ -106,15 +109,15 @@ def test_host_coordinator_matches_oracle_coordinator(port):
         np.testing.assert_allclose(zs1[s], z, rtol=1e-12, atol=1e-15)
     np.testing.assert_allclose(co.y, y, rtol=1e-12, atol=1e-15)
     np.testing.assert_allclose(co.rho, rho, rtol=1e-12)
-    assert not np.allclose(rho, rhos)  # the spectral update actually fired
+    assert not np.allclose(rho, 1.0)  # the spectral update actually fired
 
 
 @pytest.mark.parametrize("penalty", ["fixed", "spectral"])
 def test_native_host_coordinator_matches(penalty, port):
-    """nadmm_hcoord_* (the library's fused host coordinator) against the torch HostCoordinator:
-    z, y and rho over several rounds (the dot products and sums run in different orders: 1e-12)."""
+    """nadmm_hcoord_* (the library's fused host coordinator) against the torch restatement
+    (tests/coord_ref.py): z, y and rho over several rounds (sums in different orders: 1e-12)."""
     xs, ys, rhos = _fixture()
-    a = nd.HostCoordinator(D, LAM, NODES, penalty=penalty)
+    a = coord_ref.HostCoordinator(D, LAM, NODES, penalty=penalty)
     b = nd.NativeHostCoordinator(D, LAM, NODES, penalty=penalty, threads=3)
     a.y[:] = ys
     b.y[:] = ys
@@ -139,4 +142,4 @@ def test_spectral_rho_matches_oracle(port):
         if trial % 4 == 0:
             d = -c * 0.5 + 0.05 * d  # correlated z-side
         want = port.spectral_rho(a, b, c, d, 1.3)[0]
-        assert abs(nd.spectral_rho(a, b, c, d, 1.3) - want) <= 1e-12 * abs(want)
+        assert abs(coord_ref.spectral_rho(a, b, c, d, 1.3) - want) <= 1e-12 * abs(want)
