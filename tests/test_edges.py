@@ -91,11 +91,14 @@ def test_duplicate_entries_are_summed(nadmm):
 def test_tiny_dense_shapes(nadmm, port, n, p, C):
     """One-row / one-feature shards and shards smaller than one row tile of the fused passes."""
     rng = np.random.default_rng(n * 1000 + p)
-    X = rng.normal(size=(n, p))
+    # the suite's conditioning convention (features scaled by 1/sqrt(p), as test_dense_model_ops):
+    # unscaled 3,072-feature rows give logits of ~17 and a near one-hot softmax, where Hv's
+    # P o a - P (P^T a) cancels and any change of summation order shows at ~1e-11
+    X = rng.normal(size=(n, p)) / np.sqrt(p)
     y = (np.arange(n) % C + 1).astype(np.int32)
     ds = nadmm.Dataset.dense(X, y, C)
     sh = oracle.Shard(X, y, C)
-    w = rng.normal(size=sh.d) * 0.3
+    w = rng.normal(size=sh.d)
     v = rng.normal(size=sh.d)
     lw = port.loss(sh, w, 1e-3)
     assert abs(nadmm.loss(ds, w, 1e-3) - lw) <= TOL * abs(lw)
