@@ -12,7 +12,14 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
 }
 
-template <int C, int MIX>  // MIX bit 0: + LDS.64 operand, bit 1: + DFMA
+__device__ __forceinline__ double dfma_v(double a, double b, double c) {  // pinned in program order
+  double d;
+  asm volatile("fma.rn.f64 %0, %1, %2, %3;" : "=d"(d) : "d"(a), "d"(b), "d"(c));
+  return d;
+}
+
+// MIX bit 0: + LDS.64 operand, bit 1: + DFMA interleaved, bit 2: DFMAs as one burst after the DMMAs
+template <int C, int MIX>
 __global__ void kern(double* out, int iters) {
   __shared__ double sm[4096];
   for (int i = threadIdx.x; i < 4096; i += blockDim.x) sm[i] = i * 1e-6;
@@ -29,6 +36,10 @@ __global__ void kern(double* out, int iters) {
       double a = (MIX & 1) ? base[(s * 8 + it) & 255] : (threadIdx.x * 1e-3 + s);
       dmma(c[s % C], a, b);
       if (MIX & 2) r[s & 3] = fma(a, vr, r[s & 3]);
+    }
+    if (MIX & 4) {
+#pragma unroll
+      for (int s = 0; s < 16; ++s) r[s & 3] = dfma_v(b + s, vr, r[s & 3]);
     }
   }
   double t = r[0] + r[1] + r[2] + r[3];
@@ -50,7 +61,7 @@ void run(int warps, double* out, cudaEvent_t e0, cudaEvent_t e1) {
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   const double flops = 512.0 * 16 * iters * warps * (double)sms;
-  printf("warps/SM %2d chains %d %-16s %6.2f TFLOP/s (DMMA flops)\n", warps, C, MIX == 3 ? "+DFMA +LDS" : MIX == 2 ? "+DFMA" : MIX == 1 ? "+LDS" : "DMMA only",
+  printf("warps/SM %2d chains %d %-16s %6.2f TFLOP/s (DMMA flops)\n", warps, C, MIX == 3 ? "+DFMA +LDS" : MIX == 2 ? "+DFMA" : MIX == 1 ? "+LDS" : MIX == 4 ? "+DFMA burst" : MIX == 5 ? "+DFMA burst +LDS" : "DMMA only",
          flops / (ms * 1e-3) / 1e12);
 }
 
@@ -65,6 +76,8 @@ int main() {
     run<4, 1>(w, out, e0, e1);
     run<4, 2>(w, out, e0, e1);
     run<4, 3>(w, out, e0, e1);
+    run<4, 4>(w, out, e0, e1);
+    run<4, 5>(w, out, e0, e1);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
