@@ -6,7 +6,8 @@ in iteration count and test predictions with F(z^k) and z <= 1e-9 (north_star to
 iterates and objectives are held to the north_star 1e-9 here (1e-10 in test_gpu_parity.py at small sizes).
 
   cfg1  MNIST-shaped 60,000 x 784, C = 10: three Newton iterations (compute_reference's solver)
-  cfg2  CIFAR-shaped 50,000 x 3,072, C = 10, 8 ADMM nodes, SPS: the bench workload to theta <= 0.05
+  cfg2  CIFAR-shaped 50,000 x 3,072, C = 10, 8 ADMM nodes, SPS: the bench workload to theta <= 0.05;
+        and one node's L-BFGS worker rounds (run_worker's L-BFGS branch) on its 6,250-row shard
   cfg3  HIGGS-shaped 1,375,000 x 28, C = 2 (one GPU's weak-scaling shard): Hv + one Newton step
   cfg4  CSR 125,000 x 1,300,000, 650 nnz/row, C = 20 (one of 8 shards): Hv / grad / loss / predict +
         one Newton step
@@ -105,6 +106,60 @@ def test_cfg2_bench_workload_admm(nadmm, ref):
     assert rel(rg.z, run.z) <= TOL_ADMM
     te = nadmm.Dataset.dense(Xte, yte, 10)
     np.testing.assert_array_equal(nadmm.predict(te, rg.z), ref.dataset(oracle.Shard(Xte, yte, 10)).predict(run.z))
+
+
+def test_cfg2_workers_round(nadmm, ref):
+    """The e2e leg's call at the bench's size: one WorkerPool round (nadmm_workers_solve, the 8 nodes'
+    solves concurrent on the GPU, host z / y_i in, x_i out) against the reference's run_worker ADMM
+    branch on each 6,250 x 3,072 shard, two warm-started rounds."""
+    Xtr, ytr, _, _ = ref.generate_synthetic(55_556, 3072, 10, 1.0, 1.0, 0)
+    owner = ref.partition_owner(len(ytr), 8)
+    dss = [nadmm.Dataset.dense(Xtr[owner == i], ytr[owner == i], 10) for i in range(8)]
+    rws = [ref.dataset(oracle.Shard(Xtr[owner == i], ytr[owner == i], 10)).worker() for i in range(8)]
+    ws = [nadmm.Worker(ds) for ds in dss]
+    d = dss[0].weight_dim()
+    rng = np.random.default_rng(8)
+    try:
+        for k in range(2):
+            z = rng.normal(size=d) * 0.01
+            ys = [rng.normal(size=d) * 0.01 for _ in ws]
+            rho = [1.0 + 0.25 * i for i in range(8)]
+            xs, sts = nadmm.workers_solve(ws, rho, z, ys)
+            for i in range(8):
+                xr, sr = rws[i].solve(rho[i], z, ys[i])
+                assert rel(xs[i], xr) <= TOL_NEWTON
+                assert (sts[i].inner_iters, sts[i].cg_iters, sts[i].fn_evals, sts[i].flags) == \
+                    (sr["inner_iters"], sr["cg_iters"], sr["fn_evals"], sr["flags"])
+    finally:
+        for w in ws:
+            w.close()
+
+
+def test_cfg2_shard_lbfgs_worker(nadmm, ref):
+    """run_worker's L-BFGS branch (src/worker.cpp:183-195) on one bench node's 6,250 x 3,072 shard:
+    warm-started augmented rounds against the reference's lbfgs_solve."""
+    Xtr, ytr, _, _ = ref.generate_synthetic(55_556, 3072, 10, 1.0, 1.0, 0)
+    owner = ref.partition_owner(len(ytr), 8)
+    X0, y0 = Xtr[owner == 0], ytr[owner == 0]
+    ds = nadmm.Dataset.dense(X0, y0, 10)
+    rd = ref.dataset(oracle.Shard(X0, y0, 10))
+    d = ds.weight_dim()
+    w = nadmm.Worker(ds)
+    rng = np.random.default_rng(2)
+    x_ref = np.zeros(d)
+    cfg = nadmm.LbfgsConfig(grad_tol=1e-6)
+    try:
+        for k, (rho, inner) in enumerate([(1.0, 6), (0.7, 6)]):
+            z, yy = rng.normal(size=d) * 0.01, rng.normal(size=d) * 0.01
+            xg, st = w.solve_lbfgs(rho, z, yy, cfg, inner_iters=inner)
+            o = rd.lbfgs_solve(0.0, x_ref, (25, 1e-4, 0.9, inner, 20, 1e-6), rho=rho, z=z, y=yy)
+            x_ref = o["x"]
+            assert rel(xg, x_ref) <= TOL_NEWTON
+            assert st.inner_iters == len(o["trace"])
+            assert st.fn_evals == sum(int(t["fn_evals"]) for t in o["trace"])
+            assert st.grad_norm == pytest.approx(o["final_grad_norm"], rel=1e-8)
+    finally:
+        w.close()
 
 
 def test_cfg3_higgs_shard(nadmm, ref, port):
