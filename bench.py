@@ -594,6 +594,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # contract: W >= 3
+    if args.gpus != env_int("WORLD_SIZE", 1) and env_int("RANK", 0) == 0:
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={env_int('WORLD_SIZE', 1)}: N > 1 runs one process per GPU "
+              f"(python -m torch.distributed.run --nproc-per-node N ...); n_gpus reports the ranks that ran",
+              file=sys.stderr)
     if args.impl == "reference":
         return run_reference_arm(args)
     if args.config != "cfg2":
