@@ -43,6 +43,7 @@ N_TOTAL, P, C, LAM = 55_556, 3072, 10, 1e-3  # floor(9n/10) = 50,000 train rows
 NODES = 8
 SEP, NOISE, SEED = 1.0, 1.0, 0
 THETA_TARGET = 0.05
+THETA_TIGHT = 1e-3  # SPEC's second time-to-target threshold
 METRIC = "Hv products/s (Newton-ADMM shard Hessian-vector products; time-to-target alongside)"
 WORKLOAD = "cifar10-shaped dense 50000x3072 C=10 lambda=1e-3, Newton-ADMM (SPS penalty) over 8 row-shard nodes"
 
@@ -146,26 +147,32 @@ def ref_shards(oracle, r):
     return [oracle.Shard(Xtr[owner == i], ytr[owner == i], C) for i in range(NODES)], (Xtr, ytr, Xte, yte)
 
 
-def ref_time_to_target(oracle, r, shards, f_star, max_outer=60, budget_s=120.0):
+def ref_time_to_target(oracle, r, shards, f_star, max_outer=60, budget_s=120.0, targets=None):
     """The CPU reference's Newton-ADMM run (reference worker solves on a WorkerPool of host threads +
-    the port coordinator) until theta = (F(z^k) - F*)/F* <= THETA_TARGET; the clock covers solves,
-    coordinator and the F(z) evaluation, like the GPU's time-to-target leg."""
+    the port coordinator) until theta = (F(z^k) - F*)/F* <= THETA_TARGET (or every theta in
+    `targets`); the clock covers solves, coordinator and the F(z) evaluation, like the GPU's
+    time-to-target leg. Returns the run, the first target's (seconds, iteration), the CPU seconds
+    spent and {target: (seconds, iteration) or None}."""
+    targets = sorted(targets or [THETA_TARGET], reverse=True)
     run = oracle.RefAdmm(r, shards, ref_admm_cfg(oracle, max_outer), workers_parallel=True, eval_objective=True)
     t0 = time.perf_counter()
-    hit_t = hit_k = None
+    hits = {t: None for t in targets}
     try:
         while run.k < max_outer:
             row = run.step()
             row["wall_seconds"] = time.perf_counter() - t0
             row["theta"] = (row["train_objective"] - f_star) / f_star
-            if row["theta"] <= THETA_TARGET:
-                hit_t, hit_k = row["wall_seconds"], row["iteration"]
+            for t in targets:
+                if hits[t] is None and row["theta"] <= t:
+                    hits[t] = (row["wall_seconds"], row["iteration"])
+            if all(h is not None for h in hits.values()):
                 break
             if row["wall_seconds"] > budget_s:
                 break
     finally:
         run.close()
-    return run, hit_t, hit_k, time.perf_counter() - t0
+    first = hits[targets[0]] or (None, None)
+    return run, first[0], first[1], time.perf_counter() - t0, hits
 
 
 def load_f_star():
@@ -229,8 +236,8 @@ def cpu_reference_leg(Xtr, ytr, Xte, yte, owner, f_star, rows_gpu, z_gpu, pred_g
     torch.set_num_threads(cores)  # torch and the reference share one libgomp
     shards = [oracle.Shard(Xtr[owner == i], ytr[owner == i], C) for i in range(NODES)]
     k_gpu = len(rows_gpu)
-    run, hit_t, hit_k, spent = ref_time_to_target(oracle, r, shards, f_star, max_outer=max(k_gpu, 1) + 5,
-                                                  budget_s=float(os.environ.get("NADMM_CPU_BUDGET_S", 150)))
+    run, hit_t, hit_k, spent, _ = ref_time_to_target(oracle, r, shards, f_star, max_outer=max(k_gpu, 1) + 5,
+                                                     budget_s=float(os.environ.get("NADMM_CPU_BUDGET_S", 150)))
     n = min(k_gpu, len(run.metrics))
     same_trace = all((a["cg_iters"], a["fn_evals"], a["flags"]) == (b["cg_iters"], b["fn_evals"], b["flags"])
                      for a, b in zip(rows_gpu[:n], run.metrics[:n]))
@@ -298,10 +305,18 @@ def run_reference_arm(args):
     one.close()
     ttt = {}
     if not args.no_ttt and F_STAR is not None:
-        run2, hit_t, hit_k, spent = ref_time_to_target(oracle, r, shards, F_STAR)
+        # both SPEC targets (theta <= 0.05 and <= 1e-3) in one run, bounded by NADMM_REF_TTT_BUDGET_S
+        run2, hit_t, hit_k, spent, hits = ref_time_to_target(
+            oracle, r, shards, F_STAR, max_outer=150, budget_s=float(os.environ.get("NADMM_REF_TTT_BUDGET_S", 150)),
+            targets=[THETA_TARGET, THETA_TIGHT])
+        tight = hits[THETA_TIGHT]
         ttt = {"time_to_target_s": hit_t, "ttt_outer_iters": hit_k, "theta_target": THETA_TARGET, "f_star": F_STAR,
                "f_star_source": "profiles/r2_fstar.json (GPU compute_reference, certified by the CPU reference "
-                                "gradient at x*)", "ttt_cpu_seconds_spent": spent}
+                                "gradient at x*)", "ttt_cpu_seconds_spent": spent,
+               "time_to_target_1e-3_s": tight[0] if tight else None,
+               "ttt_1e-3_outer_iters": tight[1] if tight else None,
+               "ttt_1e-3_note": None if tight else f"theta <= {THETA_TIGHT} not reached within the CPU budget "
+                                                  f"({spent:.0f} s, {run2.k} outer iterations)"}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Hv/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
@@ -833,6 +848,16 @@ def main():
         ttt["test_accuracy"] = nadmm.accuracy(pred_gpu, yte)
         Xte_ds.close()
         s2.close()
+        # the SPEC's tighter threshold, theta <= 1e-3 (fresh run of the same loop)
+        barrier()
+        s3 = nadmm.AdmmSession(shards, tcfg, nadmm.EvalContext(True, f_star, THETA_TIGHT), comm)
+        s3.step(300)
+        rows3 = s3.result().metrics
+        hit3 = [r for r in rows3 if r["theta"] == r["theta"] and r["theta"] <= THETA_TIGHT]
+        t3 = max_over_ranks(hit3[0]["wall_seconds"] if hit3 else float("nan"))
+        ttt.update({"time_to_target_1e-3_s": t3 if hit3 else None,
+                    "ttt_1e-3_outer_iters": hit3[0]["iteration"] if hit3 else None})
+        s3.close()
 
         # ---- CPU reference on the same run (rank 0, N = 1): parity + cpu_baseline ----
         if rank == 0 and world == 1 and not args.no_cpu:
