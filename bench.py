@@ -519,7 +519,9 @@ def run_config(args):
                            "penalty": "spectral (SPS, rho0=1, T_f=2)", "generation_s": t_gen,
                            "l2": "no flush: per-step inputs exceed the 126 MB L2"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": None, "gpu_launches": int(st["kernel_launches"]),
-                "clocks": clk.summary(), "hv_per_step": hv_total / args.steps}
+                "clocks": clk.summary(), "hv_per_step": hv_total / args.steps,
+                # weak scaling: rows touched per second, n_loc x Hv/s summed over GPUs
+                "row_hv_per_s": value * n_loc}
         line.update(ttt)
         emit(line)
     if comm:
