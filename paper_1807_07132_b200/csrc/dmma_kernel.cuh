@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(dmma_max_threads(MT), 1) dmma_pass_kernel(Dmma
     using namespace dmma_detail;
     static_assert(STAGES >= LAG + 2, "ring depth");
     constexpr int K = 8 * KT + R;
-    static_assert(BM % 8 == 0 && BM <= 32, "row tile");
+    static_assert(BM == 8, "row tile: the row epilogues map 8 rows onto one warp (4 lanes per row)");
     constexpr int KS = DmmaSmem<K>::KS;
     constexpr int KP = DmmaSmem<K>::KP;
     constexpr int KE = (K + 1) & ~1;  // P rows are loaded K wide; region rounded to an even count
