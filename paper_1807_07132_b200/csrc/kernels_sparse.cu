@@ -4,15 +4,15 @@
 // rows pass (X W), the row's U coefficients in the columns pass (X^T U through the CSC copy) -- so the
 // pass is bound by L2 -> SM gather traffic (2 nnz K doubles per Hv), not by the CSR/CSC stream itself
 // (12 B per nonzero each). The design minimises the gathered sectors and keeps every lane busy:
-//   * the gathered tables (transposed weights wt = p x KS, U = n x KS) use a padded class stride
-//     KS = K rounded up to even, so a nonzero's K values are KS/2 aligned 16-byte double2 words
-//     (K = 19: 160 B = 5 whole sectors instead of 152 B straddling 5-6);
-//   * a warp owns a row (rows pass) or a column (columns pass); its lanes form G = 32 / (KS/2) groups
-//     of KS/2 lanes, each group gathers one nonzero's double2 words, so G nonzeros are in flight per
-//     warp instruction (K = 19: 3 nonzeros, 30 of 32 lanes busy) and kSpUnroll instructions are issued
-//     before their FMAs;
-//   * the CSR / CSC entries are read 32 at a time, one per lane (coalesced 128 B index and 256 B value
-//     loads), and broadcast to the groups by warp shuffles;
+//   * the gathered tables (transposed weights wt = p x KS, U = n x KS) use a padded class stride KS
+//     (sparse_class_stride), so a nonzero's K values are whole aligned words of VW doubles: 32-byte
+//     words (sm_100 256-bit loads, VW = 4) when KS is a multiple of 4, else 16-byte double2 words
+//     (K = 19: KS = 20, 160 B = 5 whole sectors = 5 lanes x 32 B);
+//   * a warp owns a row (rows pass) or a column (columns pass); its lanes form G = 32 / (KS/VW) groups,
+//     each group gathers one nonzero's words, so G nonzeros are in flight per warp instruction (K = 19:
+//     6 nonzeros, 30 of 32 lanes busy) and sp_unroll instructions are issued before their FMAs;
+//   * each lane loads its nonzeros' CSR / CSC entries itself (one broadcast request per group; no
+//     shuffles in the gather loop), and the warp's next segment is bulk-prefetched into L2;
 //   * group partial sums are folded into group 0 by shuffles; the row epilogue (U / softmax cache /
 //     loss / argmax) runs on group 0's lanes with 16-lane butterfly reductions.
 // When the transposed weights exceed an L2-sized budget the rows pass runs once per column block
@@ -28,7 +28,49 @@ namespace nadmm {
 namespace {
 
 constexpr int kSpThreads = 256;
-constexpr int kSpUnroll = 4;  // gathers in flight per lane before their FMAs
+// Rows / columns grids: exactly one resident wave (4 blocks of 256 threads per SM at <= 64 registers,
+// __launch_bounds__ below). cfg4 Hv: 3.07 ms at 4 per SM vs 3.23 / 3.54 / 4.74 ms at 8 / 3 / 2
+// (two waves, or fewer warps in flight).
+#ifndef NADMM_SP_BPSM
+#define NADMM_SP_BPSM 4
+#endif
+constexpr int kSpBlocksPerSm = NADMM_SP_BPSM;
+
+// Gathers in flight per lane before their FMAs: 4 x 16-byte words (VW = 2) or 3 x 32-byte words (VW = 4;
+// 6 nonzeros per warp instruction at K = 19, so a 32-entry CSR chunk is exactly 6 instructions).
+template <int VW>
+constexpr int sp_unroll() { return VW == 4 ? 3 : 4; }
+
+// One lane's VW-double word of a gathered table row (read-only path). VW = 4 is the sm_100 256-bit
+// load (LDG.E.ENL2.256): a nonzero's 160-byte K = 19 row is 5 lanes x 32 B, half the requests of
+// 16-byte words for the same sectors.
+template <int VW>
+__device__ __forceinline__ void ldg_word(const double* __restrict__ p, double (&o)[VW]) {
+    if constexpr (VW == 4) {
+        asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                     : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3])
+                     : "l"(p));
+    } else {
+        const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+        o[0] = t.x;
+        o[1] = t.y;
+    }
+}
+
+// Bulk L2 prefetch (TMA unit, no registers) of bytes [a, a + n) widened to 16-byte granules: the warp's
+// next CSR row / CSC column segment is pulled into L2 while the current one is gathered, so each
+// 32-entry index / value chunk is an L2 hit instead of a DRAM round trip in front of its gathers.
+__device__ __forceinline__ void prefetch_l2(const void* a, int64_t n) {
+    if (n <= 0) return;
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(a) & ~uintptr_t(15);
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(a) + (uintptr_t)n + 15) & ~uintptr_t(15);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
+}
+
+__device__ __forceinline__ void prefetch_segment(const int32_t* idx, const double* val, int64_t q0, int64_t q1) {
+    prefetch_l2(idx + q0, 4 * (q1 - q0));
+    prefetch_l2(val + q0, 8 * (q1 - q0));
+}
 
 // wt (p x KS, padded classes zero) = transpose of the block-major W (K x p): 32-column tiles through
 // shared memory so both the reads (along p) and the writes (32*KS contiguous doubles) are coalesced.
@@ -67,50 +109,49 @@ struct SpArgs {
 };
 
 // Gathered dot products of one segment [q0, q1) of a CSR row / CSC column: lane (group g, slot s)
-// accumulates sum_k v_k * tab[idx_k][2s..2s+1] over the segment's nonzeros k = g (mod G); group g's
-// partial is folded into group 0 (groups in ascending order). Valid on group 0's lanes.
-__device__ __forceinline__ double2 gather_segment(const int32_t* __restrict__ idx, const double* __restrict__ val,
-                                                  int64_t q0, int64_t q1, const double2* __restrict__ tab, int L,
-                                                  int G, int lane) {
+// accumulates sum_k v_k * tab[idx_k][VW s .. VW s + VW - 1] over the segment's nonzeros k = q0 + g (mod G)
+// in ascending order; group g's partial is folded into group 0 (groups in ascending order). Valid on
+// group 0's lanes. Each lane loads its nonzeros' index and value itself (a group's lanes read the same
+// address: one broadcast request, L1-resident after the first touch) -- no shuffles in the loop: the
+// earlier form (32 entries per chunk broadcast by shuffles, three SHFL per nonzero group) ran the same
+// gathers at half the rate (tools/microbench/gather_bw.cu: 6.9 vs 14.1 TB/s of gathered rows).
+template <int VW>
+__device__ __forceinline__ void gather_segment(const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                               int64_t q0, int64_t q1, const double* __restrict__ tab, int KS,
+                                               int L, int G, int lane, double (&acc)[VW]) {
+    constexpr int UNR = sp_unroll<VW>();
     const int grp = lane / L, sub = lane - grp * L;
-    const bool act = grp < G;
-    double ax = 0.0, ay = 0.0;
-    for (int64_t qb = q0; qb < q1; qb += 32) {
-        const int cnt = (int)((q1 - qb) < 32 ? (q1 - qb) : 32);
-        int jl = 0;
-        double vl = 0.0;
-        if (lane < cnt) {
-            jl = __ldg(idx + qb + lane);
-            vl = __ldg(val + qb + lane);
-        }
-        for (int t = 0; t < cnt; t += G * kSpUnroll) {
-            double2 w[kSpUnroll];
-            double v[kSpUnroll];
+    const double* __restrict__ tb = tab + sub * VW;
 #pragma unroll
-            for (int u = 0; u < kSpUnroll; ++u) {
-                const int k = t + u * G + grp;
-                const int jj = __shfl_sync(0xffffffffu, jl, k & 31);
-                const double vv = __shfl_sync(0xffffffffu, vl, k & 31);
-                const bool ok = act && k < cnt;
-                v[u] = ok ? vv : 0.0;
-                w[u] = ok ? __ldg(tab + (int64_t)jj * L + sub) : make_double2(0.0, 0.0);
-            }
+    for (int e = 0; e < VW; ++e) acc[e] = 0.0;
+    if (grp >= G) q1 = q0;  // idle lanes (32 mod L) skip the loop
+    for (int64_t t = q0 + grp; t < q1; t += (int64_t)G * UNR) {
+        // branch-free tail: slots past the segment re-read its last nonzero with weight 0
+        int jj[UNR];
+        double v[UNR];
 #pragma unroll
-            for (int u = 0; u < kSpUnroll; ++u) {
-                ax += v[u] * w[u].x;
-                ay += v[u] * w[u].y;
-            }
+        for (int u = 0; u < UNR; ++u) {
+            const int64_t k = t + (int64_t)u * G;
+            const int64_t kk = k < q1 ? k : q1 - 1;
+            jj[u] = __ldg(idx + kk);
+            const double x = __ldg(val + kk);
+            v[u] = k < q1 ? x : 0.0;
         }
+        double w[UNR][VW];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) ldg_word<VW>(tb + (int64_t)jj[u] * KS, w[u]);
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int e = 0; e < VW; ++e) acc[e] += v[u] * w[u][e];
     }
     for (int g = 1; g < G; ++g) {
-        const double ox = __shfl_sync(0xffffffffu, ax, (sub + g * L) & 31);
-        const double oy = __shfl_sync(0xffffffffu, ay, (sub + g * L) & 31);
-        if (grp == 0) {
-            ax += ox;
-            ay += oy;
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+            const double o = __shfl_sync(0xffffffffu, acc[e], (sub + g * L) & 31);
+            if (grp == 0) acc[e] += o;
         }
     }
-    return make_double2(ax, ay);
 }
 
 __device__ __forceinline__ double sum16(double v) {
@@ -125,51 +166,97 @@ __device__ __forceinline__ double max16(double v) {
     return v;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kSpThreads) sparse_rows_kernel(SpArgs a) {
+// Row epilogues on group 0's lanes (lane owns classes VW lane .. VW lane + VW - 1; L <= 16 lanes, so the
+// 16-lane butterflies cover them, other lanes contributing the identity).
+template <int MODE, int VW>
+__global__ void __launch_bounds__(kSpThreads, kSpBlocksPerSm) sparse_rows_kernel(SpArgs a) {
     if (a.guard && !*a.guard) return;
     __shared__ double red[kSpThreads / 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t warps_total = (int64_t)gridDim.x * (kSpThreads / 32);
-    const int K = a.K, KS = a.KS, L = KS >> 1, G = 32 / L;
-    const bool g0 = lane < L;  // group 0: classes c0 = 2 lane, c1 = 2 lane + 1
-    const int c0 = 2 * lane, c1 = 2 * lane + 1;
-    const bool on0 = g0 && c0 < K, on1 = g0 && c1 < K;
-    const double2* wt2 = reinterpret_cast<const double2*>(a.wt);
+    const int K = a.K, KS = a.KS, L = KS / VW, G = 32 / L;
+    const bool g0 = lane < L;
+    int cls[VW];
+    bool on[VW];
+#pragma unroll
+    for (int e = 0; e < VW; ++e) {
+        cls[e] = VW * lane + e;
+        on[e] = g0 && cls[e] < K;
+    }
     double acc_loss = 0.0;
     const bool blocked = a.nb > 1;
-    for (int64_t i = (int64_t)blockIdx.x * (kSpThreads / 32) + wib; i < a.n; i += warps_total) {
-        const int64_t q0 = blocked ? a.rblk[i * (a.nb + 1) + a.b] : a.indptr[i];
-        const int64_t q1 = blocked ? a.rblk[i * (a.nb + 1) + a.b + 1] : a.indptr[i + 1];
-        double2 lg = gather_segment(a.indices, a.vals, q0, q1, wt2, L, G, lane);
+    // segment bounds of row i (block b of the column blocks when blocked)
+    auto bounds = [&](int64_t i, int64_t& q0, int64_t& q1) {
+        const int64_t* src = blocked ? a.rblk + i * (a.nb + 1) + a.b : a.indptr + i;
+        q0 = src[0];
+        q1 = src[1];
+    };
+    int64_t i = (int64_t)blockIdx.x * (kSpThreads / 32) + wib;
+    int64_t q0 = 0, q1 = 0, nq0 = 0, nq1 = 0;
+    if (i < a.n) bounds(i, q0, q1);
+    for (; i < a.n; i += warps_total, q0 = nq0, q1 = nq1) {
+        // software pipeline: the next row's bounds are loaded (and its segment bulk-prefetched into L2)
+        // while this row is gathered
+        nq0 = 0;
+        nq1 = 0;
+        if (i + warps_total < a.n) {
+            bounds(i + warps_total, nq0, nq1);
+            if (lane == 0) prefetch_segment(a.indices, a.vals, nq0, nq1);
+        }
+        double lg[VW];
+        gather_segment<VW>(a.indices, a.vals, q0, q1, a.wt, KS, L, G, lane, lg);
         if (blocked) {  // logits = ((block 0 + block 1) + ...) + last block, in block order
-            double2* ls = reinterpret_cast<double2*>(a.lsum + i * KS) + lane;
+            double* ls = a.lsum + i * KS + VW * lane;
             if (a.b > 0 && g0) {
-                const double2 prev = *ls;
-                lg = make_double2(prev.x + lg.x, prev.y + lg.y);
+#pragma unroll
+                for (int e = 0; e < VW; ++e) lg[e] = ls[e] + lg[e];
             }
             if (a.b < a.nb - 1) {
-                if (g0) *ls = lg;
+                if (g0) {
+#pragma unroll
+                    for (int e = 0; e < VW; ++e) ls[e] = lg[e];
+                }
                 continue;
             }
         }
         const int b = a.labels[i];
         if (MODE == kModeLp) {
-            if (on0) a.Lp[i * K + c0] = lg.x;
-            if (on1) a.Lp[i * K + c1] = lg.y;
+#pragma unroll
+            for (int e = 0; e < VW; ++e)
+                if (on[e]) a.Lp[i * K + cls[e]] = lg[e];
         } else if (MODE == kModeHv) {  // U = V o P - P o rowsum(V o P)
-            const double p0 = on0 ? a.Pin[i * K + c0] : 0.0, p1 = on1 ? a.Pin[i * K + c1] : 0.0;
-            const double e0 = lg.x * p0, e1 = lg.y * p1;
-            const double rs = sum16(g0 ? e0 + e1 : 0.0);
-            if (g0) reinterpret_cast<double2*>(a.U + i * KS)[lane] = make_double2(e0 - p0 * rs, e1 - p1 * rs);
+            double pe[VW], ee[VW], es = 0.0;
+#pragma unroll
+            for (int e = 0; e < VW; ++e) {
+                pe[e] = on[e] ? a.Pin[i * K + cls[e]] : 0.0;
+                ee[e] = lg[e] * pe[e];
+                es += ee[e];
+            }
+            const double rs = sum16(g0 ? es : 0.0);
+            if (g0) {
+                double* u = a.U + i * KS + VW * lane;
+#pragma unroll
+                for (int e = 0; e < VW; ++e) u[e] = ee[e] - pe[e] * rs;
+            }
         } else {  // stable softmax (src/softmax.cpp:51-63)
-            double m = max16(fmax(on0 ? lg.x : -INFINITY, on1 ? lg.y : -INFINITY));
+            double mx = -INFINITY;
+#pragma unroll
+            for (int e = 0; e < VW; ++e) mx = fmax(mx, on[e] ? lg[e] : -INFINITY);
+            double m = max16(mx);
             m = m > 0.0 ? m : 0.0;
-            const double e0 = on0 ? exp(lg.x - m) : 0.0, e1 = on1 ? exp(lg.y - m) : 0.0;
-            const double alpha = exp(-m) + sum16(e0 + e1);
-            const double lbx = __shfl_sync(0xffffffffu, lg.x, ((b - 1) >> 1) & 31);
-            const double lby = __shfl_sync(0xffffffffu, lg.y, ((b - 1) >> 1) & 31);
-            const double lb = ((b - 1) & 1) ? lby : lbx;
+            double ex[VW], es = 0.0;
+#pragma unroll
+            for (int e = 0; e < VW; ++e) {
+                ex[e] = on[e] ? exp(lg[e] - m) : 0.0;
+                es += ex[e];
+            }
+            const double alpha = exp(-m) + sum16(es);
+            double lb = 0.0;
+#pragma unroll
+            for (int e = 0; e < VW; ++e) {
+                const double t = __shfl_sync(0xffffffffu, lg[e], ((b - 1) / VW) & 31);
+                if ((b - 1) % VW == e) lb = t;
+            }
             if (MODE == kModeCache || MODE == kModeValue) {
                 if (lane == 0) acc_loss += (m + log(alpha)) - (b <= K ? lb : 0.0);  // src/softmax.cpp:65-78
                 if (MODE == kModeCache) {
@@ -177,25 +264,30 @@ __global__ void __launch_bounds__(kSpThreads) sparse_rows_kernel(SpArgs a) {
                         a.rowM[i] = m;
                         a.rowA[i] = alpha;
                     }
-                    const double pc0 = e0 / alpha, pc1 = e1 / alpha;
-                    if (on0) {
-                        a.L0[i * K + c0] = lg.x;
-                        a.P[i * K + c0] = pc0;
+                    double* u = a.U + i * KS + VW * lane;
+#pragma unroll
+                    for (int e = 0; e < VW; ++e) {
+                        const double pc = ex[e] / alpha;
+                        if (on[e]) {
+                            a.L0[i * K + cls[e]] = lg[e];
+                            a.P[i * K + cls[e]] = pc;
+                        }
+                        // coeff = P - onehot(label) (src/softmax.cpp:86-90); padded classes 0
+                        if (g0) u[e] = on[e] ? pc - (cls[e] == b - 1 ? 1.0 : 0.0) : 0.0;
                     }
-                    if (on1) {
-                        a.L0[i * K + c1] = lg.y;
-                        a.P[i * K + c1] = pc1;
-                    }
-                    // coeff = P - onehot(label) (src/softmax.cpp:86-90); padded classes 0
-                    if (g0)
-                        reinterpret_cast<double2*>(a.U + i * KS)[lane] =
-                            make_double2(on0 ? pc0 - (c0 == b - 1 ? 1.0 : 0.0) : 0.0,
-                                         on1 ? pc1 - (c1 == b - 1 ? 1.0 : 0.0) : 0.0);
                 }
             } else {  // kModePredict: first class with P == max; class C only if strictly greater
-                const double pc0 = on0 ? e0 / alpha : -INFINITY, pc1 = on1 ? e1 / alpha : -INFINITY;
-                const double best = max16(fmax(pc0, pc1));
-                int first = (pc0 == best && on0) ? c0 : ((pc1 == best && on1) ? c1 : (1 << 20));
+                double pc[VW], pm = -INFINITY;
+#pragma unroll
+                for (int e = 0; e < VW; ++e) {
+                    pc[e] = on[e] ? ex[e] / alpha : -INFINITY;
+                    pm = fmax(pm, pc[e]);
+                }
+                const double best = max16(pm);
+                int first = 1 << 20;
+#pragma unroll
+                for (int e = VW - 1; e >= 0; --e)
+                    if (on[e] && pc[e] == best) first = cls[e];
 #pragma unroll
                 for (int o = 8; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
                 if (lane == 0) {
@@ -221,7 +313,8 @@ __global__ void __launch_bounds__(kSpThreads) sparse_rows_kernel(SpArgs a) {
 
 // X^T U through the CSC copy, one warp per column (nonzero groups as in the rows pass); fused
 // ridge / augmentation shifts and <out, dotvec> partials.
-__global__ void __launch_bounds__(kSpThreads) sparse_cols_kernel(
+template <int VW>
+__global__ void __launch_bounds__(kSpThreads, kSpBlocksPerSm) sparse_cols_kernel(
     const int64_t* __restrict__ cptr, const int32_t* __restrict__ crow, const double* __restrict__ cval, int64_t p,
     int K, int KS, const double* __restrict__ U, const double* __restrict__ vin, const DevParams* prm, int kind,
     double* __restrict__ out, const double* __restrict__ dotvec, double* blk_slot, unsigned long long* ctr,
@@ -230,22 +323,31 @@ __global__ void __launch_bounds__(kSpThreads) sparse_cols_kernel(
     if (ctr && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(ctr, 1ULL);
     __shared__ double red[32];
     const int lane = threadIdx.x & 31;
-    const int L = KS >> 1, G = 32 / L;
-    const int c0 = 2 * lane, c1 = 2 * lane + 1;
-    const bool on0 = lane < L && c0 < K, on1 = lane < L && c1 < K;
+    const int L = KS / VW, G = 32 / L;
     const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x / 32);
     const double lam = prm->lambda;
     const bool aug = kind == kXtuHv && prm->augmented;
     const double rho = prm->rho;
-    const double2* u2 = reinterpret_cast<const double2*>(U);
     double dacc = 0.0;
-    for (int64_t j = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); j < p; j += warps_total) {
-        const double2 acc = gather_segment(crow, cval, cptr[j], cptr[j + 1], u2, L, G, lane);
+    int64_t j = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    int64_t q0 = j < p ? cptr[j] : 0, q1 = j < p ? cptr[j + 1] : 0, nq0 = 0, nq1 = 0;
+    for (; j < p; j += warps_total, q0 = nq0, q1 = nq1) {
+        // software pipeline: the next column's bounds and L2 prefetch while this column is gathered
+        nq0 = 0;
+        nq1 = 0;
+        if (j + warps_total < p) {
+            nq0 = cptr[j + warps_total];
+            nq1 = cptr[j + warps_total + 1];
+            if (lane == 0) prefetch_segment(crow, cval, nq0, nq1);
+        }
+        double acc[VW];
+        gather_segment<VW>(crow, cval, q0, q1, U, KS, L, G, lane, acc);
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            if (e == 0 ? !on0 : !on1) continue;
-            const int64_t o = (int64_t)(e == 0 ? c0 : c1) * p + j;
-            double s = e == 0 ? acc.x : acc.y;
+        for (int e = 0; e < VW; ++e) {
+            const int c = VW * lane + e;
+            if (lane >= L || c >= K) continue;
+            const int64_t o = (int64_t)c * p + j;
+            double s = acc[e];
             if (lam > 0.0) s = s + lam * vin[o];
             if (aug) s = s + rho * vin[o];
             out[o] = s;
@@ -258,11 +360,27 @@ __global__ void __launch_bounds__(kSpThreads) sparse_cols_kernel(
     }
 }
 
+template <int VW>
+void launch_rows(PassMode mode, int grid, cudaStream_t st, const SpArgs& a) {
+    switch (mode) {
+        case kModeCache: sparse_rows_kernel<kModeCache, VW><<<grid, kSpThreads, 0, st>>>(a); break;
+        case kModeHv: sparse_rows_kernel<kModeHv, VW><<<grid, kSpThreads, 0, st>>>(a); break;
+        case kModeLp: sparse_rows_kernel<kModeLp, VW><<<grid, kSpThreads, 0, st>>>(a); break;
+        case kModeValue: sparse_rows_kernel<kModeValue, VW><<<grid, kSpThreads, 0, st>>>(a); break;
+        case kModePredict: sparse_rows_kernel<kModePredict, VW><<<grid, kSpThreads, 0, st>>>(a); break;
+    }
+}
+
 }  // namespace
 
 bool sparse_lanes_supported(const Shard& s) { return s.sparse && s.K <= 32 && s.wt; }
 
-int sparse_class_stride(int K) { return (K + 1) & ~1; }
+// K rounded up to a multiple of 4 (32-byte words) when that adds no padding over rounding to even
+// (K mod 4 in {0, 3}: K = 19 -> 20), else to even (16-byte words).
+int sparse_class_stride(int K) {
+    const int k4 = (K + 3) & ~3, k2 = (K + 1) & ~1;
+    return k4 == k2 ? k4 : k2;
+}
 
 void sparse_rows_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
     cudaStream_t st = s.ctx->stream;
@@ -291,20 +409,17 @@ void sparse_rows_pass(Shard& s, PassMode mode, const double* W, const int32_t* g
     a.blk = s.blk;
     a.guard = guard;
     const int grid = (int)std::max<int64_t>(
-        1, std::min<int64_t>((s.n + 7) / 8, std::min<int64_t>(kBlockPartials, 8LL * s.ctx->num_sms)));
+        1, std::min<int64_t>((s.n + 7) / 8, std::min<int64_t>(kBlockPartials, (int64_t)kSpBlocksPerSm * s.ctx->num_sms)));
     s.rows_grid = grid;
     a.nb = s.nblk;
     a.rblk = s.rblk;
     a.lsum = s.lsum;
     for (int b = 0; b < s.nblk; ++b) {  // one launch per column block (its weights stay L2-resident)
         a.b = b;
-        switch (mode) {
-            case kModeCache: sparse_rows_kernel<kModeCache><<<grid, kSpThreads, 0, st>>>(a); break;
-            case kModeHv: sparse_rows_kernel<kModeHv><<<grid, kSpThreads, 0, st>>>(a); break;
-            case kModeLp: sparse_rows_kernel<kModeLp><<<grid, kSpThreads, 0, st>>>(a); break;
-            case kModeValue: sparse_rows_kernel<kModeValue><<<grid, kSpThreads, 0, st>>>(a); break;
-            case kModePredict: sparse_rows_kernel<kModePredict><<<grid, kSpThreads, 0, st>>>(a); break;
-        }
+        if (KS % 4 == 0)
+            launch_rows<4>(mode, grid, st, a);
+        else
+            launch_rows<2>(mode, grid, st, a);
         NADMM_LAUNCH_CHECK();
     }
     s.ctx->stats.kernel_launches += 1 + s.nblk;
@@ -314,10 +429,12 @@ void sparse_rows_pass(Shard& s, PassMode mode, const double* W, const int32_t* g
 int sparse_cols_pass(Shard& s, XtuKind kind, const double* vin, double* out, const double* dotvec, int dot_slot,
                      const int32_t* guard) {
     const int grid = (int)std::max<int64_t>(
-        1, std::min<int64_t>((s.p + 7) / 8, std::min<int64_t>(kBlockPartials, 8LL * s.ctx->num_sms)));
-    sparse_cols_kernel<<<grid, kSpThreads, 0, s.ctx->stream>>>(
-        s.cptr, s.crow, s.cval, s.p, s.K, sparse_class_stride(s.K), s.U, vin, s.prm, kind, out, dotvec,
-        s.blk + (int64_t)dot_slot * kBlockPartials, kind == kXtuHv ? s.ctx->dctr : nullptr, guard);
+        1, std::min<int64_t>((s.p + 7) / 8, std::min<int64_t>(kBlockPartials, (int64_t)kSpBlocksPerSm * s.ctx->num_sms)));
+    const int KS = sparse_class_stride(s.K);
+    auto kern = KS % 4 == 0 ? sparse_cols_kernel<4> : sparse_cols_kernel<2>;
+    kern<<<grid, kSpThreads, 0, s.ctx->stream>>>(s.cptr, s.crow, s.cval, s.p, s.K, KS, s.U, vin, s.prm, kind, out,
+                                                 dotvec, s.blk + (int64_t)dot_slot * kBlockPartials,
+                                                 kind == kXtuHv ? s.ctx->dctr : nullptr, guard);
     NADMM_LAUNCH_CHECK();
     s.ctx->stats.kernel_launches++;
     s.ctx->stats.data_passes++;

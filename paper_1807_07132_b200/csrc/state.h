@@ -256,7 +256,7 @@ int op_hv_split(Shard& s, const double* v, double* out, const double* dotvec, in
 
 // ---- class-per-lane sparse passes (kernels_sparse.cu): CSR shards with C - 1 <= 32 ----
 bool sparse_lanes_supported(const Shard& s);
-int sparse_class_stride(int K);  // padded class stride of the gathered tables (K rounded up to even)
+int sparse_class_stride(int K);  // padded class stride of the gathered tables (K rounded up to 4 or to even)
 void sparse_rows_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard);
 int sparse_cols_pass(Shard& s, XtuKind kind, const double* vin, double* out, const double* dotvec, int dot_slot,
                      const int32_t* guard);
