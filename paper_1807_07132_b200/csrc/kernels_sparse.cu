@@ -8,13 +8,16 @@
 //     (sparse_class_stride), so a nonzero's K values are whole aligned words of VW doubles: 32-byte
 //     words (sm_100 256-bit loads, VW = 4) when KS is a multiple of 4, else 16-byte double2 words
 //     (K = 19: KS = 20, 160 B = 5 whole sectors = 5 lanes x 32 B);
-//   * a warp owns a row (rows pass) or a column (columns pass); its lanes form G = 32 / (KS/VW) groups,
-//     each group gathers one nonzero's words, so G nonzeros are in flight per warp instruction (K = 19:
-//     6 nonzeros, 30 of 32 lanes busy) and sp_unroll instructions are issued before their FMAs;
+//   * rows pass: a warp owns a row; its lanes form G = 32 / (KS/VW) groups, each group gathers one
+//     nonzero's words, so G nonzeros are in flight per warp instruction (K = 19: 6 nonzeros, 30 of 32
+//     lanes busy) and sp_unroll instructions are issued before their FMAs; group partial sums are
+//     folded into group 0 by shuffles and the row epilogue (U / softmax cache / loss / argmax) runs on
+//     group 0's lanes with 16-lane butterfly reductions;
+//   * columns pass (short CSC columns): each lane group owns a column and sums it sequentially -- no
+//     fold, and one column's latency chain is shared by the warp's G columns;
 //   * each lane loads its nonzeros' CSR / CSC entries itself (one broadcast request per group; no
-//     shuffles in the gather loop), and the warp's next segment is bulk-prefetched into L2;
-//   * group partial sums are folded into group 0 by shuffles; the row epilogue (U / softmax cache /
-//     loss / argmax) runs on group 0's lanes with 16-lane butterfly reductions.
+//     shuffles in the gather loop), and the next segment is bulk-prefetched into L2;
+//   * grids are exactly one resident wave (4 blocks of 256 threads per SM).
 // When the transposed weights exceed an L2-sized budget the rows pass runs once per column block
 // (running logits in `lsum` between blocks) so each block's weights stay L2-resident.
 //
@@ -151,6 +154,42 @@ __device__ __forceinline__ void gather_segment(const int32_t* __restrict__ idx, 
             const double o = __shfl_sync(0xffffffffu, acc[e], (sub + g * L) & 31);
             if (grp == 0) acc[e] += o;
         }
+    }
+}
+
+// Gathered dot products of one CSR row / CSC column segment [q0, q1) by one lane group: lane `sub` of the
+// group accumulates sum_k v_k * tab[idx_k][VW sub .. VW sub + VW - 1] over the segment's nonzeros in
+// ascending order (tb = tab + VW sub). Each lane loads its nonzeros' index and value itself (the group's
+// lanes read the same address: one broadcast request), UNR gathers in flight per lane, and slots past the
+// segment re-read its last nonzero with weight 0 (branch-free tail). The earlier form -- one warp per
+// segment, 32 entries per chunk broadcast by shuffles -- ran the same gathers at half the rate
+// (tools/microbench/gather_bw.cu: 6.9 vs 14.1 TB/s of gathered rows). Used by the columns pass (62-entry
+// CSC columns: one column per group, no cross-group fold); the rows pass keeps one warp per row
+// (gather_segment: 650-entry rows, where a group per row measured slower, 0.32 vs 0.285 ms per block).
+template <int VW>
+__device__ __forceinline__ void group_gather(const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                             int64_t q0, int64_t q1, const double* __restrict__ tb, int KS,
+                                             double (&acc)[VW]) {
+    constexpr int UNR = sp_unroll<VW>();
+#pragma unroll
+    for (int e = 0; e < VW; ++e) acc[e] = 0.0;
+    for (int64_t k = q0; k < q1; k += UNR) {
+        int jj[UNR];
+        double v[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int64_t kk = k + u < q1 ? k + u : q1 - 1;
+            jj[u] = __ldg(idx + kk);
+            const double x = __ldg(val + kk);
+            v[u] = k + u < q1 ? x : 0.0;
+        }
+        double w[UNR][VW];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) ldg_word<VW>(tb + (int64_t)jj[u] * KS, w[u]);
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int e = 0; e < VW; ++e) acc[e] += v[u] * w[u][e];
     }
 }
 
@@ -311,8 +350,10 @@ __global__ void __launch_bounds__(kSpThreads, kSpBlocksPerSm) sparse_rows_kernel
     }
 }
 
-// X^T U through the CSC copy, one warp per column (nonzero groups as in the rows pass); fused
-// ridge / augmentation shifts and <out, dotvec> partials.
+// X^T U through the CSC copy, one lane group per column: a warp's G groups (L = KS / VW lanes each) own
+// G consecutive columns and each sums its column's nonzeros sequentially in CSC (ascending row) order,
+// so there is no cross-group fold and a column's latency chain (bounds -> entries -> gathers -> store) is
+// shared by G columns; fused ridge / augmentation shifts and <out, dotvec> partials.
 template <int VW>
 __global__ void __launch_bounds__(kSpThreads, kSpBlocksPerSm) sparse_cols_kernel(
     const int64_t* __restrict__ cptr, const int32_t* __restrict__ crow, const double* __restrict__ cval, int64_t p,
@@ -324,28 +365,27 @@ __global__ void __launch_bounds__(kSpThreads, kSpBlocksPerSm) sparse_cols_kernel
     __shared__ double red[32];
     const int lane = threadIdx.x & 31;
     const int L = KS / VW, G = 32 / L;
-    const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x / 32);
+    const int grp = lane / L, sub = lane - grp * L;
+    const double* __restrict__ tb = U + sub * VW;
+    const int64_t step = (int64_t)gridDim.x * (blockDim.x / 32) * G;
     const double lam = prm->lambda;
     const bool aug = kind == kXtuHv && prm->augmented;
     const double rho = prm->rho;
     double dacc = 0.0;
-    int64_t j = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    int64_t q0 = j < p ? cptr[j] : 0, q1 = j < p ? cptr[j + 1] : 0, nq0 = 0, nq1 = 0;
-    for (; j < p; j += warps_total, q0 = nq0, q1 = nq1) {
-        // software pipeline: the next column's bounds and L2 prefetch while this column is gathered
-        nq0 = 0;
-        nq1 = 0;
-        if (j + warps_total < p) {
-            nq0 = cptr[j + warps_total];
-            nq1 = cptr[j + warps_total + 1];
-            if (lane == 0) prefetch_segment(crow, cval, nq0, nq1);
+    for (int64_t jb = ((int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * G; jb < p; jb += step) {
+        if (lane == 0 && jb + step < p) {  // the warp's next G columns are one contiguous CSC range
+            const int64_t je = jb + step + G < p ? jb + step + G : p;
+            prefetch_segment(crow, cval, cptr[jb + step], cptr[je]);
         }
+        const int64_t j = jb + grp;
+        const bool valid = grp < G && j < p;
+        const int64_t q0 = valid ? cptr[j] : 0, q1 = valid ? cptr[j + 1] : 0;
         double acc[VW];
-        gather_segment<VW>(crow, cval, q0, q1, U, KS, L, G, lane, acc);
+        group_gather<VW>(crow, cval, q0, q1, tb, KS, acc);
 #pragma unroll
         for (int e = 0; e < VW; ++e) {
-            const int c = VW * lane + e;
-            if (lane >= L || c >= K) continue;
+            const int c = VW * sub + e;
+            if (!valid || c >= K) continue;
             const int64_t o = (int64_t)c * p + j;
             double s = acc[e];
             if (lam > 0.0) s = s + lam * vin[o];
