@@ -121,7 +121,7 @@ struct SpArgs {
 template <int VW>
 __device__ __forceinline__ void gather_segment(const int32_t* __restrict__ idx, const double* __restrict__ val,
                                                int64_t q0, int64_t q1, const double* __restrict__ tab, int KS,
-                                               int L, int G, int lane, double (&acc)[VW]) {
+                                               int L, int G, int lane, double (&acc)[VW], int width = 32) {
     constexpr int UNR = sp_unroll<VW>();
     const int grp = lane / L, sub = lane - grp * L;
     const double* __restrict__ tb = tab + sub * VW;
@@ -151,7 +151,7 @@ __device__ __forceinline__ void gather_segment(const int32_t* __restrict__ idx, 
     for (int g = 1; g < G; ++g) {
 #pragma unroll
         for (int e = 0; e < VW; ++e) {
-            const double o = __shfl_sync(0xffffffffu, acc[e], (sub + g * L) & 31);
+            const double o = __shfl_sync(0xffffffffu, acc[e], (sub + g * L) & (width - 1), width);
             if (grp == 0) acc[e] += o;
         }
     }
@@ -207,13 +207,17 @@ __device__ __forceinline__ double max16(double v) {
 
 // Row epilogues on group 0's lanes (lane owns classes VW lane .. VW lane + VW - 1; L <= 16 lanes, so the
 // 16-lane butterflies cover them, other lanes contributing the identity).
-template <int MODE, int VW>
+// R rows per warp (R = 2: each half-warp owns a row, G = 16 / L groups per row -- half the fold steps
+// and two rows' latency chains per warp; the 16-lane butterflies of the epilogue stay inside a half).
+template <int MODE, int VW, int R>
 __global__ void __launch_bounds__(kSpThreads, kSpBlocksPerSm) sparse_rows_kernel(SpArgs a) {
     if (a.guard && !*a.guard) return;
     __shared__ double red[kSpThreads / 32];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t warps_total = (int64_t)gridDim.x * (kSpThreads / 32);
-    const int K = a.K, KS = a.KS, L = KS / VW, G = 32 / L;
+    constexpr int W = 32 / R;  // lanes per row
+    const int wl = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int half = wl / W, lane = wl - half * W;  // lane within the row's lanes
+    const int64_t rows_step = (int64_t)gridDim.x * (kSpThreads / 32) * R;
+    const int K = a.K, KS = a.KS, L = KS / VW, G = W / L;
     const bool g0 = lane < L;
     int cls[VW];
     bool on[VW];
@@ -226,53 +230,61 @@ __global__ void __launch_bounds__(kSpThreads, kSpBlocksPerSm) sparse_rows_kernel
     const bool blocked = a.nb > 1;
     // segment bounds of row i (block b of the column blocks when blocked)
     auto bounds = [&](int64_t i, int64_t& q0, int64_t& q1) {
+        if (i >= a.n) {
+            q0 = q1 = 0;
+            return;
+        }
         const int64_t* src = blocked ? a.rblk + i * (a.nb + 1) + a.b : a.indptr + i;
         q0 = src[0];
         q1 = src[1];
     };
-    int64_t i = (int64_t)blockIdx.x * (kSpThreads / 32) + wib;
+    // every lane of the warp stays in the loop (the fold shuffles use the full mask); a half past the
+    // last row gathers an empty segment and stores nothing
+    int64_t ib = ((int64_t)blockIdx.x * (kSpThreads / 32) + wib) * R;
     int64_t q0 = 0, q1 = 0, nq0 = 0, nq1 = 0;
-    if (i < a.n) bounds(i, q0, q1);
-    for (; i < a.n; i += warps_total, q0 = nq0, q1 = nq1) {
+    bounds(ib + half, q0, q1);
+    for (; ib < a.n; ib += rows_step, q0 = nq0, q1 = nq1) {
+        const int64_t i = ib + half;
+        const bool valid = i < a.n;
         // software pipeline: the next row's bounds are loaded (and its segment bulk-prefetched into L2)
         // while this row is gathered
-        nq0 = 0;
-        nq1 = 0;
-        if (i + warps_total < a.n) {
-            bounds(i + warps_total, nq0, nq1);
-            if (lane == 0) prefetch_segment(a.indices, a.vals, nq0, nq1);
-        }
+        bounds(i + rows_step, nq0, nq1);
+        if (lane == 0 && nq1 > nq0) prefetch_segment(a.indices, a.vals, nq0, nq1);
         double lg[VW];
-        gather_segment<VW>(a.indices, a.vals, q0, q1, a.wt, KS, L, G, lane, lg);
+        gather_segment<VW>(a.indices, a.vals, q0, q1, a.wt, KS, L, G, lane, lg, W);
+        const bool gv = g0 && valid;
+        bool onv[VW];
+#pragma unroll
+        for (int e = 0; e < VW; ++e) onv[e] = on[e] && valid;
         if (blocked) {  // logits = ((block 0 + block 1) + ...) + last block, in block order
             double* ls = a.lsum + i * KS + VW * lane;
-            if (a.b > 0 && g0) {
+            if (a.b > 0 && gv) {
 #pragma unroll
                 for (int e = 0; e < VW; ++e) lg[e] = ls[e] + lg[e];
             }
             if (a.b < a.nb - 1) {
-                if (g0) {
+                if (gv) {
 #pragma unroll
                     for (int e = 0; e < VW; ++e) ls[e] = lg[e];
                 }
                 continue;
             }
         }
-        const int b = a.labels[i];
+        const int b = valid ? a.labels[i] : 1;
         if (MODE == kModeLp) {
 #pragma unroll
             for (int e = 0; e < VW; ++e)
-                if (on[e]) a.Lp[i * K + cls[e]] = lg[e];
+                if (onv[e]) a.Lp[i * K + cls[e]] = lg[e];
         } else if (MODE == kModeHv) {  // U = V o P - P o rowsum(V o P)
             double pe[VW], ee[VW], es = 0.0;
 #pragma unroll
             for (int e = 0; e < VW; ++e) {
-                pe[e] = on[e] ? a.Pin[i * K + cls[e]] : 0.0;
+                pe[e] = onv[e] ? a.Pin[i * K + cls[e]] : 0.0;
                 ee[e] = lg[e] * pe[e];
                 es += ee[e];
             }
-            const double rs = sum16(g0 ? es : 0.0);
-            if (g0) {
+            const double rs = sum16(gv ? es : 0.0);
+            if (gv) {
                 double* u = a.U + i * KS + VW * lane;
 #pragma unroll
                 for (int e = 0; e < VW; ++e) u[e] = ee[e] - pe[e] * rs;
@@ -280,26 +292,26 @@ __global__ void __launch_bounds__(kSpThreads, kSpBlocksPerSm) sparse_rows_kernel
         } else {  // stable softmax (src/softmax.cpp:51-63)
             double mx = -INFINITY;
 #pragma unroll
-            for (int e = 0; e < VW; ++e) mx = fmax(mx, on[e] ? lg[e] : -INFINITY);
+            for (int e = 0; e < VW; ++e) mx = fmax(mx, onv[e] ? lg[e] : -INFINITY);
             double m = max16(mx);
             m = m > 0.0 ? m : 0.0;
             double ex[VW], es = 0.0;
 #pragma unroll
             for (int e = 0; e < VW; ++e) {
-                ex[e] = on[e] ? exp(lg[e] - m) : 0.0;
+                ex[e] = onv[e] ? exp(lg[e] - m) : 0.0;
                 es += ex[e];
             }
             const double alpha = exp(-m) + sum16(es);
             double lb = 0.0;
 #pragma unroll
             for (int e = 0; e < VW; ++e) {
-                const double t = __shfl_sync(0xffffffffu, lg[e], ((b - 1) / VW) & 31);
+                const double t = __shfl_sync(0xffffffffu, lg[e], ((b - 1) / VW) & (W - 1), W);
                 if ((b - 1) % VW == e) lb = t;
             }
             if (MODE == kModeCache || MODE == kModeValue) {
-                if (lane == 0) acc_loss += (m + log(alpha)) - (b <= K ? lb : 0.0);  // src/softmax.cpp:65-78
+                if (lane == 0 && valid) acc_loss += (m + log(alpha)) - (b <= K ? lb : 0.0);  // src/softmax.cpp:65-78
                 if (MODE == kModeCache) {
-                    if (lane == 0) {
+                    if (lane == 0 && valid) {
                         a.rowM[i] = m;
                         a.rowA[i] = alpha;
                     }
@@ -307,29 +319,29 @@ __global__ void __launch_bounds__(kSpThreads, kSpBlocksPerSm) sparse_rows_kernel
 #pragma unroll
                     for (int e = 0; e < VW; ++e) {
                         const double pc = ex[e] / alpha;
-                        if (on[e]) {
+                        if (onv[e]) {
                             a.L0[i * K + cls[e]] = lg[e];
                             a.P[i * K + cls[e]] = pc;
                         }
                         // coeff = P - onehot(label) (src/softmax.cpp:86-90); padded classes 0
-                        if (g0) u[e] = on[e] ? pc - (cls[e] == b - 1 ? 1.0 : 0.0) : 0.0;
+                        if (gv) u[e] = onv[e] ? pc - (cls[e] == b - 1 ? 1.0 : 0.0) : 0.0;
                     }
                 }
             } else {  // kModePredict: first class with P == max; class C only if strictly greater
                 double pc[VW], pm = -INFINITY;
 #pragma unroll
                 for (int e = 0; e < VW; ++e) {
-                    pc[e] = on[e] ? ex[e] / alpha : -INFINITY;
+                    pc[e] = onv[e] ? ex[e] / alpha : -INFINITY;
                     pm = fmax(pm, pc[e]);
                 }
                 const double best = max16(pm);
                 int first = 1 << 20;
 #pragma unroll
                 for (int e = VW - 1; e >= 0; --e)
-                    if (on[e] && pc[e] == best) first = cls[e];
+                    if (onv[e] && pc[e] == best) first = cls[e];
 #pragma unroll
                 for (int o = 8; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
-                if (lane == 0) {
+                if (lane == 0 && valid) {
                     int arg = first + 1;
                     if (exp(-m) / alpha > best) arg = K + 1;
                     a.pred[i] = arg;
@@ -339,7 +351,10 @@ __global__ void __launch_bounds__(kSpThreads, kSpBlocksPerSm) sparse_rows_kernel
         }
     }
     if ((MODE == kModeCache || MODE == kModeValue || MODE == kModePredict) && (!blocked || a.b == a.nb - 1)) {
-        if (lane == 0) red[wib] = acc_loss;
+        // the rows' sums (on each row's lane 0), halves in order
+        const double ws = R == 2 ? __shfl_sync(0xffffffffu, acc_loss, 0) + __shfl_sync(0xffffffffu, acc_loss, 16)
+                                 : acc_loss;
+        if (wl == 0) red[wib] = ws;
         __syncthreads();
         if (threadIdx.x == 0) {
             double s = 0.0;
@@ -402,12 +417,13 @@ __global__ void __launch_bounds__(kSpThreads, kSpBlocksPerSm) sparse_cols_kernel
 
 template <int VW>
 void launch_rows(PassMode mode, int grid, cudaStream_t st, const SpArgs& a) {
+    constexpr int R = VW == 4 ? 2 : 1;  // VW = 4: L <= 8 lanes per nonzero, so a half-warp holds >= 2 groups
     switch (mode) {
-        case kModeCache: sparse_rows_kernel<kModeCache, VW><<<grid, kSpThreads, 0, st>>>(a); break;
-        case kModeHv: sparse_rows_kernel<kModeHv, VW><<<grid, kSpThreads, 0, st>>>(a); break;
-        case kModeLp: sparse_rows_kernel<kModeLp, VW><<<grid, kSpThreads, 0, st>>>(a); break;
-        case kModeValue: sparse_rows_kernel<kModeValue, VW><<<grid, kSpThreads, 0, st>>>(a); break;
-        case kModePredict: sparse_rows_kernel<kModePredict, VW><<<grid, kSpThreads, 0, st>>>(a); break;
+        case kModeCache: sparse_rows_kernel<kModeCache, VW, R><<<grid, kSpThreads, 0, st>>>(a); break;
+        case kModeHv: sparse_rows_kernel<kModeHv, VW, R><<<grid, kSpThreads, 0, st>>>(a); break;
+        case kModeLp: sparse_rows_kernel<kModeLp, VW, R><<<grid, kSpThreads, 0, st>>>(a); break;
+        case kModeValue: sparse_rows_kernel<kModeValue, VW, R><<<grid, kSpThreads, 0, st>>>(a); break;
+        case kModePredict: sparse_rows_kernel<kModePredict, VW, R><<<grid, kSpThreads, 0, st>>>(a); break;
     }
 }
 
