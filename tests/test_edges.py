@@ -66,6 +66,27 @@ def test_ragged_sparse_matches_oracle(nadmm, port, C):
     np.testing.assert_allclose(g[:, -7:], 1e-3 * w.reshape(C - 1, p)[:, -7:], rtol=1e-14, atol=0)
 
 
+@pytest.mark.parametrize("C", list(range(2, 34)))
+def test_sparse_every_class_count(nadmm, port, C):
+    """Every class count the CSR lane path takes (K = C - 1 <= 32): both word widths (32-byte words when
+    K rounds up to a multiple of 4 without extra padding, else 16-byte), one or two rows per warp, a
+    lane group per CSC column; odd n so the last warp's second row is past the end; ragged rows with
+    empty rows / columns (kernels_sparse.cu; src/dataset.cpp:69-85, src/softmax.cpp:51-139)."""
+    rng = np.random.default_rng(100 + C)
+    n, p = 37, 61
+    ip, ix, vv = ragged_csr(rng, n, p)
+    y = (np.arange(n) % C + 1).astype(np.int32)
+    ds = nadmm.Dataset.sparse(ip, ix, vv, y, C, p)
+    sh = oracle.Shard(labels=y, C_=C, csr=(ip, ix, vv), p=p)
+    w = rng.normal(size=sh.d) * 0.3
+    v = rng.normal(size=sh.d)
+    lw = port.loss(sh, w, 1e-3)
+    assert abs(nadmm.loss(ds, w, 1e-3) - lw) <= TOL * abs(lw)
+    assert rel(nadmm.gradient(ds, w, 1e-3), port.gradient(sh, w, 1e-3)) <= TOL
+    assert rel(nadmm.hessian_vec(ds, w, v, 1e-3), port.hessian_vec(sh, w, v, 1e-3)) <= TOL
+    np.testing.assert_array_equal(nadmm.predict(ds, w), port.predict(sh, w))
+
+
 def test_duplicate_entries_are_summed(nadmm):
     rng = np.random.default_rng(3)
     n, p, C = 50, 40, 5
