@@ -75,18 +75,21 @@ __device__ __forceinline__ void prefetch_segment(const int32_t* idx, const doubl
     prefetch_l2(val + q0, 8 * (q1 - q0));
 }
 
-// wt (p x KS, padded classes zero) = transpose of the block-major W (K x p): 32-column tiles through
-// shared memory so both the reads (along p) and the writes (32*KS contiguous doubles) are coalesced.
+// wt (p x KS, padded classes zero) = transpose of the block-major W (K x p): 64-column tiles through
+// shared memory so both the reads (KS rows of 512 contiguous bytes, KS/4 loads in flight per thread) and
+// the writes (64*KS contiguous doubles) are coalesced.
+constexpr int kTrCols = 64;
 __global__ void __launch_bounds__(256) transpose_w_kernel(const double* __restrict__ W, int64_t p, int K, int KS,
                                                           double* __restrict__ wt, const int32_t* guard) {
     if (guard && !*guard) return;
-    __shared__ double tile[32][33];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
-    for (int64_t j0 = (int64_t)blockIdx.x * 32; j0 < p; j0 += (int64_t)gridDim.x * 32) {
-        for (int c = ty; c < KS; c += 8) tile[c][tx] = (c < K && j0 + tx < p) ? W[(int64_t)c * p + j0 + tx] : 0.0;
+    __shared__ double tile[32][kTrCols + 1];
+    const int tx = threadIdx.x & (kTrCols - 1), ty = threadIdx.x / kTrCols;  // 4 rows of 64
+    for (int64_t j0 = (int64_t)blockIdx.x * kTrCols; j0 < p; j0 += (int64_t)gridDim.x * kTrCols) {
+        for (int c = ty; c < KS; c += 256 / kTrCols)
+            tile[c][tx] = (c < K && j0 + tx < p) ? __ldcs(W + (int64_t)c * p + j0 + tx) : 0.0;
         __syncthreads();
         const int64_t base = j0 * KS;
-        const int64_t total = (p - j0 < 32 ? p - j0 : 32) * KS;
+        const int64_t total = (p - j0 < kTrCols ? p - j0 : kTrCols) * KS;
         for (int q = threadIdx.x; q < total; q += 256) wt[base + q] = tile[q % KS][q / KS];
         __syncthreads();
     }
@@ -441,7 +444,7 @@ int sparse_class_stride(int K) {
 void sparse_rows_pass(Shard& s, PassMode mode, const double* W, const int32_t* guard) {
     cudaStream_t st = s.ctx->stream;
     const int KS = sparse_class_stride(s.K);
-    const int tg = (int)std::max<int64_t>(1, std::min<int64_t>((s.p + 31) / 32, 8LL * s.ctx->num_sms));
+    const int tg = (int)std::max<int64_t>(1, std::min<int64_t>((s.p + kTrCols - 1) / kTrCols, 8LL * s.ctx->num_sms));
     transpose_w_kernel<<<tg, 256, 0, st>>>(W, s.p, s.K, KS, s.wt, guard);
     NADMM_LAUNCH_CHECK();
     SpArgs a{};
