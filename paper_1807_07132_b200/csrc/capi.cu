@@ -418,12 +418,16 @@ nadmm_status nadmm_shard_csr(nadmm_ctx ctx, const int64_t* indptr, const int32_t
             rv = cv.data();
         }
         const int64_t nnz = rp[n];
-        // CSC copy (counting sort by column; rows ascending within a column)
+        // CSC copy (counting sort by column; rows ascending within a column). For the lane-group columns
+        // pass (C - 1 <= 32) every column is padded to a multiple of kCscQuad entries (row of its last
+        // entry, value 0) so a lane reads a quad of row indices / values with one 16-byte / 32-byte load.
+        const int64_t quad = C - 1 <= 32 ? kCscQuad : 1;
         std::vector<int64_t> colptr(p + 1, 0);
         for (int64_t k = 0; k < nnz; ++k) colptr[ri[k] + 1]++;
-        for (int64_t j = 0; j < p; ++j) colptr[j + 1] += colptr[j];
-        std::vector<int32_t> crow(nnz);
-        std::vector<double> cval(nnz);
+        for (int64_t j = 0; j < p; ++j) colptr[j + 1] = colptr[j] + (colptr[j + 1] + quad - 1) / quad * quad;
+        const int64_t cnnz = colptr[p];
+        std::vector<int32_t> crow(cnnz);
+        std::vector<double> cval(cnnz, 0.0);
         {
             std::vector<int64_t> pos(colptr.begin(), colptr.end() - 1);
             for (int64_t i = 0; i < n; ++i)
@@ -432,6 +436,8 @@ nadmm_status nadmm_shard_csr(nadmm_ctx ctx, const int64_t* indptr, const int32_t
                     crow[q] = (int32_t)i;
                     cval[q] = rv[k];
                 }
+            for (int64_t j = 0; j < p; ++j)
+                for (int64_t q = pos[j]; q < colptr[j + 1]; ++q) crow[q] = crow[pos[j] - 1];
         }
         std::unique_ptr<nadmm_shard_s> s(new nadmm_shard_s());
         s->ctx = ctx;
@@ -446,14 +452,14 @@ nadmm_status nadmm_shard_csr(nadmm_ctx ctx, const int64_t* indptr, const int32_t
         s->indices = dev_alloc<int32_t>(*s, nnz);
         s->vals = dev_alloc<double>(*s, nnz);
         s->cptr = dev_alloc<int64_t>(*s, p + 1);
-        s->crow = dev_alloc<int32_t>(*s, nnz);
-        s->cval = dev_alloc<double>(*s, nnz);
+        s->crow = dev_alloc<int32_t>(*s, cnnz);
+        s->cval = dev_alloc<double>(*s, cnnz);
         upload(s->indptr, rp, sizeof(int64_t) * (n + 1), ctx->stream);
         upload(s->indices, ri, sizeof(int32_t) * nnz, ctx->stream);
         upload(s->vals, rv, sizeof(double) * nnz, ctx->stream);
         upload(s->cptr, colptr.data(), sizeof(int64_t) * (p + 1), ctx->stream);
-        upload(s->crow, crow.data(), sizeof(int32_t) * nnz, ctx->stream);
-        upload(s->cval, cval.data(), sizeof(double) * nnz, ctx->stream);
+        upload(s->crow, crow.data(), sizeof(int32_t) * cnnz, ctx->stream);
+        upload(s->cval, cval.data(), sizeof(double) * cnnz, ctx->stream);
         s->labels = dev_alloc<int32_t>(*s, n + kRowPad);
         NADMM_CUDA(cudaMemsetAsync(s->labels, 0, sizeof(int32_t) * (n + kRowPad), ctx->stream));
         upload(s->labels, labels, sizeof(int32_t) * n, ctx->stream);

@@ -32,6 +32,7 @@ struct Error : std::runtime_error {
 
 constexpr int kMaxClasses = 128;   // C - 1 <= kMaxClasses on the SIMT paths
 constexpr int kRowPad = 32;        // extra rows allocated in row-indexed work buffers (tile over-read)
+constexpr int kCscQuad = 4;        // CSC columns of the lane-group path are padded to multiples of this
 constexpr int kBlockPartials = 1024;  // max blocks writing partials in one reduction slot
 
 // ---------------------------------------------------------------------------------------------

@@ -14,7 +14,8 @@
 //     folded into group 0 by shuffles and the row epilogue (U / softmax cache / loss / argmax) runs on
 //     group 0's lanes with 16-lane butterfly reductions;
 //   * columns pass (short CSC columns): each lane group owns a column and sums it sequentially -- no
-//     fold, and one column's latency chain is shared by the warp's G columns;
+//     fold, and one column's latency chain is shared by the warp's G columns; the CSC copy is padded to
+//     quads of entries, read with one 16-byte index load and one 32-byte value load per quad;
 //   * each lane loads its nonzeros' CSR / CSC entries itself (one broadcast request per group; no
 //     shuffles in the gather loop), and the next segment is bulk-prefetched into L2;
 //   * grids are exactly one resident wave (4 blocks of 256 threads per SM).
@@ -160,37 +161,33 @@ __device__ __forceinline__ void gather_segment(const int32_t* __restrict__ idx, 
     }
 }
 
-// Gathered dot products of one CSR row / CSC column segment [q0, q1) by one lane group: lane `sub` of the
-// group accumulates sum_k v_k * tab[idx_k][VW sub .. VW sub + VW - 1] over the segment's nonzeros in
-// ascending order (tb = tab + VW sub). Each lane loads its nonzeros' index and value itself (the group's
-// lanes read the same address: one broadcast request), UNR gathers in flight per lane, and slots past the
-// segment re-read its last nonzero with weight 0 (branch-free tail). The earlier form -- one warp per
-// segment, 32 entries per chunk broadcast by shuffles -- ran the same gathers at half the rate
-// (tools/microbench/gather_bw.cu: 6.9 vs 14.1 TB/s of gathered rows). Used by the columns pass (62-entry
-// CSC columns: one column per group, no cross-group fold); the rows pass keeps one warp per row
-// (gather_segment: 650-entry rows, where a group per row measured slower, 0.32 vs 0.285 ms per block).
+// Gathered dot products of one quad-padded CSC column [q0, q1) by one lane group (capi.cu pads every
+// column to kCscQuad entries with weight-0 copies of its last row): lane `sub` of the group accumulates
+// sum_k v_k * U[row_k][VW sub .. VW sub + VW - 1] over the column's entries in ascending order (tb = U +
+// VW sub); a lane reads a quad's 4 row indices with one 16-byte load and its 4 values with one 32-byte
+// load (the group's lanes read the same address: one broadcast request), then issues the 4 gathers.
+// No shuffles: the earlier form -- one warp per column, 32 entries per chunk broadcast by shuffles --
+// ran the same gathers at half the rate (tools/microbench/gather_bw.cu: 6.9 vs 14.1 TB/s of gathered
+// rows); per-entry scalar index / value loads instead of quads: columns pass 1.22 vs 1.11 ms at cfg4.
 template <int VW>
-__device__ __forceinline__ void group_gather(const int32_t* __restrict__ idx, const double* __restrict__ val,
-                                             int64_t q0, int64_t q1, const double* __restrict__ tb, int KS,
-                                             double (&acc)[VW]) {
-    constexpr int UNR = sp_unroll<VW>();
+__device__ __forceinline__ void group_gather_quads(const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                                   int64_t q0, int64_t q1, const double* __restrict__ tb, int KS,
+                                                   double (&acc)[VW]) {
+    static_assert(kCscQuad == 4, "quad loads");
 #pragma unroll
     for (int e = 0; e < VW; ++e) acc[e] = 0.0;
-    for (int64_t k = q0; k < q1; k += UNR) {
-        int jj[UNR];
-        double v[UNR];
+    for (int64_t k = q0; k < q1; k += 4) {
+        const int4 j4 = __ldg(reinterpret_cast<const int4*>(idx + k));
+        double v[4];
+        asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                     : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                     : "l"(val + k));
+        const int jj[4] = {j4.x, j4.y, j4.z, j4.w};
+        double w[4][VW];
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            const int64_t kk = k + u < q1 ? k + u : q1 - 1;
-            jj[u] = __ldg(idx + kk);
-            const double x = __ldg(val + kk);
-            v[u] = k + u < q1 ? x : 0.0;
-        }
-        double w[UNR][VW];
+        for (int u = 0; u < 4; ++u) ldg_word<VW>(tb + (int64_t)jj[u] * KS, w[u]);
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) ldg_word<VW>(tb + (int64_t)jj[u] * KS, w[u]);
-#pragma unroll
-        for (int u = 0; u < UNR; ++u)
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int e = 0; e < VW; ++e) acc[e] += v[u] * w[u][e];
     }
@@ -399,7 +396,7 @@ __global__ void __launch_bounds__(kSpThreads, kSpBlocksPerSm) sparse_cols_kernel
         const bool valid = grp < G && j < p;
         const int64_t q0 = valid ? cptr[j] : 0, q1 = valid ? cptr[j + 1] : 0;
         double acc[VW];
-        group_gather<VW>(crow, cval, q0, q1, tb, KS, acc);
+        group_gather_quads<VW>(crow, cval, q0, q1, tb, KS, acc);
 #pragma unroll
         for (int e = 0; e < VW; ++e) {
             const int c = VW * sub + e;
