@@ -448,28 +448,14 @@ nadmm_status nadmm_shard_csr(nadmm_ctx ctx, const int64_t* indptr, const int32_t
         s->d = (int64_t)s->K * p;
         s->sparse = true;
         s->nnz = nnz;
-        s->indptr = dev_alloc<int64_t>(*s, n + 1);
-        s->indices = dev_alloc<int32_t>(*s, nnz);
-        s->vals = dev_alloc<double>(*s, nnz);
-        s->cptr = dev_alloc<int64_t>(*s, p + 1);
-        s->crow = dev_alloc<int32_t>(*s, cnnz);
-        s->cval = dev_alloc<double>(*s, cnnz);
-        upload(s->indptr, rp, sizeof(int64_t) * (n + 1), ctx->stream);
-        upload(s->indices, ri, sizeof(int32_t) * nnz, ctx->stream);
-        upload(s->vals, rv, sizeof(double) * nnz, ctx->stream);
-        upload(s->cptr, colptr.data(), sizeof(int64_t) * (p + 1), ctx->stream);
-        upload(s->crow, crow.data(), sizeof(int32_t) * cnnz, ctx->stream);
-        upload(s->cval, cval.data(), sizeof(double) * cnnz, ctx->stream);
-        s->labels = dev_alloc<int32_t>(*s, n + kRowPad);
-        NADMM_CUDA(cudaMemsetAsync(s->labels, 0, sizeof(int32_t) * (n + kRowPad), ctx->stream));
-        upload(s->labels, labels, sizeof(int32_t) * n, ctx->stream);
         // column blocks for the rows pass: transposed weights of one block within ~48 MB of L2
         const int64_t wbytes = 8 * (int64_t)sparse_class_stride(C - 1) * p;
         int64_t kBlockBudget = int64_t(48) << 20;
         if (const char* e = getenv("NADMM_SPARSE_BLOCK_KB")) kBlockBudget = std::max<int64_t>(1, atoll(e)) << 10;
         std::vector<int64_t> rblk;
+        int nb = 1;
         if (C - 1 <= 32 && wbytes > kBlockBudget) {
-            const int nb = (int)std::min<int64_t>(64, (wbytes + kBlockBudget - 1) / kBlockBudget);
+            nb = (int)std::min<int64_t>(64, (wbytes + kBlockBudget - 1) / kBlockBudget);
             const int64_t width = (p + nb - 1) / nb;
             rblk.resize((size_t)n * (nb + 1));
             for (int64_t i = 0; i < n; ++i) {  // rows are canonical: columns ascending
@@ -481,6 +467,60 @@ nadmm_status nadmm_shard_csr(nadmm_ctx ctx, const int64_t* indptr, const int32_t
                 }
                 rblk[(size_t)i * (nb + 1) + nb] = rp[i + 1];
             }
+        }
+        // Lane-group rows pass (C - 1 <= 32): every row segment (one per column block) is padded to a
+        // multiple of kCscQuad entries (column of its last entry, value 0) so a lane reads a quad of
+        // indices / values with one 16-byte / 32-byte load; offsets become the padded indptr (one block)
+        // or the padded rblk. The generic CSR path (C - 1 > 32) keeps the canonical arrays.
+        std::vector<int64_t> pptr;
+        std::vector<int32_t> pidx;
+        std::vector<double> pval;
+        const int64_t* up_ptr = rp;
+        const int32_t* up_idx = ri;
+        const double* up_val = rv;
+        int64_t rnnz = nnz;
+        if (C - 1 <= 32) {
+            const int64_t segs = n * (int64_t)nb;
+            auto seg0 = [&](int64_t t) { return nb == 1 ? rp[t] : rblk[(size_t)(t / nb) * (nb + 1) + t % nb]; };
+            auto seg1 = [&](int64_t t) { return nb == 1 ? rp[t + 1] : rblk[(size_t)(t / nb) * (nb + 1) + t % nb + 1]; };
+            std::vector<int64_t> off((size_t)segs + 1, 0);
+            for (int64_t t = 0; t < segs; ++t)
+                off[t + 1] = off[t] + (seg1(t) - seg0(t) + kCscQuad - 1) / kCscQuad * kCscQuad;
+            rnnz = off[segs];
+            pidx.resize((size_t)rnnz);
+            pval.assign((size_t)rnnz, 0.0);
+            for (int64_t t = 0; t < segs; ++t) {
+                const int64_t a0 = seg0(t), len = seg1(t) - a0;
+                std::copy(ri + a0, ri + a0 + len, pidx.begin() + off[t]);
+                std::copy(rv + a0, rv + a0 + len, pval.begin() + off[t]);
+                for (int64_t q = off[t] + len; q < off[t + 1]; ++q) pidx[q] = ri[a0 + len - 1];
+            }
+            if (nb == 1) {
+                pptr.swap(off);
+                up_ptr = pptr.data();
+            } else {
+                for (int64_t i = 0; i < n; ++i)
+                    for (int b = 0; b <= nb; ++b) rblk[(size_t)i * (nb + 1) + b] = off[(size_t)i * nb + b];
+            }
+            up_idx = pidx.data();
+            up_val = pval.data();
+        }
+        s->indptr = dev_alloc<int64_t>(*s, n + 1);
+        s->indices = dev_alloc<int32_t>(*s, rnnz);
+        s->vals = dev_alloc<double>(*s, rnnz);
+        s->cptr = dev_alloc<int64_t>(*s, p + 1);
+        s->crow = dev_alloc<int32_t>(*s, cnnz);
+        s->cval = dev_alloc<double>(*s, cnnz);
+        upload(s->indptr, up_ptr, sizeof(int64_t) * (n + 1), ctx->stream);
+        upload(s->indices, up_idx, sizeof(int32_t) * rnnz, ctx->stream);
+        upload(s->vals, up_val, sizeof(double) * rnnz, ctx->stream);
+        upload(s->cptr, colptr.data(), sizeof(int64_t) * (p + 1), ctx->stream);
+        upload(s->crow, crow.data(), sizeof(int32_t) * cnnz, ctx->stream);
+        upload(s->cval, cval.data(), sizeof(double) * cnnz, ctx->stream);
+        s->labels = dev_alloc<int32_t>(*s, n + kRowPad);
+        NADMM_CUDA(cudaMemsetAsync(s->labels, 0, sizeof(int32_t) * (n + kRowPad), ctx->stream));
+        upload(s->labels, labels, sizeof(int32_t) * n, ctx->stream);
+        if (nb > 1) {
             s->nblk = nb;
             s->rblk = dev_alloc<int64_t>(*s, (int64_t)rblk.size());
             upload(s->rblk, rblk.data(), sizeof(int64_t) * rblk.size(), ctx->stream);

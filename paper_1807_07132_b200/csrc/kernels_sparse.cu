@@ -8,16 +8,17 @@
 //     (sparse_class_stride), so a nonzero's K values are whole aligned words of VW doubles: 32-byte
 //     words (sm_100 256-bit loads, VW = 4) when KS is a multiple of 4, else 16-byte double2 words
 //     (K = 19: KS = 20, 160 B = 5 whole sectors = 5 lanes x 32 B);
-//   * rows pass: a warp owns a row; its lanes form G = 32 / (KS/VW) groups, each group gathers one
-//     nonzero's words, so G nonzeros are in flight per warp instruction (K = 19: 6 nonzeros, 30 of 32
-//     lanes busy) and sp_unroll instructions are issued before their FMAs; group partial sums are
-//     folded into group 0 by shuffles and the row epilogue (U / softmax cache / loss / argmax) runs on
-//     group 0's lanes with 16-lane butterfly reductions;
+//   * rows pass: a half-warp owns a row (two rows per warp); its lanes form G = 16 / (KS/VW) groups,
+//     each group gathers one nonzero's words (K = 19: 3 groups per row, 30 of 32 lanes busy), each
+//     lane issuing a quad's 4 gathers before their FMAs; group partial sums are folded into group 0 by
+//     shuffles and the row epilogue (U / softmax cache / loss / argmax) runs on group 0's lanes with
+//     16-lane butterfly reductions inside the half;
 //   * columns pass (short CSC columns): each lane group owns a column and sums it sequentially -- no
-//     fold, and one column's latency chain is shared by the warp's G columns; the CSC copy is padded to
-//     quads of entries, read with one 16-byte index load and one 32-byte value load per quad;
-//   * each lane loads its nonzeros' CSR / CSC entries itself (one broadcast request per group; no
-//     shuffles in the gather loop), and the next segment is bulk-prefetched into L2;
+//     fold, and one column's latency chain is shared by the warp's G columns;
+//   * CSR row segments (per column block) and CSC columns are padded to quads of entries (weight-0
+//     copies of the last entry, capi.cu); each lane loads its quads itself with one 16-byte index and
+//     one 32-byte value load (one broadcast request per group; no shuffles in the gather loop), and the
+//     next segment is bulk-prefetched into L2;
 //   * grids are exactly one resident wave (4 blocks of 256 threads per SM).
 // When the transposed weights exceed an L2-sized budget the rows pass runs once per column block
 // (running logits in `lsum` between blocks) so each block's weights stay L2-resident.
@@ -39,11 +40,6 @@ constexpr int kSpThreads = 256;
 #define NADMM_SP_BPSM 4
 #endif
 constexpr int kSpBlocksPerSm = NADMM_SP_BPSM;
-
-// Gathers in flight per lane before their FMAs: 4 x 16-byte words (VW = 2) or 3 x 32-byte words (VW = 4;
-// 6 nonzeros per warp instruction at K = 19, so a 32-entry CSR chunk is exactly 6 instructions).
-template <int VW>
-constexpr int sp_unroll() { return VW == 4 ? 3 : 4; }
 
 // One lane's VW-double word of a gathered table row (read-only path). VW = 4 is the sm_100 256-bit
 // load (LDG.E.ENL2.256): a nonzero's 160-byte K = 19 row is 5 lanes x 32 B, half the requests of
@@ -115,40 +111,36 @@ struct SpArgs {
     double* lsum;  // n x KS
 };
 
-// Gathered dot products of one segment [q0, q1) of a CSR row / CSC column: lane (group g, slot s)
-// accumulates sum_k v_k * tab[idx_k][VW s .. VW s + VW - 1] over the segment's nonzeros k = q0 + g (mod G)
-// in ascending order; group g's partial is folded into group 0 (groups in ascending order). Valid on
-// group 0's lanes. Each lane loads its nonzeros' index and value itself (a group's lanes read the same
-// address: one broadcast request, L1-resident after the first touch) -- no shuffles in the loop: the
-// earlier form (32 entries per chunk broadcast by shuffles, three SHFL per nonzero group) ran the same
-// gathers at half the rate (tools/microbench/gather_bw.cu: 6.9 vs 14.1 TB/s of gathered rows).
+// Gathered dot products of one quad-padded CSR row segment [q0, q1) (capi.cu pads every row segment to
+// kCscQuad entries with weight-0 copies of its last column) by the lanes of one row: lane (group g,
+// slot s) accumulates sum_k v_k * tab[idx_k][VW s .. VW s + VW - 1] over the quads g, g + G, g + 2G, ...
+// of the segment, in order, reading each quad's 4 indices / 4 values with one 16-byte / one 32-byte
+// load (the group's lanes read the same address: one broadcast request) and then issuing its 4
+// gathers; group g's partial is folded into group 0 (groups in ascending order). Valid on group 0's
+// lanes. No shuffles in the loop: the earlier form (32 entries per chunk broadcast by shuffles) ran the
+// same gathers at half the rate (tools/microbench/gather_bw.cu: 6.9 vs 14.1 TB/s of gathered rows).
 template <int VW>
 __device__ __forceinline__ void gather_segment(const int32_t* __restrict__ idx, const double* __restrict__ val,
                                                int64_t q0, int64_t q1, const double* __restrict__ tab, int KS,
                                                int L, int G, int lane, double (&acc)[VW], int width = 32) {
-    constexpr int UNR = sp_unroll<VW>();
+    static_assert(kCscQuad == 4, "quad loads");
     const int grp = lane / L, sub = lane - grp * L;
     const double* __restrict__ tb = tab + sub * VW;
 #pragma unroll
     for (int e = 0; e < VW; ++e) acc[e] = 0.0;
-    if (grp >= G) q1 = q0;  // idle lanes (32 mod L) skip the loop
-    for (int64_t t = q0 + grp; t < q1; t += (int64_t)G * UNR) {
-        // branch-free tail: slots past the segment re-read its last nonzero with weight 0
-        int jj[UNR];
-        double v[UNR];
+    if (grp >= G) q1 = q0;  // idle lanes (width mod L) skip the loop
+    for (int64_t k = q0 + 4 * grp; k < q1; k += 4 * (int64_t)G) {
+        const int4 j4 = __ldg(reinterpret_cast<const int4*>(idx + k));
+        double v[4];
+        asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                     : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                     : "l"(val + k));
+        const int jj[4] = {j4.x, j4.y, j4.z, j4.w};
+        double w[4][VW];
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            const int64_t k = t + (int64_t)u * G;
-            const int64_t kk = k < q1 ? k : q1 - 1;
-            jj[u] = __ldg(idx + kk);
-            const double x = __ldg(val + kk);
-            v[u] = k < q1 ? x : 0.0;
-        }
-        double w[UNR][VW];
+        for (int u = 0; u < 4; ++u) ldg_word<VW>(tb + (int64_t)jj[u] * KS, w[u]);
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) ldg_word<VW>(tb + (int64_t)jj[u] * KS, w[u]);
-#pragma unroll
-        for (int u = 0; u < UNR; ++u)
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int e = 0; e < VW; ++e) acc[e] += v[u] * w[u][e];
     }
