@@ -129,12 +129,17 @@ __device__ __forceinline__ void gather_segment(const int32_t* __restrict__ idx, 
 #pragma unroll
     for (int e = 0; e < VW; ++e) acc[e] = 0.0;
     if (grp >= G) q1 = q0;  // idle lanes (width mod L) skip the loop
+    uint64_t pol;  // the CSR stream is read once: L2 evict_first, so the weight block stays resident
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     for (int64_t k = q0 + 4 * grp; k < q1; k += 4 * (int64_t)G) {
-        const int4 j4 = __ldg(reinterpret_cast<const int4*>(idx + k));
+        int4 j4;
+        asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+                     : "=r"(j4.x), "=r"(j4.y), "=r"(j4.z), "=r"(j4.w)
+                     : "l"(idx + k), "l"(pol));
         double v[4];
-        asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+        asm volatile("ld.global.nc.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
                      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
-                     : "l"(val + k));
+                     : "l"(val + k), "l"(pol));
         const int jj[4] = {j4.x, j4.y, j4.z, j4.w};
         double w[4][VW];
 #pragma unroll
